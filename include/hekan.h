@@ -1,0 +1,149 @@
+/*
+ * hekan.h — C ABI of the B200 RNS-CKKS engine behind the reference's
+ * `HeBackend` plugin contract (/root/reference/pkg/src/hekan/backend.py:132-270).
+ *
+ * The reference is a pure-Python float64 slot simulator; this ABI is the
+ * boundary a real scheme is substituted behind ("a swappable contract so a real
+ * scheme can be substituted behind the same semantics", backend.py:6-7). Every
+ * entry point below replaces one reference method; the Python host mirror
+ * (paper_2409_07751_b200/backend.py) binds them with ctypes.
+ *
+ * Two libraries export this ABI:
+ *   paper_2409_07751_b200/libhekan_gpu.so — the product (sm_100a CUDA); all
+ *       buffer arguments are DEVICE pointers, work is enqueued on the stream set
+ *       with hk_set_stream (default: the legacy stream).
+ *   oracle/libckks_oracle.so — CPU restatement used only by tests/bench as the
+ *       bit-exact checker; buffer arguments are HOST pointers.
+ *
+ * Conventions
+ *   N = 2^log_n coefficients, S = N/2 complex slots (real payloads only).
+ *   A ciphertext at reference level l has l+1 RNS limbs (primes q_0..q_l) and
+ *   layout u64 [2][l+1][B][N]  (poly, limb, batch, coefficient), NTT domain,
+ *   canonical residues in [0, q_i). A plaintext at level l is u64 [l+1][Bp][N]
+ *   with Bp = 1 (broadcast over the batch) or Bp = B.
+ *   NTT domain order: position j holds a(psi^(2*brv(j)+1)) (bit-reversed).
+ *   Slot j <-> root zeta^(5^j mod 2N); rotate-left by t <-> galois 5^t mod 2N.
+ *   Levels passed as ints; an op on operands at different levels first drops
+ *   the higher one to the lower (limbs beyond are ignored), as
+ *   HeBackend.slotwise takes level = min(a.level, b.level) (backend.py:202-203).
+ *
+ * Status codes (every function returns int): HK_OK or one of HK_E_* below; a
+ * message is available from hk_last_error(ctx). The Python mirror maps them to
+ * the reference's exception taxonomy (errors.py:4-87).
+ */
+#ifndef HEKAN_H
+#define HEKAN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HK_OK 0
+#define HK_E_ARG 1        /* ValueError: bad level/size/argument (backend.py:163-164, :240-241) */
+#define HK_E_DEPTH 2      /* DepthExhausted: multiply at level < 1 (backend.py:216-217)          */
+#define HK_E_LENGTH 3     /* LengthMismatch: wrong operand kind/size (backend.py:198-201, :253-255) */
+#define HK_E_NOKEY 4      /* rotation/relin key missing for this galois element                  */
+#define HK_E_CUDA 5       /* CUDA runtime error (product library only)                            */
+#define HK_E_NOMEM 6      /* allocation failure                                                  */
+
+typedef struct hk_ctx hk_ctx;
+
+typedef struct hk_params {
+    int32_t log_n;          /* N = 2^log_n                                            */
+    int32_t n_q;            /* ciphertext primes q_0..q_{n_q-1}; depth budget = n_q-1 */
+    int32_t n_p;            /* special primes for hybrid key switching                */
+    int32_t dnum;           /* key-switching digits over the full q chain             */
+    const uint64_t *q;      /* [n_q]                                                  */
+    const uint64_t *p;      /* [n_p]                                                  */
+    const uint64_t *psi_q;  /* [n_q] primitive 2N-th roots                            */
+    const uint64_t *psi_p;  /* [n_p]                                                  */
+} hk_params;
+
+/* ---- context (replaces BackendConfig + HeBackend.__init__, backend.py:23-66, :140-143) */
+int hk_ctx_create(const hk_params *params, int32_t device, hk_ctx **out);
+void hk_ctx_destroy(hk_ctx *ctx);
+const char *hk_last_error(const hk_ctx *ctx);
+int hk_set_stream(hk_ctx *ctx, void *cuda_stream);   /* oracle: no-op */
+int hk_sync(hk_ctx *ctx);
+
+/* ---- keys (client side; replaces nothing — the reference has no keys).
+ * Secret key, relinearisation key and one Galois key per element, all from
+ * the counter-based stream seeded by `seed` (identical in oracle and GPU). */
+int hk_keygen(hk_ctx *ctx, uint64_t seed);
+int hk_add_galois_keys(hk_ctx *ctx, uint64_t seed, const uint32_t *galois_elts, int32_t n);
+int hk_has_galois_key(const hk_ctx *ctx, uint32_t galois_elt);
+/* copy key material out (parity tests): which = 0 secret [n_q+n_p][N];
+ * 1 relin [n_digits][2][n_q+n_p][N]; 2 galois key for `galois_elt`. */
+int hk_export_key(hk_ctx *ctx, int32_t which, uint32_t galois_elt, uint64_t *out);
+uint64_t hk_key_words(const hk_ctx *ctx, int32_t which);
+
+/* ---- transforms on raw limb buffers [n_limbs][batch][N]; limb l uses prime
+ * index limb0 + l in the concatenated chain (q_0..q_{n_q-1}, p_0..p_{n_p-1}). */
+int hk_ntt_fwd(hk_ctx *ctx, uint64_t *buf, int32_t limb0, int32_t n_limbs, int32_t batch);
+int hk_ntt_inv(hk_ctx *ctx, uint64_t *buf, int32_t limb0, int32_t n_limbs, int32_t batch);
+
+/* ---- encode / decode (HeBackend.encode, backend.py:149-158; decrypt :168-170).
+ * slots: f64 [batch][S] (real payloads). pt: u64 [level+1][batch][N], NTT. */
+int hk_encode(hk_ctx *ctx, const double *slots, int32_t batch, int32_t level,
+              double scale, uint64_t *pt);
+/* Constant c at scale: per-limb residues of round(c*scale) for limbs 0..level. */
+int hk_encode_const(hk_ctx *ctx, double c, int32_t level, double scale, uint64_t *res);
+
+/* ---- encrypt / decrypt (HeBackend.encrypt / decrypt, backend.py:160-170).
+ * Secret-key RLWE encryption, randomness from (seed, batch index, limb, coeff). */
+int hk_encrypt(hk_ctx *ctx, const uint64_t *pt, int32_t level, int32_t batch,
+               uint64_t seed, uint64_t *ct);
+int hk_decrypt(hk_ctx *ctx, const uint64_t *ct, int32_t level, int32_t batch,
+               double scale, double *slots);
+
+/* ---- slot-wise arithmetic (HeBackend.slotwise add/sub, backend.py:192-214) */
+int hk_add(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
+           uint64_t *out, int32_t batch);
+int hk_sub(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
+           uint64_t *out, int32_t batch);
+/* ct +/- plaintext; pt at level >= la (limbs beyond la ignored), pt_batch 1 or batch */
+int hk_add_plain(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *pt, int32_t lp,
+                 int32_t pt_batch, int32_t negate, uint64_t *out, int32_t batch);
+/* ct + constant: res[l] = residue of the constant for limb l (hk_encode_const) */
+int hk_add_const(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *res,
+                 uint64_t *out, int32_t batch);
+
+/* ---- multiplications (slotwise mul_pt / mul_ct, backend.py:215-224): each
+ * consumes one level (rescale by q_la); out is at level la-1 (or min-1). */
+int hk_mul_plain(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *pt, int32_t lp,
+                 int32_t pt_batch, uint64_t *out, int32_t batch);
+int hk_mul_const(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *res,
+                 uint64_t *out, int32_t batch);
+/* ct x ct: tensor product, relinearisation (hybrid key switch), rescale */
+int hk_mul(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
+           uint64_t *out, int32_t batch);
+/* rescale only (drop q_la): out level la-1 */
+int hk_rescale(hk_ctx *ctx, const uint64_t *a, int32_t la, uint64_t *out, int32_t batch);
+
+/* ---- rotation (HeBackend.rotate, backend.py:237-245): Galois automorphism
+ * X -> X^g plus key switch back to s. Left rotation by t uses g = 5^t mod 2N. */
+int hk_rotate(hk_ctx *ctx, const uint64_t *a, int32_t la, uint32_t galois_elt,
+              uint64_t *out, int32_t batch);
+/* Hoisted rotations of one source (baby steps of bsgs_matvec,
+ * inference.py:161-162): one ModUp shared by all n outputs. outs[i] is a
+ * ct at level la for galois_elts[i]. */
+int hk_rotate_hoisted(hk_ctx *ctx, const uint64_t *a, int32_t la,
+                      const uint32_t *galois_elts, int32_t n, uint64_t *const *outs,
+                      int32_t batch);
+
+/* ---- fused BSGS giant-step block (inference.py:166-178): for one giant step
+ * out = sum_i pt_i (*) babies_i, accumulated lazily, then ONE rescale.
+ * babies[i]: ct at level la; pts[i]: plaintext at level >= la (pt_batch 1).
+ * Logically this is n mul_pt + (n-1) add; out is at level la-1. */
+int hk_mac_plain(hk_ctx *ctx, const uint64_t *const *babies, const uint64_t *const *pts,
+                 int32_t n, int32_t la, int32_t lp, uint64_t *out, int32_t batch);
+
+/* ---- introspection */
+int32_t hk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEKAN_H */

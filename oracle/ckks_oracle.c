@@ -1,0 +1,960 @@
+/*
+ * ckks_oracle.c — CPU RNS-CKKS oracle. TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load this library; it is the bit-exact checker for
+ * the sm_100a product (paper_2409_07751_b200/libhekan_gpu.so), never part of
+ * the product path.
+ *
+ * PARITY STATUS: the reference (arxiv 2409.07751, `hekan`)
+ * contains no RNS arithmetic at all — its HeBackend is a float64 slot
+ * simulator (/root/reference/pkg/src/hekan/backend.py:1-8) and SPEC.md:8/:84
+ * declare lattice cryptography out of scope; the paper's SEAL 3.6.6
+ * is neither vendored nor installed. Integer-level parity is
+ * therefore anchored on THIS restatement of the textbook RNS-CKKS algorithms
+ * (negacyclic NTT, special-FFT encoding, RLWE encryption, hybrid key switching
+ * after Han-Ki, rescale by the last prime), and the restatement itself is
+ * pinned at the value level against the reference's own semantics: every
+ * HeBackend op (backend.py:192-245) decrypts to the CleartextBackend result
+ * within CKKS error, and the reference pipeline's golden outputs
+ * (tests/golden/, generated from /root/reference by tests/golden/make_golden.py)
+ * are reproduced within 1e-4. At the RNS level parity is "self-pinned"
+ * (NTT vs schoolbook, encode vs direct DFT, decrypt(encrypt) round trips).
+ *
+ * Semantics of each entry point: include/hekan.h. All buffers HOST pointers.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <stdarg.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "../include/hekan.h"
+
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+/* ------------------------------------------------------------------------ */
+/* modular arithmetic (plain, obviously-correct forms)                       */
+/* ------------------------------------------------------------------------ */
+static inline uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) {
+    return (uint64_t)(((u128)a * b) % q);
+}
+static inline uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) {
+    uint64_t s = a + b;
+    return s >= q ? s - q : s;
+}
+static inline uint64_t submod(uint64_t a, uint64_t b, uint64_t q) {
+    return a >= b ? a - b : a + q - b;
+}
+static uint64_t powmod(uint64_t b, uint64_t e, uint64_t q) {
+    uint64_t r = 1 % q;
+    b %= q;
+    while (e) {
+        if (e & 1) r = mulmod(r, b, q);
+        b = mulmod(b, b, q);
+        e >>= 1;
+    }
+    return r;
+}
+static uint64_t invmod(uint64_t a, uint64_t q) { return powmod(a, q - 2, q); } /* q prime */
+/* Shoup: w' = floor(w * 2^64 / q); a*w mod q for any a < 2^64 */
+static inline uint64_t shoup_pre(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+static inline uint64_t shoup_mul(uint64_t a, uint64_t w, uint64_t wp, uint64_t q) {
+    uint64_t hi = (uint64_t)(((u128)a * wp) >> 64);
+    uint64_t r = a * w - hi * q;
+    return r >= q ? r - q : r;
+}
+/* signed value -> residue */
+static inline uint64_t smod(int64_t v, uint64_t q) {
+    if (v >= 0) return (uint64_t)v % q;
+    uint64_t m = (uint64_t)(-(v + 1)) % q; /* avoid overflow at INT64_MIN */
+    return q - 1 - m;
+}
+
+static inline uint32_t brv(uint32_t x, int bits) {
+    uint32_t r = 0;
+    for (int i = 0; i < bits; ++i) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+
+/* ------------------------------------------------------------------------ */
+/* counter-based randomness (identical formula in the CUDA product)          */
+/* ------------------------------------------------------------------------ */
+static inline uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static inline uint64_t rng64(uint64_t seed, uint64_t stream, uint64_t ctr) {
+    return mix64(mix64(seed ^ mix64(stream * 0xD1B54A32D192ED03ull)) + ctr);
+}
+/* centered binomial, eta = 21: variance 10.5 (sigma 3.24) */
+static inline int64_t cbd21(uint64_t x) {
+    return (int64_t)__builtin_popcountll(x & 0x1FFFFFull) -
+           (int64_t)__builtin_popcountll((x >> 21) & 0x1FFFFFull);
+}
+static inline int64_t ternary(uint64_t x) { return (int64_t)(x % 3) - 1; }
+
+enum { ST_SECRET = 1, ST_ENC_A = 2, ST_ENC_E = 3, ST_KEY_A = 0x100, ST_KEY_E = 0x200 };
+
+/* ------------------------------------------------------------------------ */
+/* context                                                                    */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    uint32_t g;
+    uint64_t *key; /* [n_digits][2][n_q+n_p][N] */
+} galkey_t;
+
+struct hk_ctx {
+    int log_n, n, slots, n_q, n_p, dnum, alpha, n_digits, n_mod;
+    uint64_t *mod;        /* [n_mod] q then p */
+    uint64_t *psi_rev;    /* [n_mod][N]  psi^brv(k) */
+    uint64_t *psi_rev_sh;
+    uint64_t *ipsi_rev;   /* [n_mod][N]  psi^-brv(k) */
+    uint64_t *ipsi_rev_sh;
+    uint64_t *n_inv;      /* [n_mod] */
+    double *zr, *zi;      /* [2N] zeta^k */
+    uint32_t *rot_group;  /* [S] 5^j mod 2N */
+    uint64_t *sk;         /* [n_mod][N] NTT */
+    uint64_t *relin;      /* [n_digits][2][n_mod][N] */
+    galkey_t *gal;
+    int n_gal;
+    int have_keys;
+    char err[512];
+};
+
+static int fail(hk_ctx *c, int code, const char *fmt, ...) {
+    if (c) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(c->err, sizeof c->err, fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+const char *hk_last_error(const hk_ctx *c) { return c ? c->err : "null context"; }
+int32_t hk_version(void) { return 1; }
+int hk_set_stream(hk_ctx *c, void *s) { (void)c; (void)s; return HK_OK; }
+int hk_sync(hk_ctx *c) { (void)c; return HK_OK; }
+
+int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
+    (void)device;
+    if (!pr || !out || pr->log_n < 2 || pr->log_n > 17 || pr->n_q < 1 || pr->n_p < 1 || pr->dnum < 1)
+        return HK_E_ARG;
+    hk_ctx *c = (hk_ctx *)calloc(1, sizeof *c);
+    c->log_n = pr->log_n;
+    c->n = 1 << pr->log_n;
+    c->slots = c->n / 2;
+    c->n_q = pr->n_q;
+    c->n_p = pr->n_p;
+    c->dnum = pr->dnum;
+    c->alpha = (pr->n_q + pr->dnum - 1) / pr->dnum;
+    c->n_digits = (pr->n_q + c->alpha - 1) / c->alpha;
+    c->n_mod = pr->n_q + pr->n_p;
+    int N = c->n, nm = c->n_mod;
+    c->mod = (uint64_t *)malloc(sizeof(uint64_t) * nm);
+    uint64_t *psi = (uint64_t *)malloc(sizeof(uint64_t) * nm);
+    for (int i = 0; i < pr->n_q; ++i) { c->mod[i] = pr->q[i]; psi[i] = pr->psi_q[i]; }
+    for (int i = 0; i < pr->n_p; ++i) { c->mod[pr->n_q + i] = pr->p[i]; psi[pr->n_q + i] = pr->psi_p[i]; }
+    for (int i = 0; i < nm; ++i) {
+        uint64_t q = c->mod[i];
+        if (q >= (1ull << 61) || (q - 1) % (2ull * N) != 0 || powmod(psi[i], N, q) != q - 1) {
+            free(psi);
+            hk_ctx_destroy(c);
+            return HK_E_ARG;
+        }
+    }
+    size_t tsz = sizeof(uint64_t) * (size_t)nm * N;
+    c->psi_rev = malloc(tsz); c->psi_rev_sh = malloc(tsz);
+    c->ipsi_rev = malloc(tsz); c->ipsi_rev_sh = malloc(tsz);
+    c->n_inv = malloc(sizeof(uint64_t) * nm);
+    for (int m = 0; m < nm; ++m) {
+        uint64_t q = c->mod[m], w = psi[m], iw = invmod(psi[m], q);
+        uint64_t pw = 1, ipw = 1;
+        uint64_t *pr_ = c->psi_rev + (size_t)m * N, *ip_ = c->ipsi_rev + (size_t)m * N;
+        for (int k = 0; k < N; ++k) {
+            uint32_t r = brv((uint32_t)k, c->log_n);
+            pr_[r] = pw;
+            ip_[r] = ipw;
+            pw = mulmod(pw, w, q);
+            ipw = mulmod(ipw, iw, q);
+        }
+        for (int k = 0; k < N; ++k) {
+            c->psi_rev_sh[(size_t)m * N + k] = shoup_pre(pr_[k], q);
+            c->ipsi_rev_sh[(size_t)m * N + k] = shoup_pre(ip_[k], q);
+        }
+        c->n_inv[m] = invmod((uint64_t)N % q, q);
+    }
+    free(psi);
+    int M = 2 * N;
+    c->zr = malloc(sizeof(double) * M);
+    c->zi = malloc(sizeof(double) * M);
+    for (int k = 0; k < M; ++k) {
+        double ang = 2.0 * M_PI * (double)k / (double)M;
+        c->zr[k] = cos(ang);
+        c->zi[k] = sin(ang);
+    }
+    c->rot_group = malloc(sizeof(uint32_t) * c->slots);
+    uint32_t g = 1;
+    for (int j = 0; j < c->slots; ++j) { c->rot_group[j] = g; g = (uint32_t)(((uint64_t)g * 5) % (uint64_t)M); }
+    *out = c;
+    return HK_OK;
+}
+
+void hk_ctx_destroy(hk_ctx *c) {
+    if (!c) return;
+    free(c->mod); free(c->psi_rev); free(c->psi_rev_sh); free(c->ipsi_rev); free(c->ipsi_rev_sh);
+    free(c->n_inv); free(c->zr); free(c->zi); free(c->rot_group); free(c->sk); free(c->relin);
+    for (int i = 0; i < c->n_gal; ++i) free(c->gal[i].key);
+    free(c->gal);
+    free(c);
+}
+
+/* ------------------------------------------------------------------------ */
+/* NTT (Cooley-Tukey, natural in -> bit-reversed out; Gentleman-Sande back)  */
+/* ------------------------------------------------------------------------ */
+static void ntt_fwd_1(const hk_ctx *c, uint64_t *a, int m) {
+    const int N = c->n;
+    const uint64_t q = c->mod[m];
+    const uint64_t *w = c->psi_rev + (size_t)m * N, *ws = c->psi_rev_sh + (size_t)m * N;
+    int t = N;
+    for (int mm = 1; mm < N; mm <<= 1) {
+        t >>= 1;
+        for (int i = 0; i < mm; ++i) {
+            const int j1 = 2 * i * t;
+            const uint64_t S = w[mm + i], Sp = ws[mm + i];
+            for (int j = j1; j < j1 + t; ++j) {
+                uint64_t U = a[j], V = shoup_mul(a[j + t], S, Sp, q);
+                a[j] = addmod(U, V, q);
+                a[j + t] = submod(U, V, q);
+            }
+        }
+    }
+}
+
+static void ntt_inv_1(const hk_ctx *c, uint64_t *a, int m) {
+    const int N = c->n;
+    const uint64_t q = c->mod[m];
+    const uint64_t *w = c->ipsi_rev + (size_t)m * N, *ws = c->ipsi_rev_sh + (size_t)m * N;
+    int t = 1;
+    for (int mm = N; mm > 1; mm >>= 1) {
+        const int h = mm >> 1;
+        int j1 = 0;
+        for (int i = 0; i < h; ++i) {
+            const uint64_t S = w[h + i], Sp = ws[h + i];
+            for (int j = j1; j < j1 + t; ++j) {
+                uint64_t U = a[j], V = a[j + t];
+                a[j] = addmod(U, V, q);
+                a[j + t] = shoup_mul(submod(U, V, q), S, Sp, q);
+            }
+            j1 += 2 * t;
+        }
+        t <<= 1;
+    }
+    const uint64_t ni = c->n_inv[m], nis = shoup_pre(ni, q);
+    for (int j = 0; j < N; ++j) a[j] = shoup_mul(a[j], ni, nis, q);
+}
+
+int hk_ntt_fwd(hk_ctx *c, uint64_t *buf, int32_t limb0, int32_t nl, int32_t B) {
+    if (limb0 < 0 || nl < 0 || limb0 + nl > c->n_mod || B < 0) return fail(c, HK_E_ARG, "ntt: bad limb range");
+    #pragma omp parallel for collapse(2) schedule(static)
+    for (int l = 0; l < nl; ++l)
+        for (int b = 0; b < B; ++b) ntt_fwd_1(c, buf + ((size_t)l * B + b) * c->n, limb0 + l);
+    return HK_OK;
+}
+
+int hk_ntt_inv(hk_ctx *c, uint64_t *buf, int32_t limb0, int32_t nl, int32_t B) {
+    if (limb0 < 0 || nl < 0 || limb0 + nl > c->n_mod || B < 0) return fail(c, HK_E_ARG, "intt: bad limb range");
+    #pragma omp parallel for collapse(2) schedule(static)
+    for (int l = 0; l < nl; ++l)
+        for (int b = 0; b < B; ++b) ntt_inv_1(c, buf + ((size_t)l * B + b) * c->n, limb0 + l);
+    return HK_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* special FFT for the canonical embedding (slot j <-> zeta^(5^j))            */
+/* ------------------------------------------------------------------------ */
+static void bitrev_cplx(double *re, double *im, int n) {
+    int bits = 0;
+    while ((1 << bits) < n) ++bits;
+    for (int i = 0; i < n; ++i) {
+        int r = (int)brv((uint32_t)i, bits);
+        if (r > i) {
+            double t = re[i]; re[i] = re[r]; re[r] = t;
+            t = im[i]; im[i] = im[r]; im[r] = t;
+        }
+    }
+}
+
+/* evaluation: z_j = w(zeta^(5^j)); input w in natural order */
+static void fft_special_fwd(const hk_ctx *c, double *re, double *im) {
+    const int S = c->slots, M = 2 * c->n;
+    bitrev_cplx(re, im, S);
+    for (int len = 2; len <= S; len <<= 1) {
+        const int h = len >> 1, lq = len << 2, gap = M / lq;
+        for (int i = 0; i < S; i += len) {
+            for (int j = 0; j < h; ++j) {
+                const int idx = (int)(c->rot_group[j] % (uint32_t)lq) * gap;
+                const double tr = c->zr[idx], ti = c->zi[idx];
+                const double br = re[i + j + h], bi = im[i + j + h];
+                const double vr = br * tr - bi * ti;
+                const double vi = br * ti + bi * tr;
+                const double ar = re[i + j], ai = im[i + j];
+                re[i + j] = ar + vr; im[i + j] = ai + vi;
+                re[i + j + h] = ar - vr; im[i + j + h] = ai - vi;
+            }
+        }
+    }
+}
+
+/* interpolation (inverse of the above, times S) */
+static void fft_special_inv(const hk_ctx *c, double *re, double *im) {
+    const int S = c->slots, M = 2 * c->n;
+    for (int len = S; len >= 2; len >>= 1) {
+        const int h = len >> 1, lq = len << 2, gap = M / lq;
+        for (int i = 0; i < S; i += len) {
+            for (int j = 0; j < h; ++j) {
+                const int idx = (int)(c->rot_group[j] % (uint32_t)lq) * gap;
+                const double tr = c->zr[idx], ti = c->zi[idx];
+                const double Ar = re[i + j], Ai = im[i + j];
+                const double Br = re[i + j + h], Bi = im[i + j + h];
+                const double ur = Ar + Br, ui = Ai + Bi;
+                const double vr = Ar - Br, vi = Ai - Bi;
+                re[i + j] = ur; im[i + j] = ui;
+                re[i + j + h] = vr * tr + vi * ti;
+                im[i + j + h] = vi * tr - vr * ti;
+            }
+        }
+    }
+    bitrev_cplx(re, im, S);
+}
+
+/* slots (S reals) -> signed integer coefficients (N) at `scale` */
+static int encode_coeffs(const hk_ctx *c, const double *slots, double scale, int64_t *coef) {
+    const int S = c->slots;
+    double *re = malloc(sizeof(double) * S), *im = malloc(sizeof(double) * S);
+    for (int j = 0; j < S; ++j) { re[j] = slots[j]; im[j] = 0.0; }
+    fft_special_inv(c, re, im);
+    const double inv_s = 1.0 / (double)S;
+    int ok = 1;
+    for (int i = 0; i < S; ++i) {
+        const double vr = (re[i] * inv_s) * scale, vi = (im[i] * inv_s) * scale;
+        if (!(fabs(vr) < 9.0e18) || !(fabs(vi) < 9.0e18)) ok = 0;
+        coef[i] = ok ? llrint(vr) : 0;
+        coef[i + S] = ok ? llrint(vi) : 0;
+    }
+    free(re); free(im);
+    return ok;
+}
+
+int hk_encode(hk_ctx *c, const double *slots, int32_t B, int32_t level, double scale, uint64_t *pt) {
+    if (level < 0 || level >= c->n_q || B < 0) return fail(c, HK_E_ARG, "encode: level %d out of range", level);
+    const int N = c->n, S = c->slots, nl = level + 1;
+    int bad = 0;
+    #pragma omp parallel for schedule(static) reduction(|:bad)
+    for (int b = 0; b < B; ++b) {
+        int64_t *coef = malloc(sizeof(int64_t) * N);
+        if (!encode_coeffs(c, slots + (size_t)b * S, scale, coef)) bad = 1;
+        for (int l = 0; l < nl; ++l) {
+            uint64_t *dst = pt + ((size_t)l * B + b) * N;
+            for (int k = 0; k < N; ++k) dst[k] = smod(coef[k], c->mod[l]);
+        }
+        free(coef);
+    }
+    if (bad) return fail(c, HK_E_ARG, "encode: |value * scale| overflows 63 bits");
+    return hk_ntt_fwd(c, pt, 0, nl, B);
+}
+
+int hk_encode_const(hk_ctx *c, double v, int32_t level, double scale, uint64_t *res) {
+    if (level < 0 || level >= c->n_q) return fail(c, HK_E_ARG, "encode_const: level out of range");
+    const double x = v * scale;
+    if (!(fabs(x) < 9.0e18)) return fail(c, HK_E_ARG, "encode_const: |c * scale| overflows 63 bits");
+    const int64_t k = llrint(x);
+    for (int l = 0; l <= level; ++l) res[l] = smod(k, c->mod[l]);
+    return HK_OK;
+}
+
+/* centered CRT of limbs 0..(nl-1), nl in {1,2}, as a double (deterministic) */
+static inline double crt_center(const hk_ctx *c, uint64_t x0, uint64_t x1, int nl) {
+    if (nl == 1) {
+        const uint64_t q0 = c->mod[0];
+        int64_t v = x0 > q0 / 2 ? -(int64_t)(q0 - x0) : (int64_t)x0;
+        return (double)v;
+    }
+    const uint64_t q0 = c->mod[0], q1 = c->mod[1];
+    const uint64_t i0 = invmod(q1 % q0, q0), i1 = invmod(q0 % q1, q1);
+    const u128 Q = (u128)q0 * q1;
+    u128 v = (u128)mulmod(x0, i0, q0) * q1 + (u128)mulmod(x1, i1, q1) * q0;
+    v %= Q;
+    /* magnitude first, sign last: exact whenever |value| < 2^53 */
+    const int neg = v > Q / 2;
+    const u128 mag = neg ? Q - v : v;
+    const double d = ldexp((double)(uint64_t)(mag >> 64), 64) + (double)(uint64_t)mag;
+    return neg ? -d : d;
+}
+
+/* ------------------------------------------------------------------------ */
+/* keys                                                                       */
+/* ------------------------------------------------------------------------ */
+static void sample_uniform_ntt(const hk_ctx *c, uint64_t seed, uint64_t stream, uint64_t ctr0,
+                               int m, uint64_t *dst) {
+    const uint64_t q = c->mod[m];
+    for (int k = 0; k < c->n; ++k) dst[k] = rng64(seed, stream, ctr0 + (uint64_t)k) % q;
+}
+
+/* key-switching key for target s' (NTT over all n_mod limbs), digits over q */
+static void make_ks_key(const hk_ctx *c, uint64_t seed, uint64_t stream_tag, const uint64_t *sprime,
+                        uint64_t *key) {
+    const int N = c->n, nm = c->n_mod;
+    uint64_t P_mod[64];
+    for (int i = 0; i < c->n_q; ++i) {
+        uint64_t acc = 1;
+        for (int k = 0; k < c->n_p; ++k) acc = mulmod(acc, c->mod[c->n_q + k] % c->mod[i], c->mod[i]);
+        P_mod[i] = acc;
+    }
+    for (int j = 0; j < c->n_digits; ++j) {
+        const int d0 = j * c->alpha, d1 = (j + 1) * c->alpha < c->n_q ? (j + 1) * c->alpha : c->n_q;
+        uint64_t *bj = key + ((size_t)j * 2 + 0) * nm * N;
+        uint64_t *aj = key + ((size_t)j * 2 + 1) * nm * N;
+        int64_t *e = malloc(sizeof(int64_t) * N);
+        for (int k = 0; k < N; ++k)
+            e[k] = cbd21(rng64(seed, ST_KEY_E + stream_tag * 64 + j, (uint64_t)k));
+        #pragma omp parallel for schedule(static)
+        for (int m = 0; m < nm; ++m) {
+            const uint64_t q = c->mod[m];
+            uint64_t *a = aj + (size_t)m * N, *b = bj + (size_t)m * N;
+            sample_uniform_ntt(c, seed, ST_KEY_A + stream_tag * 64 + j, (uint64_t)m * N, m, a);
+            for (int k = 0; k < N; ++k) b[k] = smod(e[k], q);
+            ntt_fwd_1(c, b, m);
+            const uint64_t *s = c->sk + (size_t)m * N, *sp = sprime + (size_t)m * N;
+            const int in_digit = (m >= d0 && m < d1);
+            for (int k = 0; k < N; ++k) {
+                uint64_t v = submod(b[k], mulmod(a[k], s[k], q), q);
+                if (in_digit) v = addmod(v, mulmod(P_mod[m], sp[k], q), q);
+                b[k] = v;
+            }
+        }
+        free(e);
+    }
+}
+
+/* NTT-domain automorphism X -> X^g: out[j] = in[idx(e(j) * g)] */
+static inline uint32_t auto_src(uint32_t j, uint32_t g, int log_n) {
+    const uint32_t M = 2u << log_n;
+    const uint32_t e = 2u * brv(j, log_n) + 1u;
+    const uint32_t eg = (uint32_t)(((uint64_t)e * g) & (M - 1));
+    return brv((eg - 1u) >> 1, log_n);
+}
+static void automorph_ntt(const hk_ctx *c, const uint64_t *in, uint64_t *out, uint32_t g) {
+    for (uint32_t j = 0; j < (uint32_t)c->n; ++j) out[j] = in[auto_src(j, g, c->log_n)];
+}
+
+uint64_t hk_key_words(const hk_ctx *c, int32_t which) {
+    const uint64_t nm = (uint64_t)c->n_mod, N = (uint64_t)c->n;
+    if (which == 0) return nm * N;
+    return (uint64_t)c->n_digits * 2 * nm * N;
+}
+
+int hk_keygen(hk_ctx *c, uint64_t seed) {
+    const int N = c->n, nm = c->n_mod;
+    free(c->sk); free(c->relin);
+    c->sk = malloc(sizeof(uint64_t) * (size_t)nm * N);
+    int64_t *s = malloc(sizeof(int64_t) * N);
+    for (int k = 0; k < N; ++k) s[k] = ternary(rng64(seed, ST_SECRET, (uint64_t)k));
+    for (int m = 0; m < nm; ++m) {
+        uint64_t *dst = c->sk + (size_t)m * N;
+        for (int k = 0; k < N; ++k) dst[k] = smod(s[k], c->mod[m]);
+        ntt_fwd_1(c, dst, m);
+    }
+    free(s);
+    uint64_t *s2 = malloc(sizeof(uint64_t) * (size_t)nm * N);
+    for (int m = 0; m < nm; ++m)
+        for (int k = 0; k < N; ++k) {
+            const size_t o = (size_t)m * N + k;
+            s2[o] = mulmod(c->sk[o], c->sk[o], c->mod[m]);
+        }
+    c->relin = malloc(sizeof(uint64_t) * hk_key_words(c, 1));
+    make_ks_key(c, seed, 0, s2, c->relin);
+    free(s2);
+    for (int i = 0; i < c->n_gal; ++i) free(c->gal[i].key);
+    free(c->gal);
+    c->gal = NULL;
+    c->n_gal = 0;
+    c->have_keys = 1;
+    return HK_OK;
+}
+
+int hk_has_galois_key(const hk_ctx *c, uint32_t g) {
+    for (int i = 0; i < c->n_gal; ++i)
+        if (c->gal[i].g == g) return 1;
+    return 0;
+}
+
+static const uint64_t *find_gal(const hk_ctx *c, uint32_t g) {
+    for (int i = 0; i < c->n_gal; ++i)
+        if (c->gal[i].g == g) return c->gal[i].key;
+    return NULL;
+}
+
+int hk_add_galois_keys(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n) {
+    if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
+    const int N = c->n, nm = c->n_mod;
+    const uint32_t M = 2u * (uint32_t)N;
+    for (int i = 0; i < n; ++i) {
+        const uint32_t g = gs[i];
+        if ((g & 1u) == 0 || g >= M) return fail(c, HK_E_ARG, "galois element %u invalid", g);
+        if (hk_has_galois_key(c, g)) continue;
+        uint64_t *sg = malloc(sizeof(uint64_t) * (size_t)nm * N);
+        for (int m = 0; m < nm; ++m) automorph_ntt(c, c->sk + (size_t)m * N, sg + (size_t)m * N, g);
+        uint64_t *key = malloc(sizeof(uint64_t) * hk_key_words(c, 1));
+        make_ks_key(c, seed, 1 + (uint64_t)g, sg, key);
+        free(sg);
+        c->gal = realloc(c->gal, sizeof(galkey_t) * (c->n_gal + 1));
+        c->gal[c->n_gal].g = g;
+        c->gal[c->n_gal].key = key;
+        c->n_gal++;
+    }
+    return HK_OK;
+}
+
+int hk_export_key(hk_ctx *c, int32_t which, uint32_t g, uint64_t *out) {
+    if (!c->have_keys) return fail(c, HK_E_NOKEY, "no keys");
+    const uint64_t *src = which == 0 ? c->sk : which == 1 ? c->relin : find_gal(c, g);
+    if (!src) return fail(c, HK_E_NOKEY, "no galois key for %u", g);
+    memcpy(out, src, sizeof(uint64_t) * hk_key_words(c, which == 0 ? 0 : 1));
+    return HK_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* encrypt / decrypt                                                          */
+/* ------------------------------------------------------------------------ */
+int hk_encrypt(hk_ctx *c, const uint64_t *pt, int32_t level, int32_t B, uint64_t seed, uint64_t *ct) {
+    if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
+    if (level < 0 || level >= c->n_q) return fail(c, HK_E_ARG, "encrypt: level out of range");
+    const int N = c->n, nl = level + 1;
+    const size_t poly = (size_t)nl * B * N;
+    uint64_t *c0 = ct, *c1 = ct + poly;
+    #pragma omp parallel for schedule(static)
+    for (int b = 0; b < B; ++b) {
+        int64_t *e = malloc(sizeof(int64_t) * N);
+        uint64_t *tmp = malloc(sizeof(uint64_t) * N);
+        for (int k = 0; k < N; ++k) e[k] = cbd21(rng64(seed, ST_ENC_E, (uint64_t)b * N + k));
+        for (int l = 0; l < nl; ++l) {
+            const uint64_t q = c->mod[l];
+            const size_t o = ((size_t)l * B + b) * N;
+            sample_uniform_ntt(c, seed, ST_ENC_A, ((uint64_t)b * nl + l) * N, l, c1 + o);
+            for (int k = 0; k < N; ++k) tmp[k] = smod(e[k], q);
+            ntt_fwd_1(c, tmp, l);
+            const uint64_t *s = c->sk + (size_t)l * N;
+            for (int k = 0; k < N; ++k) {
+                uint64_t v = addmod(pt[o + k], tmp[k], q);
+                c0[o + k] = submod(v, mulmod(c1[o + k], s[k], q), q);
+            }
+        }
+        free(e); free(tmp);
+    }
+    return HK_OK;
+}
+
+int hk_decrypt(hk_ctx *c, const uint64_t *ct, int32_t level, int32_t B, double scale, double *slots) {
+    if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
+    if (level < 0 || level >= c->n_q) return fail(c, HK_E_ARG, "decrypt: level out of range");
+    const int N = c->n, S = c->slots, nl = level + 1, use = nl >= 2 ? 2 : 1;
+    const size_t poly = (size_t)nl * B * N;
+    #pragma omp parallel for schedule(static)
+    for (int b = 0; b < B; ++b) {
+        uint64_t *m = malloc(sizeof(uint64_t) * 2 * N);
+        for (int l = 0; l < use; ++l) {
+            const uint64_t q = c->mod[l];
+            const size_t o = ((size_t)l * B + b) * N;
+            const uint64_t *s = c->sk + (size_t)l * N;
+            for (int k = 0; k < N; ++k) m[(size_t)l * N + k] = addmod(ct[o + k], mulmod(ct[poly + o + k], s[k], q), q);
+            ntt_inv_1(c, m + (size_t)l * N, l);
+        }
+        double *re = malloc(sizeof(double) * S), *im = malloc(sizeof(double) * S);
+        for (int i = 0; i < S; ++i) {
+            const double a = crt_center(c, m[i], use == 2 ? m[N + i] : 0, use);
+            const double bb = crt_center(c, m[i + S], use == 2 ? m[N + i + S] : 0, use);
+            re[i] = a / scale;
+            im[i] = bb / scale;
+        }
+        fft_special_fwd(c, re, im);
+        for (int j = 0; j < S; ++j) slots[(size_t)b * S + j] = re[j];
+        free(re); free(im); free(m);
+    }
+    return HK_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* slot-wise add/sub                                                          */
+/* ------------------------------------------------------------------------ */
+static int addsub(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, int lb, uint64_t *out,
+                  int B, int neg) {
+    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return fail(c, HK_E_ARG, "add: level out of range");
+    const int lo = la < lb ? la : lb, N = c->n;
+    for (int p = 0; p < 2; ++p)
+        for (int l = 0; l <= lo; ++l) {
+            const uint64_t q = c->mod[l];
+            const uint64_t *x = a + ((size_t)p * (la + 1) + l) * B * N;
+            const uint64_t *y = b + ((size_t)p * (lb + 1) + l) * B * N;
+            uint64_t *z = out + ((size_t)p * (lo + 1) + l) * B * N;
+            for (size_t k = 0; k < (size_t)B * N; ++k) z[k] = neg ? submod(x[k], y[k], q) : addmod(x[k], y[k], q);
+        }
+    return HK_OK;
+}
+int hk_add(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *o, int32_t B) {
+    return addsub(c, a, la, b, lb, o, B, 0);
+}
+int hk_sub(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *o, int32_t B) {
+    return addsub(c, a, la, b, lb, o, B, 1);
+}
+
+int hk_add_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, int32_t lp, int32_t pb,
+                 int32_t negate, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q || lp < la) return fail(c, HK_E_ARG, "add_plain: level mismatch");
+    if (pb != 1 && pb != B) return fail(c, HK_E_LENGTH, "add_plain: plaintext batch");
+    const int N = c->n;
+    const size_t poly = (size_t)(la + 1) * B * N;
+    for (int l = 0; l <= la; ++l) {
+        const uint64_t q = c->mod[l];
+        for (int b = 0; b < B; ++b) {
+            const uint64_t *x = a + ((size_t)l * B + b) * N;
+            const uint64_t *y = pt + ((size_t)l * pb + (pb == 1 ? 0 : b)) * N;
+            uint64_t *z = out + ((size_t)l * B + b) * N;
+            for (int k = 0; k < N; ++k) z[k] = negate ? submod(x[k], y[k], q) : addmod(x[k], y[k], q);
+        }
+    }
+    memcpy(out + poly, a + poly, sizeof(uint64_t) * poly);
+    return HK_OK;
+}
+
+int hk_add_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q) return fail(c, HK_E_ARG, "add_const: level");
+    const int N = c->n;
+    const size_t poly = (size_t)(la + 1) * B * N;
+    for (int l = 0; l <= la; ++l) {
+        const uint64_t q = c->mod[l], r = res[l];
+        for (size_t k = 0; k < (size_t)B * N; ++k) out[(size_t)l * B * N + k] = addmod(a[(size_t)l * B * N + k], r, q);
+    }
+    memcpy(out + poly, a + poly, sizeof(uint64_t) * poly);
+    return HK_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* rescale: drop q_l with rounding (centered remainder)                      */
+/* ------------------------------------------------------------------------ */
+/* in: one poly [l+1][B][N] at level l; out: [l][B][N] */
+static void rescale_poly(const hk_ctx *c, const uint64_t *in, int l, int B, uint64_t *out) {
+    const int N = c->n;
+    const uint64_t ql = c->mod[l];
+    #pragma omp parallel for schedule(static)
+    for (int b = 0; b < B; ++b) {
+        uint64_t *last = malloc(sizeof(uint64_t) * N), *r = malloc(sizeof(uint64_t) * N);
+        memcpy(last, in + ((size_t)l * B + b) * N, sizeof(uint64_t) * N);
+        ntt_inv_1(c, last, l);
+        for (int i = 0; i < l; ++i) {
+            const uint64_t q = c->mod[i], qinv = invmod(ql % q, q);
+            for (int k = 0; k < N; ++k) {
+                const uint64_t x = last[k];
+                r[k] = x > ql / 2 ? submod(0, (ql - x) % q, q) : x % q;
+            }
+            ntt_fwd_1(c, r, i);
+            const uint64_t *x = in + ((size_t)i * B + b) * N;
+            uint64_t *z = out + ((size_t)i * B + b) * N;
+            for (int k = 0; k < N; ++k) z[k] = mulmod(submod(x[k], r[k], q), qinv, q);
+        }
+        free(last); free(r);
+    }
+}
+
+int hk_rescale(hk_ctx *c, const uint64_t *a, int32_t la, uint64_t *out, int32_t B) {
+    if (la < 1 || la >= c->n_q) return fail(c, HK_E_DEPTH, "rescale at level %d", la);
+    const size_t pin = (size_t)(la + 1) * B * c->n, pout = (size_t)la * B * c->n;
+    rescale_poly(c, a, la, B, out);
+    rescale_poly(c, a + pin, la, B, out + pout);
+    return HK_OK;
+}
+
+int hk_mul_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, int32_t lp, int32_t pb,
+                 uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q || lp < la) return fail(c, HK_E_ARG, "mul_plain: level mismatch");
+    if (la < 1) return fail(c, HK_E_DEPTH, "multiplication at level %d", la);
+    if (pb != 1 && pb != B) return fail(c, HK_E_LENGTH, "mul_plain: plaintext batch");
+    const int N = c->n;
+    const size_t poly = (size_t)(la + 1) * B * N;
+    uint64_t *t = malloc(sizeof(uint64_t) * 2 * poly);
+    for (int p = 0; p < 2; ++p)
+        for (int l = 0; l <= la; ++l) {
+            const uint64_t q = c->mod[l];
+            for (int b = 0; b < B; ++b) {
+                const uint64_t *x = a + p * poly + ((size_t)l * B + b) * N;
+                const uint64_t *y = pt + ((size_t)l * pb + (pb == 1 ? 0 : b)) * N;
+                uint64_t *z = t + p * poly + ((size_t)l * B + b) * N;
+                for (int k = 0; k < N; ++k) z[k] = mulmod(x[k], y[k], q);
+            }
+        }
+    int rc = hk_rescale(c, t, la, out, B);
+    free(t);
+    return rc;
+}
+
+int hk_mul_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q) return fail(c, HK_E_ARG, "mul_const: level");
+    if (la < 1) return fail(c, HK_E_DEPTH, "multiplication at level %d", la);
+    const int N = c->n;
+    const size_t poly = (size_t)(la + 1) * B * N;
+    uint64_t *t = malloc(sizeof(uint64_t) * 2 * poly);
+    for (int p = 0; p < 2; ++p)
+        for (int l = 0; l <= la; ++l) {
+            const uint64_t q = c->mod[l], r = res[l];
+            for (size_t k = 0; k < (size_t)B * N; ++k) {
+                const size_t o = p * poly + (size_t)l * B * N + k;
+                t[o] = mulmod(a[o], r, q);
+            }
+        }
+    int rc = hk_rescale(c, t, la, out, B);
+    free(t);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* hybrid key switching (ModUp per digit -> key inner product -> ModDown)    */
+/* ------------------------------------------------------------------------ */
+/* index of limb t of the extended basis (0..l, then specials) in the n_mod chain */
+static inline int ext_mod(const hk_ctx *c, int l, int t) { return t <= l ? t : c->n_q + (t - l - 1); }
+
+/* ModUp: d (NTT, [l+1][B][N]) -> ext [n_dig][l+1+n_p][B][N] NTT */
+static void modup(const hk_ctx *c, const uint64_t *d, int l, int B, uint64_t *ext) {
+    const int N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    uint64_t *dc = malloc(sizeof(uint64_t) * (size_t)(l + 1) * B * N);
+    memcpy(dc, d, sizeof(uint64_t) * (size_t)(l + 1) * B * N);
+    for (int i = 0; i <= l; ++i)
+        for (int b = 0; b < B; ++b) ntt_inv_1(c, dc + ((size_t)i * B + b) * N, i);
+    for (int j = 0; j < nd; ++j) {
+        const int d0 = j * c->alpha, d1 = (j + 1) * c->alpha < l + 1 ? (j + 1) * c->alpha : l + 1;
+        const int nD = d1 - d0;
+        /* per-source constants: inv_i = (Q_D/q_i)^-1 mod q_i */
+        uint64_t inv[64];
+        for (int i = d0; i < d1; ++i) {
+            uint64_t prod = 1;
+            for (int k = d0; k < d1; ++k)
+                if (k != i) prod = mulmod(prod, c->mod[k] % c->mod[i], c->mod[i]);
+            inv[i - d0] = invmod(prod, c->mod[i]);
+        }
+        #pragma omp parallel for schedule(dynamic)
+        for (int t = 0; t < ne; ++t) {
+            const int m = ext_mod(c, l, t);
+            uint64_t *dst = ext + ((size_t)j * ne + t) * B * N;
+            if (t >= d0 && t < d1) {
+                memcpy(dst, d + (size_t)t * B * N, sizeof(uint64_t) * B * N);
+                continue;
+            }
+            const uint64_t qt = c->mod[m];
+            uint64_t hat[64]; /* (Q_D/q_i) mod q_t */
+            for (int i = d0; i < d1; ++i) {
+                uint64_t prod = 1;
+                for (int k = d0; k < d1; ++k)
+                    if (k != i) prod = mulmod(prod, c->mod[k] % qt, qt);
+                hat[i - d0] = prod;
+            }
+            for (int b = 0; b < B; ++b) {
+                uint64_t *o = dst + (size_t)b * N;
+                for (int k = 0; k < N; ++k) {
+                    uint64_t acc = 0;
+                    for (int ii = 0; ii < nD; ++ii) {
+                        const int i = d0 + ii;
+                        const uint64_t v = mulmod(dc[((size_t)i * B + b) * N + k], inv[ii], c->mod[i]);
+                        acc = addmod(acc, mulmod(v % qt, hat[ii], qt), qt);
+                    }
+                    o[k] = acc;
+                }
+                ntt_fwd_1(c, o, m);
+            }
+        }
+    }
+    free(dc);
+}
+
+/* key inner product for one automorphism g (g = 1: identity):
+ * acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][mod(t)] ; acc [2][ne][B][N] */
+static void key_ip(const hk_ctx *c, const uint64_t *ext, int l, int B, const uint64_t *key, uint32_t g,
+                   uint64_t *acc) {
+    const int N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1, nm = c->n_mod;
+    #pragma omp parallel for collapse(2) schedule(static)
+    for (int t = 0; t < ne; ++t)
+        for (int b = 0; b < B; ++b) {
+            const int m = ext_mod(c, l, t);
+            const uint64_t q = c->mod[m];
+            uint64_t *o0 = acc + ((size_t)0 * ne + t) * B * N + (size_t)b * N;
+            uint64_t *o1 = acc + ((size_t)1 * ne + t) * B * N + (size_t)b * N;
+            uint64_t *tmp = malloc(sizeof(uint64_t) * N);
+            for (int k = 0; k < N; ++k) { o0[k] = 0; o1[k] = 0; }
+            for (int j = 0; j < nd; ++j) {
+                const uint64_t *src = ext + ((size_t)j * ne + t) * B * N + (size_t)b * N;
+                const uint64_t *x = src;
+                if (g != 1) { automorph_ntt(c, src, tmp, g); x = tmp; }
+                const uint64_t *k0 = key + (((size_t)j * 2 + 0) * nm + m) * N;
+                const uint64_t *k1 = key + (((size_t)j * 2 + 1) * nm + m) * N;
+                for (int k = 0; k < N; ++k) {
+                    o0[k] = addmod(o0[k], mulmod(x[k], k0[k], q), q);
+                    o1[k] = addmod(o1[k], mulmod(x[k], k1[k], q), q);
+                }
+            }
+            free(tmp);
+        }
+}
+
+/* ModDown one poly: acc [ne][B][N] (NTT) -> out [l+1][B][N] = (acc - conv([acc]_P)) * P^-1 */
+static void moddown(const hk_ctx *c, const uint64_t *acc, int l, int B, uint64_t *out) {
+    const int N = c->n, np = c->n_p;
+    uint64_t *sp = malloc(sizeof(uint64_t) * (size_t)np * B * N);
+    memcpy(sp, acc + (size_t)(l + 1) * B * N, sizeof(uint64_t) * (size_t)np * B * N);
+    for (int k = 0; k < np; ++k)
+        for (int b = 0; b < B; ++b) ntt_inv_1(c, sp + ((size_t)k * B + b) * N, c->n_q + k);
+    uint64_t inv[64];
+    for (int k = 0; k < np; ++k) {
+        const uint64_t pk = c->mod[c->n_q + k];
+        uint64_t prod = 1;
+        for (int r = 0; r < np; ++r)
+            if (r != k) prod = mulmod(prod, c->mod[c->n_q + r] % pk, pk);
+        inv[k] = invmod(prod, pk);
+    }
+    #pragma omp parallel for schedule(dynamic)
+    for (int i = 0; i <= l; ++i) {
+        const uint64_t q = c->mod[i];
+        uint64_t hat[64], Pinv, Pm = 1;
+        for (int k = 0; k < np; ++k) {
+            uint64_t prod = 1;
+            for (int r = 0; r < np; ++r)
+                if (r != k) prod = mulmod(prod, c->mod[c->n_q + r] % q, q);
+            hat[k] = prod;
+            Pm = mulmod(Pm, c->mod[c->n_q + k] % q, q);
+        }
+        Pinv = invmod(Pm, q);
+        uint64_t *conv = malloc(sizeof(uint64_t) * N);
+        for (int b = 0; b < B; ++b) {
+            for (int n = 0; n < N; ++n) {
+                uint64_t s = 0;
+                for (int k = 0; k < np; ++k) {
+                    const uint64_t pk = c->mod[c->n_q + k];
+                    const uint64_t v = mulmod(sp[((size_t)k * B + b) * N + n], inv[k], pk);
+                    s = addmod(s, mulmod(v % q, hat[k], q), q);
+                }
+                conv[n] = s;
+            }
+            ntt_fwd_1(c, conv, i);
+            const uint64_t *x = acc + ((size_t)i * B + b) * N;
+            uint64_t *z = out + ((size_t)i * B + b) * N;
+            for (int n = 0; n < N; ++n) z[n] = mulmod(submod(x[n], conv[n], q), Pinv, q);
+        }
+        free(conv);
+    }
+    free(sp);
+}
+
+int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {
+    if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return fail(c, HK_E_ARG, "mul: level");
+    const int l = la < lb ? la : lb, N = c->n;
+    if (l < 1) return fail(c, HK_E_DEPTH, "multiplication at level %d", l);
+    const size_t pl = (size_t)(l + 1) * B * N;
+    const size_t pa = (size_t)(la + 1) * B * N, pb = (size_t)(lb + 1) * B * N;
+    uint64_t *d = malloc(sizeof(uint64_t) * 3 * pl); /* d0, d1, d2 */
+    for (int i = 0; i <= l; ++i) {
+        const uint64_t q = c->mod[i];
+        for (size_t k = 0; k < (size_t)B * N; ++k) {
+            const size_t o = (size_t)i * B * N + k;
+            const uint64_t a0 = a[o], a1 = a[pa + o], b0 = b[o], b1 = b[pb + o];
+            d[o] = mulmod(a0, b0, q);
+            d[pl + o] = addmod(mulmod(a0, b1, q), mulmod(a1, b0, q), q);
+            d[2 * pl + o] = mulmod(a1, b1, q);
+        }
+    }
+    const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    uint64_t *ext = malloc(sizeof(uint64_t) * (size_t)nd * ne * B * N);
+    uint64_t *acc = malloc(sizeof(uint64_t) * 2 * (size_t)ne * B * N);
+    modup(c, d + 2 * pl, l, B, ext);
+    key_ip(c, ext, l, B, c->relin, 1u, acc);
+    uint64_t *ks = malloc(sizeof(uint64_t) * 2 * pl);
+    moddown(c, acc, l, B, ks);
+    moddown(c, acc + (size_t)ne * B * N, l, B, ks + pl);
+    for (int i = 0; i <= l; ++i) {
+        const uint64_t q = c->mod[i];
+        for (size_t k = 0; k < (size_t)B * N; ++k) {
+            const size_t o = (size_t)i * B * N + k;
+            d[o] = addmod(d[o], ks[o], q);
+            d[pl + o] = addmod(d[pl + o], ks[pl + o], q);
+        }
+    }
+    int rc = hk_rescale(c, d, l, out, B);
+    free(d); free(ext); free(acc); free(ks);
+    return rc;
+}
+
+int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *gs, int32_t n,
+                      uint64_t *const *outs, int32_t B) {
+    if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || la >= c->n_q) return fail(c, HK_E_ARG, "rotate: level");
+    for (int i = 0; i < n; ++i)
+        if (!find_gal(c, gs[i])) return fail(c, HK_E_NOKEY, "no galois key for element %u", gs[i]);
+    const int l = la, N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    const size_t pl = (size_t)(l + 1) * B * N;
+    uint64_t *ext = malloc(sizeof(uint64_t) * (size_t)nd * ne * B * N);
+    uint64_t *acc = malloc(sizeof(uint64_t) * 2 * (size_t)ne * B * N);
+    modup(c, a + pl, l, B, ext);
+    for (int r = 0; r < n; ++r) {
+        const uint32_t g = gs[r];
+        uint64_t *o = outs[r];
+        key_ip(c, ext, l, B, find_gal(c, g), g, acc);
+        moddown(c, acc, l, B, o);
+        moddown(c, acc + (size_t)ne * B * N, l, B, o + pl);
+        uint64_t *tmp = malloc(sizeof(uint64_t) * N);
+        for (int i = 0; i <= l; ++i) {
+            const uint64_t q = c->mod[i];
+            for (int b = 0; b < B; ++b) {
+                const size_t off = ((size_t)i * B + b) * N;
+                automorph_ntt(c, a + off, tmp, g);
+                for (int k = 0; k < N; ++k) o[off + k] = addmod(o[off + k], tmp[k], q);
+            }
+        }
+        free(tmp);
+    }
+    free(ext); free(acc);
+    return HK_OK;
+}
+
+int hk_rotate(hk_ctx *c, const uint64_t *a, int32_t la, uint32_t g, uint64_t *out, int32_t B) {
+    uint64_t *outs[1] = {out};
+    return hk_rotate_hoisted(c, a, la, &g, 1, outs, B);
+}
+
+int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const *pts, int32_t n,
+                 int32_t la, int32_t lp, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q || lp < la || n < 1) return fail(c, HK_E_ARG, "mac_plain: args");
+    if (la < 1) return fail(c, HK_E_DEPTH, "multiplication at level %d", la);
+    const int N = c->n;
+    const size_t poly = (size_t)(la + 1) * B * N;
+    uint64_t *t = calloc(2 * poly, sizeof(uint64_t));
+    for (int p = 0; p < 2; ++p)
+        for (int l = 0; l <= la; ++l) {
+            const uint64_t q = c->mod[l];
+            for (int b = 0; b < B; ++b) {
+                uint64_t *z = t + p * poly + ((size_t)l * B + b) * N;
+                for (int i = 0; i < n; ++i) {
+                    const uint64_t *x = babies[i] + p * poly + ((size_t)l * B + b) * N;
+                    const uint64_t *y = pts[i] + (size_t)l * N;
+                    for (int k = 0; k < N; ++k) z[k] = addmod(z[k], mulmod(x[k], y[k], q), q);
+                }
+            }
+        }
+    int rc = hk_rescale(c, t, la, out, B);
+    free(t);
+    return rc;
+}

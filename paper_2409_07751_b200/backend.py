@@ -1,0 +1,512 @@
+"""RNS-CKKS backend behind the reference's `HeBackend` plugin contract.
+
+Mirrors `/root/reference/pkg/src/hekan/backend.py:23-309` name for name:
+`BackendConfig`, `OpCounter`, `PlainVector`, `CipherText`, `HeBackend`
+methods (`encode`, `encrypt`, `decrypt`, `refresh`, `reset_counter`,
+`slotwise`, `add`, `sub`, `mul`, `rotate`) and the module helpers
+(`slotwise`, `rotate`, `decrypt`, `make_backend`), with the reference's level
+rule, counters and error behaviour. Underneath, every op is one call into the
+sm_100a library (include/hekan.h) on limb-major RNS buffers in HBM:
+
+  reference                          engine
+  --------------------------------   -----------------------------------------
+  CipherText.slots float64[S]        u64 [2][level+1][B][N], NTT domain
+  slotwise add/sub (:209-214)        hk_add / hk_sub / hk_add_plain / hk_add_const
+  slotwise mul_pt  (:215-224)        hk_mul_plain / hk_mul_const (+ rescale)
+  slotwise mul_ct  (:215-224)        hk_mul: tensor + relinearise + rescale
+  rotate np.roll(-t) (:237-245)      hk_rotate: X -> X^(5^t) + key switch
+
+Batching: a `CipherText` carries a leading batch dimension B (independent
+samples in one buffer, one launch per op). Counters tally LOGICAL ops per call,
+i.e. per inference, exactly as the reference counts one ciphertext.
+Plain operands are shared across the batch.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import itertools
+import json
+import math
+from dataclasses import dataclass, field, fields, replace
+
+import numpy as np
+
+from .errors import DepthExhausted, InputTooLong, LengthMismatch
+from .params import CkksParams, kan_params
+
+OP_KINDS = ("add", "sub", "mul_ct", "mul_pt")
+
+
+# ---------------------------------------------------------------------------
+# configuration and counters (backend.py:23-105)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class BackendConfig:
+    """Reference scheme parameters (backend.py:23-66). slot_count = N/2 of the
+    CKKS ring; depth_budget = top level (number of rescaling primes)."""
+
+    slot_count: int
+    depth_budget: int
+    noise_std: float = 0.0
+    rng_seed: int = 0
+
+    def __post_init__(self):
+        if self.slot_count <= 0 or (self.slot_count & (self.slot_count - 1)) != 0:
+            raise ValueError(f"slot_count must be a positive power of two, got {self.slot_count}")
+        if self.depth_budget < 0:
+            raise ValueError("depth_budget must be >= 0")
+        if self.noise_std < 0:
+            raise ValueError("noise_std must be >= 0")
+
+    @classmethod
+    def from_json(cls, source) -> "BackendConfig":
+        if isinstance(source, dict):
+            doc = source
+        elif isinstance(source, str) and source.lstrip().startswith("{"):
+            doc = json.loads(source)
+        else:
+            with open(source) as fh:
+                doc = json.load(fh)
+        known = {f.name for f in fields(cls)}
+        unknown = set(doc) - known
+        if unknown:
+            raise ValueError(f"unknown BackendConfig keys: {sorted(unknown)}")
+        return cls(**doc)
+
+    def to_json(self) -> dict:
+        return {"slot_count": self.slot_count, "depth_budget": self.depth_budget,
+                "noise_std": self.noise_std, "rng_seed": self.rng_seed}
+
+
+@dataclass
+class OpCounter:
+    """Logical op tallies (backend.py:69-105)."""
+
+    adds: int = 0
+    subs: int = 0
+    ct_mults: int = 0
+    pt_mults: int = 0
+    rotations: int = 0
+    max_depth_consumed: int = 0
+
+    def copy(self) -> "OpCounter":
+        return replace(self)
+
+    def merge(self, other: "OpCounter") -> None:
+        self.adds += other.adds
+        self.subs += other.subs
+        self.ct_mults += other.ct_mults
+        self.pt_mults += other.pt_mults
+        self.rotations += other.rotations
+        self.max_depth_consumed = max(self.max_depth_consumed, other.max_depth_consumed)
+
+    def since(self, earlier: "OpCounter") -> "OpCounter":
+        return OpCounter(adds=self.adds - earlier.adds, subs=self.subs - earlier.subs,
+                         ct_mults=self.ct_mults - earlier.ct_mults,
+                         pt_mults=self.pt_mults - earlier.pt_mults,
+                         rotations=self.rotations - earlier.rotations,
+                         max_depth_consumed=self.max_depth_consumed)
+
+    @property
+    def mults(self) -> int:
+        return self.ct_mults + self.pt_mults
+
+
+@dataclass(frozen=True)
+class PlainVector:
+    """Unencrypted slot vector (backend.py:108-112)."""
+
+    slots: np.ndarray
+
+
+class CipherText:
+    """Batched RNS-CKKS ciphertext handle (reference value type
+    backend.py:115-129). Immutable: every op returns a new handle that owns a
+    fresh HBM buffer u64 [2][level+1][batch][N]. `slots` decrypts lazily
+    (debug/test convenience; needs the secret key held by the backend)."""
+
+    __slots__ = ("data", "level", "tag", "backend", "batch", "batched", "__weakref__")
+
+    def __init__(self, data, level: int, tag: str, backend: "HeBackend", batch: int,
+                 batched: bool):
+        self.data = data
+        self.level = level
+        self.tag = tag
+        self.backend = backend
+        self.batch = batch
+        self.batched = batched
+
+    @property
+    def slots(self) -> np.ndarray:
+        return self.backend.decrypt(self)
+
+    def __repr__(self) -> str:
+        return f"CipherText(level={self.level}, tag={self.tag!r}, batch={self.batch})"
+
+
+def _slot_rows(values, slot_count: int):
+    """Encode-style zero padding / broadcast to (B, S) plus the batched flag."""
+    if np.isscalar(values):
+        return np.full((1, slot_count), float(values)), False
+    arr = np.asarray(values, dtype=float)
+    batched = arr.ndim >= 2
+    rows = arr.reshape(arr.shape[0], -1) if batched else arr.reshape(1, -1)
+    if rows.shape[1] > slot_count:
+        raise InputTooLong(f"{rows.shape[1]} values > {slot_count} slots")
+    out = np.zeros((rows.shape[0], slot_count))
+    out[:, : rows.shape[1]] = rows
+    return out, batched
+
+
+def _const_of(arr: np.ndarray):
+    """Python float if every slot holds the same value (scalar fast path)."""
+    if arr.size and np.all(arr == arr.flat[0]):
+        return float(arr.flat[0])
+    return None
+
+
+def galois_element(t: int, slot_count: int) -> int:
+    """Left rotation by t <-> X -> X^(5^t mod 2N) (slot j <-> zeta^(5^j))."""
+    return pow(5, t % slot_count, 4 * slot_count)
+
+
+# ---------------------------------------------------------------------------
+# backend
+# ---------------------------------------------------------------------------
+
+
+class HeBackend:
+    """RNS-CKKS implementation of the reference backend contract
+    (backend.py:132-270). `engine` is the sm_100a library (GpuEngine) in the
+    product; tests may substitute the CPU oracle engine to check bit-exactness."""
+
+    def __init__(self, config: BackendConfig, params: CkksParams | None = None,
+                 engine=None, device: int = 0):
+        if params is None:
+            log_n = int(math.log2(config.slot_count)) + 1
+            params = kan_params(config.depth_budget, log_n=log_n)
+        if params.slot_count != config.slot_count:
+            raise ValueError(f"params give {params.slot_count} slots, config {config.slot_count}")
+        if config.depth_budget > params.depth:
+            raise ValueError(f"depth_budget {config.depth_budget} > chain depth {params.depth}")
+        self.config = config
+        self.params = params
+        self.counter = OpCounter()
+        self._tags = itertools.count()
+        if engine is None:
+            from .engine import GpuEngine
+            engine = GpuEngine(params, device)
+        self.engine = engine
+        self.n = params.n
+        self._enc_counter = itertools.count()
+        self._pt_cache: dict = {}
+        self._pt_cache_bytes = 0
+        self.pt_cache_limit = 8 << 30
+        self.engine.call("hk_keygen", C.c_uint64(self._seed("keys")))
+
+    # ------------------------------------------------------------------
+    # boundary plumbing
+    # ------------------------------------------------------------------
+
+    def _seed(self, what: str, idx: int = 0) -> int:
+        h = hashlib.blake2b(f"{self.config.rng_seed}:{what}:{idx}".encode(), digest_size=8)
+        return int.from_bytes(h.digest(), "little")
+
+    def encode(self, values) -> PlainVector:
+        """Zero-pad a vector (or broadcast a scalar) to the slot count (:149-158)."""
+        if np.isscalar(values):
+            return PlainVector(np.full(self.config.slot_count, float(values)))
+        arr = np.asarray(values, dtype=float).ravel()
+        if arr.size > self.config.slot_count:
+            raise InputTooLong(f"{arr.size} values > {self.config.slot_count} slots")
+        out = np.zeros(self.config.slot_count)
+        out[: arr.size] = arr
+        return PlainVector(out)
+
+    def encrypt(self, values, level: int | None = None) -> CipherText:
+        """Fresh RLWE encryption at `level` (:160-166). A 2-D input (B, n)
+        yields one batched ciphertext of B samples."""
+        if level is None:
+            level = self.config.depth_budget
+        if not 0 <= level <= self.config.depth_budget:
+            raise ValueError(f"level {level} outside [0, {self.config.depth_budget}]")
+        rows, batched = _slot_rows(values, self.config.slot_count)
+        return self._encrypt_rows(rows, level, batched)
+
+    def _encrypt_rows(self, rows: np.ndarray, level: int, batched: bool) -> CipherText:
+        eng, B = self.engine, rows.shape[0]
+        slots = eng.put_f64(rows)
+        pt = eng.alloc_u64((level + 1) * B * self.n)
+        eng.call("hk_encode", eng.addr(slots), B, level, self.params.scale(level), eng.addr(pt))
+        ct = eng.alloc_u64(2 * (level + 1) * B * self.n)
+        seed = self._seed("enc", next(self._enc_counter))
+        eng.call("hk_encrypt", eng.addr(pt), level, B, C.c_uint64(seed), eng.addr(ct))
+        return self._wrap(ct, level, B, batched)
+
+    def decrypt(self, a: CipherText) -> np.ndarray:
+        self._check_ours(a)
+        eng = self.engine
+        out = eng.alloc_f64(a.batch * self.config.slot_count)
+        eng.call("hk_decrypt", eng.addr(a.data), a.level, a.batch, self.params.scale(a.level),
+                 eng.addr(out))
+        vals = eng.get_f64(out).reshape(a.batch, self.config.slot_count)
+        return vals if a.batched else vals[0]
+
+    def refresh(self, a: CipherText, level: int | None = None) -> CipherText:
+        """Level reset (:172-180). The reference's zero-cost bootstrapping
+        stand-in; here a secret-key decrypt/re-encrypt debug path (real
+        bootstrapping is out of scope). No counts."""
+        if level is None:
+            level = self.config.depth_budget
+        self._check_ours(a)
+        vals = self.decrypt(a)
+        rows = vals if a.batched else vals[None, :]
+        return self._encrypt_rows(rows, level, a.batched)
+
+    def reset_counter(self) -> OpCounter:
+        old = self.counter
+        self.counter = OpCounter()
+        return old
+
+    # ------------------------------------------------------------------
+    # plaintext encoding cache
+    # ------------------------------------------------------------------
+
+    def _encoded(self, slots: np.ndarray, level: int, scale: float):
+        """Device plaintext u64 [level+1][1][N] for `slots`, cached."""
+        key = (hashlib.blake2b(np.ascontiguousarray(slots).view(np.uint8), digest_size=16).digest(),
+               level, scale)
+        hit = self._pt_cache.get(key)
+        if hit is not None:
+            return hit
+        eng = self.engine
+        dev = eng.put_f64(slots)
+        pt = eng.alloc_u64((level + 1) * self.n)
+        eng.call("hk_encode", eng.addr(dev), 1, level, scale, eng.addr(pt))
+        nbytes = (level + 1) * self.n * 8
+        if self._pt_cache_bytes + nbytes > self.pt_cache_limit:
+            self._pt_cache.clear()
+            self._pt_cache_bytes = 0
+        self._pt_cache[key] = pt
+        self._pt_cache_bytes += nbytes
+        return pt
+
+    def _const_residues(self, value: float, level: int, scale: float):
+        res = (C.c_uint64 * (level + 1))()
+        self.engine.call("hk_encode_const", C.c_double(value), level, C.c_double(scale), res)
+        return res
+
+    # ------------------------------------------------------------------
+    # homomorphic operations
+    # ------------------------------------------------------------------
+
+    def slotwise(self, op_kind: str, a: CipherText, b) -> CipherText:
+        """Element-wise add/sub/mul with a cipher or plain operand (:192-224)."""
+        if op_kind not in OP_KINDS:
+            raise ValueError(f"unknown op_kind {op_kind!r}")
+        self._check_ours(a)
+        is_ct = isinstance(b, CipherText)
+        if op_kind == "mul_ct" and not is_ct:
+            raise LengthMismatch("mul_ct requires a ciphertext right operand")
+        if op_kind == "mul_pt" and is_ct:
+            raise LengthMismatch("mul_pt requires a plaintext right operand")
+        if is_ct:
+            self._check_ours(b)
+            if b.batch != a.batch:
+                raise LengthMismatch(f"batch {a.batch} vs {b.batch}")
+            level = min(a.level, b.level)
+            b_slots = None
+        else:
+            b_slots = self._plain_slots(b)
+            level = a.level
+
+        eng, B, n = self.engine, a.batch, self.n
+        if op_kind in ("add", "sub"):
+            out = eng.alloc_u64(2 * (level + 1) * B * n)
+            if is_ct:
+                eng.call("hk_add" if op_kind == "add" else "hk_sub", eng.addr(a.data), a.level,
+                         eng.addr(b.data), b.level, eng.addr(out), B)
+            else:
+                c = _const_of(b_slots)
+                if c is not None:
+                    res = self._const_residues(c if op_kind == "add" else -c, level,
+                                               self.params.scale(level))
+                    eng.call("hk_add_const", eng.addr(a.data), a.level, res, eng.addr(out), B)
+                else:
+                    pt = self._encoded(b_slots, level, self.params.scale(level))
+                    eng.call("hk_add_plain", eng.addr(a.data), a.level, eng.addr(pt), level, 1,
+                             1 if op_kind == "sub" else 0, eng.addr(out), B)
+            if op_kind == "add":
+                self.counter.adds += 1
+            else:
+                self.counter.subs += 1
+        else:
+            if level < 1:
+                raise DepthExhausted(f"multiplication at level {level} (tag {a.tag})")
+            out = eng.alloc_u64(2 * level * B * n)
+            if is_ct:
+                eng.call("hk_mul", eng.addr(a.data), a.level, eng.addr(b.data), b.level,
+                         eng.addr(out), B)
+                self.counter.ct_mults += 1
+            else:
+                scale = self.params.pt_mult_scale(level)
+                c = _const_of(b_slots)
+                if c is not None:
+                    res = self._const_residues(c, level, scale)
+                    eng.call("hk_mul_const", eng.addr(a.data), a.level, res, eng.addr(out), B)
+                else:
+                    pt = self._encoded(b_slots, level, scale)
+                    eng.call("hk_mul_plain", eng.addr(a.data), a.level, eng.addr(pt), level, 1,
+                             eng.addr(out), B)
+                self.counter.pt_mults += 1
+            level -= 1
+        return self._wrap(out, level, B, a.batched or (is_ct and b.batched))
+
+    def add(self, a: CipherText, b) -> CipherText:
+        return self.slotwise("add", a, b)
+
+    def sub(self, a: CipherText, b) -> CipherText:
+        return self.slotwise("sub", a, b)
+
+    def mul(self, a: CipherText, b) -> CipherText:
+        kind = "mul_ct" if isinstance(b, CipherText) else "mul_pt"
+        return self.slotwise(kind, a, b)
+
+    def rotate(self, a: CipherText, t: int) -> CipherText:
+        """Cyclic shift: left for t > 0, right for t < 0 (:237-245)."""
+        self._check_ours(a)
+        if abs(t) >= self.config.slot_count:
+            raise ValueError(f"|t| = {abs(t)} must be < slot_count {self.config.slot_count}")
+        if t == 0:
+            return a
+        self.counter.rotations += 1
+        g = galois_element(t, self.config.slot_count)
+        self.ensure_galois_keys([g])
+        eng = self.engine
+        out = eng.alloc_u64(2 * (a.level + 1) * a.batch * self.n)
+        eng.call("hk_rotate", eng.addr(a.data), a.level, C.c_uint32(g), eng.addr(out), a.batch)
+        return self._wrap(out, a.level, a.batch, a.batched)
+
+    def rotate_many(self, a: CipherText, steps) -> list:
+        """Hoisted rotations of one source: one ModUp shared by every step
+        (the baby steps of bsgs_matvec, inference.py:162). Counts one rotation
+        per nonzero step, like calling rotate() per step."""
+        self._check_ours(a)
+        steps = [int(t) for t in steps]
+        for t in steps:
+            if abs(t) >= self.config.slot_count:
+                raise ValueError(f"|t| = {abs(t)} must be < slot_count {self.config.slot_count}")
+        todo = [t for t in steps if t != 0]
+        outs = {}
+        if todo:
+            gs = [galois_element(t, self.config.slot_count) for t in todo]
+            self.ensure_galois_keys(gs)
+            eng = self.engine
+            bufs = [eng.alloc_u64(2 * (a.level + 1) * a.batch * self.n) for _ in todo]
+            eng.call("hk_rotate_hoisted", eng.addr(a.data), a.level, eng.u32_array(gs), len(gs),
+                     eng.addr_array(bufs), a.batch)
+            self.counter.rotations += len(todo)
+            for t, buf in zip(todo, bufs):
+                outs[t] = self._wrap(buf, a.level, a.batch, a.batched)
+        return [a if t == 0 else outs[t] for t in steps]
+
+    def mac_plain(self, babies, plains) -> CipherText:
+        """sum_i babies[i] * plains[i] with ONE rescale (fused BSGS block,
+        inference.py:171-178). Counts len(babies) pt_mults and len-1 adds."""
+        n_terms = len(babies)
+        if n_terms == 0 or n_terms != len(plains):
+            raise LengthMismatch("mac_plain needs matching non-empty operand lists")
+        a0 = babies[0]
+        for x in babies:
+            self._check_ours(x)
+            if x.batch != a0.batch:
+                raise LengthMismatch("batch mismatch in mac_plain")
+        level = min(x.level for x in babies)
+        if level < 1:
+            raise DepthExhausted(f"multiplication at level {level}")
+        scale = self.params.pt_mult_scale(level)
+        pts = [self._encoded(self._plain_slots(p), level, scale) for p in plains]
+        eng, B = self.engine, a0.batch
+        if any(x.level != level for x in babies):
+            raise ValueError("mac_plain operands must share one level")
+        out = eng.alloc_u64(2 * level * B * self.n)
+        eng.call("hk_mac_plain", eng.addr_array([x.data for x in babies]), eng.addr_array(pts),
+                 n_terms, level, level, eng.addr(out), B)
+        self.counter.pt_mults += n_terms
+        self.counter.adds += n_terms - 1
+        return self._wrap(out, level - 1, B, a0.batched)
+
+    def ensure_galois_keys(self, galois_elts) -> None:
+        missing = [int(g) for g in galois_elts
+                   if not self.engine.lib.hk_has_galois_key(self.engine.ctx, C.c_uint32(int(g)))]
+        if missing:
+            missing = sorted(set(missing))
+            self.engine.call("hk_add_galois_keys", C.c_uint64(self._seed("galois")),
+                             self.engine.u32_array(missing), len(missing))
+
+    def ensure_rotation_keys(self, steps) -> None:
+        self.ensure_galois_keys([galois_element(t, self.config.slot_count)
+                                 for t in steps if t % self.config.slot_count])
+
+    # ------------------------------------------------------------------
+    # internals
+    # ------------------------------------------------------------------
+
+    def _plain_slots(self, b) -> np.ndarray:
+        if isinstance(b, PlainVector):
+            if b.slots.size != self.config.slot_count:
+                raise LengthMismatch(
+                    f"plain operand has {b.slots.size} slots, backend {self.config.slot_count}")
+            return b.slots
+        return self.encode(b).slots
+
+    def _check_ours(self, a) -> None:
+        if not isinstance(a, CipherText) or a.backend is not self:
+            raise LengthMismatch("ciphertext belongs to a different backend")
+
+    def _wrap(self, data, level: int, batch: int, batched: bool) -> CipherText:
+        consumed = self.config.depth_budget - level
+        if consumed > self.counter.max_depth_consumed:
+            self.counter.max_depth_consumed = consumed
+        return CipherText(data, level, f"ct{next(self._tags)}", self, batch, batched)
+
+    # ------------------------------------------------------------------
+    # raw access (parity tests, serialisation)
+    # ------------------------------------------------------------------
+
+    def export_ct(self, a: CipherText) -> np.ndarray:
+        """u64 [2][level+1][B][N] host copy of the RNS limbs."""
+        self.engine.sync()
+        return self.engine.get_u64(a.data).reshape(2, a.level + 1, a.batch, self.n)
+
+    def import_ct(self, limbs: np.ndarray, level: int, batched: bool = True) -> CipherText:
+        limbs = np.asarray(limbs, dtype=np.uint64)
+        B = limbs.shape[2]
+        if limbs.shape != (2, level + 1, B, self.n):
+            raise LengthMismatch(f"limb array shape {limbs.shape}")
+        return self._wrap(self.engine.put_u64(limbs), level, B, batched)
+
+
+CkksBackend = HeBackend
+
+
+def make_backend(config: BackendConfig, params: CkksParams | None = None, engine=None,
+                 device: int = 0) -> HeBackend:
+    """RNS-CKKS backend on the sm_100a engine (reference factory :293-297)."""
+    return HeBackend(config, params=params, engine=engine, device=device)
+
+
+def slotwise(op_kind: str, a: CipherText, b) -> CipherText:
+    return a.backend.slotwise(op_kind, a, b)
+
+
+def rotate(a: CipherText, t: int) -> CipherText:
+    return a.backend.rotate(a, t)
+
+
+def decrypt(a: CipherText) -> np.ndarray:
+    return a.backend.decrypt(a)

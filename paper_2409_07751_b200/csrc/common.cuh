@@ -1,0 +1,170 @@
+// common.cuh — shared device arithmetic and the engine context (sm_100a).
+//
+// All moduli are primes < 2^61 (the parameter generator keeps them < 2^50);
+// residues are canonical in [0, q) at every kernel boundary so results are
+// bit-identical to the CPU oracle (oracle/ckks_oracle.c).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/hekan.h"
+
+typedef unsigned __int128 u128;
+
+#define HK_MAX_MOD 128
+
+// ---------------------------------------------------------------------------
+// modular arithmetic
+// ---------------------------------------------------------------------------
+struct ModQ {
+    uint64_t q;    // prime
+    uint64_t mu;   // floor(2^(63+k) / q), k = bitlen(q)
+    uint32_t k;    // bit length of q
+};
+
+__device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) {
+    uint64_t s = a + b;
+    return s >= q ? s - q : s;
+}
+__device__ __forceinline__ uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t q) {
+    return a >= b ? a - b : a + q - b;
+}
+// Shoup: a * w mod q for any a < 2^64, wp = floor(w * 2^64 / q)
+__device__ __forceinline__ uint64_t mul_shoup(uint64_t a, uint64_t w, uint64_t wp, uint64_t q) {
+    uint64_t hi = __umul64hi(a, wp);
+    uint64_t r = a * w - hi * q;
+    return r >= q ? r - q : r;
+}
+// lazy Shoup: result in [0, 2q)
+__device__ __forceinline__ uint64_t mul_shoup_lazy(uint64_t a, uint64_t w, uint64_t wp, uint64_t q) {
+    return a * w - __umul64hi(a, wp) * q;
+}
+// Barrett on a 128-bit value x = hi:lo < 2^(2k): one mulhi estimate, <= 2 corrections
+__device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo, const ModQ &m) {
+    uint64_t t = (hi << (65 - m.k)) | (lo >> (m.k - 1));
+    uint64_t q3 = __umul64hi(t, m.mu);
+    uint64_t r = lo - q3 * m.q;
+    if (r >= m.q) r -= m.q;
+    if (r >= m.q) r -= m.q;
+    return r;
+}
+__device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const ModQ &m) {
+    return reduce128(__umul64hi(a, b), a * b, m);
+}
+// 128-bit accumulate
+__device__ __forceinline__ void mac128(uint64_t &hi, uint64_t &lo, uint64_t a, uint64_t b) {
+    uint64_t l = a * b, h = __umul64hi(a, b);
+    lo += l;
+    hi += h + (lo < l);
+}
+// reduce an arbitrary 128-bit value (hi may exceed the < q^2 bound): fold hi first
+__device__ __forceinline__ uint64_t reduce128_any(uint64_t hi, uint64_t lo, const ModQ &m,
+                                                  uint64_t two64_mod_q, uint64_t two64_sh) {
+    // hi*2^64 + lo = (hi mod q)*2^64 + lo  (mod q)
+    uint64_t h = mul_shoup(hi, two64_mod_q, two64_sh, m.q);  // hi * 2^64 mod q
+    uint64_t l = lo >= m.q ? lo % m.q : lo;
+    return add_mod(h, l, m.q);
+}
+
+__device__ __forceinline__ uint32_t brev_bits(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
+
+// counter-based randomness — identical formulas to the oracle
+__host__ __device__ __forceinline__ uint64_t hk_mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t hk_rng64(uint64_t seed, uint64_t stream, uint64_t ctr) {
+    return hk_mix64(hk_mix64(seed ^ hk_mix64(stream * 0xD1B54A32D192ED03ull)) + ctr);
+}
+__device__ __forceinline__ int64_t cbd21(uint64_t x) {
+    return (int64_t)__popcll(x & 0x1FFFFFull) - (int64_t)__popcll((x >> 21) & 0x1FFFFFull);
+}
+__device__ __forceinline__ uint64_t smod_dev(int64_t v, uint64_t q) {
+    if (v >= 0) return (uint64_t)v % q;
+    uint64_t m = (uint64_t)(-(v + 1)) % q;
+    return q - 1 - m;
+}
+enum { ST_SECRET = 1, ST_ENC_A = 2, ST_ENC_E = 3, ST_KEY_A = 0x100, ST_KEY_E = 0x200 };
+
+// ---------------------------------------------------------------------------
+// basis-conversion tables for one (source set -> target set) conversion
+// ---------------------------------------------------------------------------
+struct ConvTable {
+    int n_src, n_dst;
+    uint64_t *d_inv;      // [n_src]  (Q_src/q_i)^-1 mod q_i
+    uint64_t *d_inv_sh;   // [n_src]  Shoup companions
+    uint64_t *d_hat;      // [n_dst][n_src] (Q_src/q_i) mod t
+    int32_t *d_src_mod;   // [n_src]  chain index of each source prime
+    int32_t *d_dst_mod;   // [n_dst]  chain index of each target prime
+};
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct hk_ctx {
+    int log_n, n, slots, n_q, n_p, dnum, alpha, n_digits, n_mod;
+    int device;
+    cudaStream_t stream;
+    std::vector<uint64_t> mod_h;
+    std::vector<ModQ> modq_h;
+    // device tables
+    ModQ *d_modq;          // [n_mod]
+    ulonglong2 *d_tw;      // [n_mod][N] {psi^brv(k), shoup}
+    ulonglong2 *d_itw;     // [n_mod][N] {psi^-brv(k), shoup}
+    ulonglong2 *d_ninv;    // [n_mod] {N^-1, shoup}
+    double2 *d_zeta;       // [2N]
+    uint32_t *d_rot_group; // [S]
+    // rescale: qinv[l][i] = q_l^-1 mod q_i (i < l), Shoup pairs
+    ulonglong2 *d_rs_qinv; // [n_q][n_q]
+    // key switching: per (level, digit) ModUp tables; ModDown (P -> q) tables
+    std::vector<std::vector<ConvTable>> modup;  // [level][digit]
+    ConvTable moddown;                          // sources: specials, targets: q_0..q_{n_q-1}
+    ulonglong2 *d_pinv;                         // [n_q] P^-1 mod q_i
+    // keys
+    uint64_t *d_sk;                 // [n_mod][N]
+    uint64_t *d_relin;              // [n_digits][2][n_mod][N]
+    std::map<uint32_t, uint64_t *> gal;
+    bool have_keys;
+    // scratch workspace (grown on demand, stream-ordered use only)
+    void *ws;
+    size_t ws_bytes;
+    std::string err;
+};
+
+// error plumbing
+int hk_fail(hk_ctx *c, int code, const char *fmt, ...);
+int hk_cuda_check(hk_ctx *c, cudaError_t e, const char *what);
+#define HK_CUDA(c, call)                                                  \
+    do {                                                                  \
+        cudaError_t _e = (call);                                          \
+        if (_e != cudaSuccess) return hk_cuda_check((c), _e, #call);      \
+    } while (0)
+#define HK_LAUNCH_CHECK(c, what)                                          \
+    do {                                                                  \
+        cudaError_t _e = cudaGetLastError();                              \
+        if (_e != cudaSuccess) return hk_cuda_check((c), _e, what);       \
+    } while (0)
+
+// workspace: returns a pointer to at least `bytes` bytes (reallocates)
+void *hk_workspace(hk_ctx *c, size_t bytes);
+
+// internal launchers (defined across translation units)
+int ntt_fwd_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int batch, int limb_stride_polys);
+int ntt_inv_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int batch, int limb_stride_polys);
+int rescale_launch(hk_ctx *c, const uint64_t *in, int l, int batch, uint64_t *out, uint64_t *scratch);
+int keyswitch_launch(hk_ctx *c, const uint64_t *d, int l, int batch, const uint64_t *const *keys,
+                     const uint32_t *galois, int n_keys, uint64_t *const *outs_c0,
+                     const uint64_t *c0_src, bool add_c0_auto);
+
+static inline int hk_grid(long long work, int threads) {
+    long long b = (work + threads - 1) / threads;
+    if (b > (1ll << 30)) b = 1ll << 30;
+    return (int)(b < 1 ? 1 : b);
+}

@@ -1,0 +1,467 @@
+// ops.cu — slot-wise arithmetic, rescale, relinearised product, rotation.
+//
+// Each extern "C" entry replaces one branch of HeBackend.slotwise/rotate
+// (hekan/backend.py:192-245); see include/hekan.h for the argument contract.
+// Data layout: ct u64 [2][l+1][B][N] limb-major, NTT domain, canonical residues.
+//
+// Key switching is hybrid (Han-Ki): ModUp per digit of alpha primes (fast
+// basis conversion + NTT), key inner product (128-bit lazy accumulation over
+// digits, one Barrett reduction), ModDown by the special primes P.
+#include <algorithm>
+
+#include "common.cuh"
+
+int automorph_launch(hk_ctx *c, const uint64_t *in, uint64_t *out, uint32_t g, long long n_polys);
+
+namespace {
+
+constexpr int kMaxSrc = 48;     // basis-conversion sources per thread (alpha or n_p)
+constexpr int kMacMax = 64;     // operands per mac_plain launch
+
+struct Residues { uint64_t v[HK_MAX_MOD]; };
+struct PtrList { const uint64_t *p[kMacMax]; };
+
+__device__ __forceinline__ uint32_t auto_src(uint32_t j, uint32_t g, int log_n) {
+    const uint32_t M = 2u << log_n;
+    const uint32_t e = 2u * brev_bits(j, log_n) + 1u;
+    const uint32_t eg = (uint32_t)(((uint64_t)e * g) & (M - 1));
+    return brev_bits((eg - 1u) >> 1, log_n);
+}
+
+// ------------------------------------------------------------ add / sub
+__global__ void k_addsub(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb,
+                         uint64_t *__restrict__ out, int lo, long long BN, int neg, const ModQ *__restrict__ mq,
+                         long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;  // total = 2 (lo+1) B N
+    const long long pl = gid / BN, e = gid - pl * BN;
+    const int p = (int)(pl / (lo + 1)), l = (int)(pl - (long long)p * (lo + 1));
+    const uint64_t q = mq[l].q;
+    const uint64_t x = a[((long long)p * (la + 1) + l) * BN + e];
+    const uint64_t y = b[((long long)p * (lb + 1) + l) * BN + e];
+    out[gid] = neg ? sub_mod(x, y, q) : add_mod(x, y, q);
+}
+
+// c0 +/- pt (pt_batch 1 or B), c1 copied
+__global__ void k_add_plain(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ pt, int pb,
+                            int neg, uint64_t *__restrict__ out, int B, int log_n, const ModQ *__restrict__ mq,
+                            long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;  // total = 2 (la+1) B N
+    const long long poly = (long long)(la + 1) * B << log_n;
+    if (gid >= poly) { out[gid] = a[gid]; return; }
+    const int N = 1 << log_n;
+    const long long lb_ = gid >> log_n;
+    const int l = (int)(lb_ / B), b = (int)(lb_ - (long long)l * B), k = (int)(gid & (N - 1));
+    const uint64_t y = pt[((long long)l * pb + (pb == 1 ? 0 : b)) * N + k];
+    const uint64_t q = mq[l].q;
+    out[gid] = neg ? sub_mod(a[gid], y, q) : add_mod(a[gid], y, q);
+}
+
+__global__ void k_add_const(const uint64_t *__restrict__ a, int la, Residues r, uint64_t *__restrict__ out,
+                            long long BN, const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;
+    const long long poly = (long long)(la + 1) * BN;
+    if (gid >= poly) { out[gid] = a[gid]; return; }
+    const int l = (int)(gid / BN);
+    out[gid] = add_mod(a[gid], r.v[l], mq[l].q);
+}
+
+// tmp = a (.) pt for both polys (limbs 0..la)
+__global__ void k_mul_plain(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ pt, int pb,
+                            uint64_t *__restrict__ out, int B, int log_n, const ModQ *__restrict__ mq,
+                            long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;
+    const int N = 1 << log_n;
+    const long long poly = (long long)(la + 1) * B << log_n;
+    const long long e = gid >= poly ? gid - poly : gid;
+    const long long lb_ = e >> log_n;
+    const int l = (int)(lb_ / B), b = (int)(lb_ - (long long)l * B), k = (int)(e & (N - 1));
+    const uint64_t y = pt[((long long)l * pb + (pb == 1 ? 0 : b)) * N + k];
+    out[gid] = mul_mod(a[gid], y, mq[l]);
+}
+
+__global__ void k_mul_const(const uint64_t *__restrict__ a, int la, Residues r, uint64_t *__restrict__ out,
+                            long long BN, const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;
+    const long long poly = (long long)(la + 1) * BN;
+    const long long e = gid >= poly ? gid - poly : gid;
+    const int l = (int)(e / BN);
+    out[gid] = mul_mod(a[gid], r.v[l], mq[l]);
+}
+
+// out = sum_i babies[i] (.) pts[i], both polys; `init` adds the previous out
+__global__ void k_mac(PtrList babies, PtrList pts, int n, int la, uint64_t *__restrict__ out, int B, int log_n,
+                      int init, const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;
+    const int N = 1 << log_n;
+    const long long poly = (long long)(la + 1) * B << log_n;
+    const long long e = gid >= poly ? gid - poly : gid;
+    const int l = (int)((e >> log_n) / B), k = (int)(e & (N - 1));
+    uint64_t hi = 0, lo = init ? out[gid] : 0;
+    for (int i = 0; i < n; ++i) mac128(hi, lo, babies.p[i][gid], pts.p[i][(size_t)l * N + k]);
+    out[gid] = reduce128(hi, lo, mq[l]);
+}
+
+// ------------------------------------------------------------ rescale
+// R[i][pb][k] = centered(L[pb][k] mod q_l) mod q_i, i < l
+__global__ void k_rs_center(const uint64_t *__restrict__ L, uint64_t *__restrict__ R, int l, long long BN2,
+                            const ModQ *__restrict__ mq) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= BN2) return;
+    const uint64_t ql = mq[l].q, x = L[gid];
+    const bool neg = x > (ql >> 1);
+    const uint64_t mag = neg ? ql - x : x;
+    for (int i = 0; i < l; ++i) {
+        const uint64_t q = mq[i].q;
+        const uint64_t r = mag >= q ? mag % q : mag;
+        R[(long long)i * BN2 + gid] = neg ? (r ? q - r : 0) : r;
+    }
+}
+
+// out[p][i] = (in[p][i] - R[i][p]) * q_l^-1 ; in at level l, out at level l-1
+__global__ void k_rs_finish(const uint64_t *__restrict__ in, const uint64_t *__restrict__ R,
+                            uint64_t *__restrict__ out, int l, long long BN, const ulonglong2 *__restrict__ qinv,
+                            const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;  // 2 * l * BN
+    const long long pl = gid / BN, e = gid - pl * BN;
+    const int p = (int)(pl / l), i = (int)(pl - (long long)p * l);
+    const uint64_t q = mq[i].q;
+    const ulonglong2 w = qinv[i];
+    const uint64_t x = in[((long long)p * (l + 1) + i) * BN + e];
+    const uint64_t y = R[(long long)i * 2 * BN + (long long)p * BN + e];
+    out[gid] = mul_shoup(sub_mod(x, y, q), w.x, w.y, q);
+}
+
+// ------------------------------------------------------------ tensor product
+__global__ void k_tensor(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb, int l,
+                         uint64_t *__restrict__ d, long long BN, const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;  // (l+1) BN
+    const int i = (int)(gid / BN);
+    const ModQ m = mq[i];
+    const uint64_t a0 = a[gid], a1 = a[(long long)(la + 1) * BN + gid];
+    const uint64_t b0 = b[gid], b1 = b[(long long)(lb + 1) * BN + gid];
+    const long long pl = (long long)(l + 1) * BN;
+    d[gid] = mul_mod(a0, b0, m);
+    uint64_t hi = 0, lo = 0;
+    mac128(hi, lo, a0, b1);
+    mac128(hi, lo, a1, b0);
+    d[pl + gid] = reduce128(hi, lo, m);
+    d[2 * pl + gid] = mul_mod(a1, b1, m);
+}
+
+// ------------------------------------------------------------ key switching
+// fast basis conversion: dst[t] = sum_i [src_i * inv_i]_{q_i} * hat[t][i] mod q_t
+// mode 0 (ModUp): dst limb index of chain prime m = (m <= l ? m : l + 1 + m - n_q)
+// mode 1 (ModDown): dst limb index = target position d
+__global__ void k_conv(const uint64_t *__restrict__ src, int n_src, const uint64_t *__restrict__ inv,
+                       const uint64_t *__restrict__ inv_sh, const uint64_t *__restrict__ hat,
+                       const int32_t *__restrict__ src_mod, const int32_t *__restrict__ dst_mod, int n_dst,
+                       uint64_t *__restrict__ dst, int mode, int l, int n_q, long long BN,
+                       const ModQ *__restrict__ mq) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= BN) return;
+    uint64_t v[kMaxSrc];
+#pragma unroll 4
+    for (int i = 0; i < n_src; ++i) {
+        const uint64_t qi = mq[src_mod[i]].q;
+        v[i] = mul_shoup(src[(long long)i * BN + e], inv[i], inv_sh[i], qi);
+    }
+    for (int d = 0; d < n_dst; ++d) {
+        const int m = dst_mod[d];
+        const ModQ mt = mq[m];
+        const uint64_t *h = hat + (long long)d * n_src;
+        uint64_t hi = 0, lo = 0;
+        for (int i = 0; i < n_src; ++i) mac128(hi, lo, v[i], h[i]);
+        const int out_idx = mode == 0 ? (m <= l ? m : l + 1 + m - n_q) : d;
+        dst[(long long)out_idx * BN + e] = reduce128(hi, lo, mt);
+    }
+}
+
+// acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][chain(t)]  (t over l+1+n_p limbs)
+__global__ void k_key_ip(const uint64_t *__restrict__ ext, int nd, int ne, int l, int n_q, int nm, int B,
+                         int log_n, const uint64_t *__restrict__ key, uint32_t g, uint64_t *__restrict__ acc0,
+                         uint64_t *__restrict__ acc1, const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;  // ne * B * N
+    const int N = 1 << log_n;
+    const long long BN = (long long)B << log_n;
+    const int t = (int)(gid / BN);
+    const long long e = gid - (long long)t * BN;
+    const int k = (int)(e & (N - 1));
+    const long long src_e = g == 1u ? e : (e - k + auto_src((uint32_t)k, g, log_n));
+    const int m = t <= l ? t : n_q + (t - l - 1);
+    const ModQ mm = mq[m];
+    uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    for (int j = 0; j < nd; ++j) {
+        const uint64_t x = ext[((long long)j * ne + t) * BN + src_e];
+        const uint64_t *kj = key + ((size_t)j * 2 * nm + m) * N;
+        mac128(h0, l0, x, kj[k]);
+        mac128(h1, l1, x, kj[(size_t)nm * N + k]);
+    }
+    acc0[gid] = reduce128(h0, l0, mm);
+    acc1[gid] = reduce128(h1, l1, mm);
+}
+
+// out_i = (acc_i - conv_i) * P^-1 (+ optional addend, optionally automorphed)
+__global__ void k_md_finish(const uint64_t *__restrict__ acc, const uint64_t *__restrict__ conv,
+                            uint64_t *__restrict__ out, const uint64_t *__restrict__ addend, uint32_t g,
+                            int log_n, long long BN, const ulonglong2 *__restrict__ pinv,
+                            const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;  // (l+1) BN
+    const int i = (int)(gid / BN);
+    const uint64_t q = mq[i].q;
+    const ulonglong2 w = pinv[i];
+    uint64_t r = mul_shoup(sub_mod(acc[gid], conv[gid], q), w.x, w.y, q);
+    if (addend) {
+        long long src = gid;
+        if (g != 1u) {
+            const int N = 1 << log_n;
+            const int k = (int)(gid & (N - 1));
+            src = gid - k + auto_src((uint32_t)k, g, log_n);
+        }
+        r = add_mod(r, addend[src], q);
+    }
+    out[gid] = r;
+}
+
+}  // namespace
+
+// words of scratch the key switch at level l needs
+static size_t ks_scratch_words(const hk_ctx *c, int l, int B) {
+    const size_t BN = (size_t)B * c->n;
+    const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    return BN * ((size_t)(l + 1) + (size_t)nd * ne + 2 * (size_t)ne + c->n_p + (l + 1));
+}
+
+static size_t rs_scratch_words(const hk_ctx *c, int l, int B) {
+    return (size_t)B * c->n * (2 + 2 * (size_t)l);
+}
+
+int rescale_launch(hk_ctx *c, const uint64_t *in, int l, int B, uint64_t *out, uint64_t *scratch) {
+    const long long BN = (long long)B * c->n;
+    uint64_t *L = scratch, *R = scratch + 2 * BN;
+    HK_CUDA(c, cudaMemcpyAsync(L, in + (long long)l * BN, sizeof(uint64_t) * BN, cudaMemcpyDeviceToDevice,
+                               c->stream));
+    HK_CUDA(c, cudaMemcpyAsync(L + BN, in + (long long)(2 * l + 1) * BN, sizeof(uint64_t) * BN,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    int rc = ntt_inv_launch(c, L, l, 1, 2 * B, 0);
+    if (rc) return rc;
+    k_rs_center<<<hk_grid(2 * BN, 256), 256, 0, c->stream>>>(L, R, l, 2 * BN, c->d_modq);
+    rc = ntt_fwd_launch(c, R, 0, l, 2 * B, 0);
+    if (rc) return rc;
+    const long long total = 2LL * l * BN;
+    k_rs_finish<<<hk_grid(total, 256), 256, 0, c->stream>>>(in, R, out, l, BN, c->d_rs_qinv + (size_t)l * c->n_q,
+                                                               c->d_modq, total);
+    HK_LAUNCH_CHECK(c, "rescale");
+    return HK_OK;
+}
+
+// Key switch d (NTT, [l+1][B][N]) under n keys; for key r writes
+//   out0[r] = ks0 (+ sigma_g(add0) if add0) and out1[r] = ks1, each [l+1][B][N].
+static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
+                     const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
+                     uint64_t *scratch) {
+    const int N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
+    const long long BN = (long long)B * N;
+    uint64_t *dc = scratch;
+    uint64_t *ext = dc + (size_t)(l + 1) * BN;
+    uint64_t *acc = ext + (size_t)nd * ne * BN;
+    uint64_t *sp = acc + (size_t)2 * ne * BN;
+    uint64_t *conv = sp + (size_t)np * BN;
+    // ModUp
+    HK_CUDA(c, cudaMemcpyAsync(dc, d, sizeof(uint64_t) * (l + 1) * BN, cudaMemcpyDeviceToDevice, c->stream));
+    int rc = ntt_inv_launch(c, dc, 0, l + 1, B, 0);
+    if (rc) return rc;
+    for (int j = 0; j < nd; ++j) {
+        const ConvTable &T = c->modup[l][j];
+        const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, l + 1);
+        uint64_t *ej = ext + (size_t)j * ne * BN;
+        if (T.n_src > kMaxSrc) return hk_fail(c, HK_E_ARG, "digit of %d primes exceeds %d", T.n_src, kMaxSrc);
+        k_conv<<<hk_grid(BN, 128), 128, 0, c->stream>>>(dc + (size_t)d0 * BN, T.n_src, T.d_inv, T.d_inv_sh,
+                                                         T.d_hat, T.d_src_mod, T.d_dst_mod, T.n_dst, ej, 0, l,
+                                                         c->n_q, BN, c->d_modq);
+        HK_LAUNCH_CHECK(c, "modup conv");
+        if (d0 > 0 && (rc = ntt_fwd_launch(c, ej, 0, d0, B, 0))) return rc;
+        if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
+        if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
+        HK_CUDA(c, cudaMemcpyAsync(ej + (size_t)d0 * BN, d + (size_t)d0 * BN, sizeof(uint64_t) * (d1 - d0) * BN,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+    }
+    // per key: inner product, ModDown of both halves
+    for (int r = 0; r < n; ++r) {
+        const long long tot = (long long)ne * BN;
+        k_key_ip<<<hk_grid(tot, 256), 256, 0, c->stream>>>(ext, nd, ne, l, c->n_q, c->n_mod, B, c->log_n, keys[r],
+                                                            gal[r], acc, acc + (size_t)ne * BN, c->d_modq, tot);
+        HK_LAUNCH_CHECK(c, "key inner product");
+        for (int p = 0; p < 2; ++p) {
+            const uint64_t *a = acc + (size_t)p * ne * BN;
+            HK_CUDA(c, cudaMemcpyAsync(sp, a + (size_t)(l + 1) * BN, sizeof(uint64_t) * np * BN,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+            if ((rc = ntt_inv_launch(c, sp, c->n_q, np, B, 0))) return rc;
+            const ConvTable &T = c->moddown;
+            k_conv<<<hk_grid(BN, 128), 128, 0, c->stream>>>(sp, T.n_src, T.d_inv, T.d_inv_sh, T.d_hat, T.d_src_mod,
+                                                             T.d_dst_mod, l + 1, conv, 1, l, c->n_q, BN, c->d_modq);
+            HK_LAUNCH_CHECK(c, "moddown conv");
+            if ((rc = ntt_fwd_launch(c, conv, 0, l + 1, B, 0))) return rc;
+            const long long t2 = (long long)(l + 1) * BN;
+            k_md_finish<<<hk_grid(t2, 256), 256, 0, c->stream>>>(a, conv, p == 0 ? out0[r] : out1[r],
+                                                                  p == 0 ? add0 : nullptr, gal[r], c->log_n, BN,
+                                                                  c->d_pinv, c->d_modq, t2);
+            HK_LAUNCH_CHECK(c, "moddown finish");
+        }
+    }
+    return HK_OK;
+}
+
+extern "C" {
+
+int hk_add(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *o, int32_t B) {
+    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "add: level out of range");
+    const int lo = std::min(la, lb);
+    const long long BN = (long long)B * c->n, total = 2LL * (lo + 1) * BN;
+    k_addsub<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 0, c->d_modq, total);
+    HK_LAUNCH_CHECK(c, "add");
+    return HK_OK;
+}
+
+int hk_sub(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *o, int32_t B) {
+    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "sub: level out of range");
+    const int lo = std::min(la, lb);
+    const long long BN = (long long)B * c->n, total = 2LL * (lo + 1) * BN;
+    k_addsub<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 1, c->d_modq, total);
+    HK_LAUNCH_CHECK(c, "sub");
+    return HK_OK;
+}
+
+int hk_add_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, int32_t lp, int32_t pb,
+                 int32_t negate, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q || lp < la) return hk_fail(c, HK_E_ARG, "add_plain: level mismatch");
+    if (pb != 1 && pb != B) return hk_fail(c, HK_E_LENGTH, "add_plain: plaintext batch");
+    const long long total = 2LL * (la + 1) * B * c->n;
+    k_add_plain<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, pt, pb, negate, out, B, c->log_n, c->d_modq,
+                                                              total);
+    HK_LAUNCH_CHECK(c, "add_plain");
+    return HK_OK;
+}
+
+int hk_add_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q) return hk_fail(c, HK_E_ARG, "add_const: level");
+    Residues r;
+    for (int l = 0; l <= la; ++l) r.v[l] = res[l];
+    const long long BN = (long long)B * c->n, total = 2LL * (la + 1) * BN;
+    k_add_const<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, r, out, BN, c->d_modq, total);
+    HK_LAUNCH_CHECK(c, "add_const");
+    return HK_OK;
+}
+
+int hk_rescale(hk_ctx *c, const uint64_t *a, int32_t la, uint64_t *out, int32_t B) {
+    if (la < 1 || la >= c->n_q) return hk_fail(c, HK_E_DEPTH, "rescale at level %d", la);
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
+    if (!ws) return hk_fail(c, HK_E_NOMEM, "rescale workspace");
+    return rescale_launch(c, a, la, B, out, ws);
+}
+
+int hk_mul_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, int32_t lp, int32_t pb,
+                 uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q || lp < la) return hk_fail(c, HK_E_ARG, "mul_plain: level mismatch");
+    if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
+    if (pb != 1 && pb != B) return hk_fail(c, HK_E_LENGTH, "mul_plain: plaintext batch");
+    const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
+    if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_plain workspace");
+    k_mul_plain<<<hk_grid(tot, 256), 256, 0, c->stream>>>(a, la, pt, pb, ws, B, c->log_n, c->d_modq, tot);
+    HK_LAUNCH_CHECK(c, "mul_plain");
+    return rescale_launch(c, ws, la, B, out, ws + tot);
+}
+
+int hk_mul_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q) return hk_fail(c, HK_E_ARG, "mul_const: level");
+    if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
+    Residues r;
+    for (int l = 0; l <= la; ++l) r.v[l] = res[l];
+    const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
+    if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_const workspace");
+    k_mul_const<<<hk_grid(tot, 256), 256, 0, c->stream>>>(a, la, r, ws, BN, c->d_modq, tot);
+    HK_LAUNCH_CHECK(c, "mul_const");
+    return rescale_launch(c, ws, la, B, out, ws + tot);
+}
+
+int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const *pts, int32_t n, int32_t la,
+                 int32_t lp, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q || lp < la || n < 1) return hk_fail(c, HK_E_ARG, "mac_plain: args");
+    if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
+    const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
+    if (!ws) return hk_fail(c, HK_E_NOMEM, "mac_plain workspace");
+    for (int s = 0; s < n; s += kMacMax) {
+        const int cnt = std::min(kMacMax, n - s);
+        PtrList bl, pl;
+        for (int i = 0; i < cnt; ++i) {
+            bl.p[i] = babies[s + i];
+            pl.p[i] = pts[s + i];
+        }
+        k_mac<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bl, pl, cnt, la, ws, B, c->log_n, s > 0, c->d_modq, tot);
+    }
+    HK_LAUNCH_CHECK(c, "mac_plain");
+    return rescale_launch(c, ws, la, B, out, ws + tot);
+}
+
+int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {
+    if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "mul: level");
+    const int l = std::min(la, lb);
+    if (l < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", l);
+    const long long BN = (long long)B * c->n, pl = (long long)(l + 1) * BN;
+    const size_t extra = std::max(ks_scratch_words(c, l, B), rs_scratch_words(c, l, B));
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (5 * pl + extra));
+    if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
+    uint64_t *d = ws, *ks = ws + 3 * pl, *scr = ws + 5 * pl;
+    k_tensor<<<hk_grid(pl, 256), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq, pl);
+    HK_LAUNCH_CHECK(c, "tensor");
+    uint64_t *o0 = ks, *o1 = ks + pl;
+    const uint64_t *keys[1] = {c->d_relin};
+    const uint32_t g1[1] = {1u};
+    int rc = keyswitch(c, d + 2 * pl, l, B, 1, keys, g1, &o0, &o1, nullptr, scr);
+    if (rc) return rc;
+    // d0 += ks0, d1 += ks1 (d0, d1 contiguous = a level-l ciphertext)
+    const long long tot = 2 * pl;
+    k_addsub<<<hk_grid(tot, 256), 256, 0, c->stream>>>(d, l, ks, l, d, l, BN, 0, c->d_modq, tot);
+    HK_LAUNCH_CHECK(c, "relin add");
+    return rescale_launch(c, d, l, B, out, scr);
+}
+
+int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *gs, int32_t n,
+                      uint64_t *const *outs, int32_t B) {
+    if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || la >= c->n_q) return hk_fail(c, HK_E_ARG, "rotate: level");
+    if (n < 1) return HK_OK;
+    std::vector<const uint64_t *> keys(n);
+    std::vector<uint64_t *> o0(n), o1(n);
+    const long long pl = (long long)(la + 1) * B * c->n;
+    for (int i = 0; i < n; ++i) {
+        auto it = c->gal.find(gs[i]);
+        if (it == c->gal.end()) return hk_fail(c, HK_E_NOKEY, "no galois key for element %u", gs[i]);
+        keys[i] = it->second;
+        o0[i] = outs[i];
+        o1[i] = outs[i] + pl;
+    }
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * ks_scratch_words(c, la, B));
+    if (!ws) return hk_fail(c, HK_E_NOMEM, "rotate workspace");
+    return keyswitch(c, a + pl, la, B, n, keys.data(), gs, o0.data(), o1.data(), a, ws);
+}
+
+int hk_rotate(hk_ctx *c, const uint64_t *a, int32_t la, uint32_t g, uint64_t *out, int32_t B) {
+    uint64_t *outs[1] = {out};
+    return hk_rotate_hoisted(c, a, la, &g, 1, outs, B);
+}
+
+}  // extern "C"

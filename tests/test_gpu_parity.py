@@ -1,0 +1,121 @@
+"""Bit-exact parity: the sm_100a library vs the CPU oracle, op by op.
+
+Same parameters, same seeds, same inputs -> identical u64 limbs (canonical
+residues) for every C-ABI entry point in include/hekan.h. Sizes cover the
+generic per-stage NTT path (small N) and the N = 2^16 fast path.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2409_07751_b200.backend import BackendConfig, HeBackend, galois_element
+from paper_2409_07751_b200.params import make_params, microbench_params
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(5, 6), (10, 4), (13, 3), (16, 3)]
+
+
+def _pair(log_n, depth, seed=0, dnum=3):
+    from oracle.engine import OracleEngine
+    from paper_2409_07751_b200.engine import GpuEngine
+    p = make_params(log_n, depth, dnum=dnum)
+    cfg = BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=seed)
+    g = HeBackend(cfg, p, engine=GpuEngine(p))
+    o = HeBackend(cfg, p, engine=OracleEngine(p))
+    return g, o, p
+
+
+def _same(g, o, cg, co, what):
+    a, b = g.export_ct(cg), o.export_ct(co)
+    assert a.shape == b.shape, what
+    bad = np.count_nonzero(a != b)
+    assert bad == 0, f"{what}: {bad} of {a.size} limbs differ"
+
+
+@pytest.mark.parametrize("log_n,depth", CASES)
+def test_ntt_roundtrip_and_parity(gpu_lib, log_n, depth):
+    import torch
+    from oracle.engine import OracleEngine
+    from paper_2409_07751_b200.engine import GpuEngine
+    p = make_params(log_n, depth)
+    ge, oe = GpuEngine(p), OracleEngine(p)
+    rng = np.random.default_rng(log_n)
+    nl, B, N = len(p.q) + len(p.p), 3, p.n
+    mods = np.array(list(p.q) + list(p.p), dtype=np.uint64)
+    x = (rng.integers(0, 1 << 62, size=(nl, B, N), dtype=np.uint64) % mods[:, None, None]).astype(np.uint64)
+    gb, ob = ge.put_u64(x), oe.put_u64(x)
+    ge.call("hk_ntt_fwd", ge.addr(gb), 0, nl, B)
+    oe.call("hk_ntt_fwd", oe.addr(ob), 0, nl, B)
+    ge.sync()
+    assert np.array_equal(ge.get_u64(gb), oe.get_u64(ob))
+    ge.call("hk_ntt_inv", ge.addr(gb), 0, nl, B)
+    ge.sync()
+    assert np.array_equal(ge.get_u64(gb), x.ravel())
+
+
+@pytest.mark.parametrize("log_n,depth", CASES)
+def test_keys_encrypt_bitexact(gpu_lib, log_n, depth):
+    g, o, p = _pair(log_n, depth)
+    for which in (0, 1):
+        n = g.engine.lib.hk_key_words(g.engine.ctx, which)
+        kg, ko = g.engine.alloc_u64(n), o.engine.alloc_u64(n)
+        g.engine.call("hk_export_key", which, 0, g.engine.addr(kg))
+        o.engine.call("hk_export_key", which, 0, o.engine.addr(ko))
+        g.engine.sync()
+        assert np.array_equal(g.engine.get_u64(kg), o.engine.get_u64(ko)), f"key {which}"
+    x = np.random.default_rng(1).uniform(-1, 1, (2, p.slot_count))
+    cg, co = g.encrypt(x), o.encrypt(x)
+    _same(g, o, cg, co, "encrypt")
+    np.testing.assert_array_equal(g.decrypt(cg), o.decrypt(co))
+    assert np.abs(g.decrypt(cg) - x).max() < 1e-6
+
+
+@pytest.mark.parametrize("log_n,depth", CASES)
+def test_ops_bitexact(gpu_lib, log_n, depth):
+    g, o, p = _pair(log_n, depth)
+    S = p.slot_count
+    rng = np.random.default_rng(7)
+    x, y, w = (rng.uniform(-1, 1, (2, S)) for _ in range(3))
+    ga, gb = g.encrypt(x), g.encrypt(y)
+    oa, ob = o.encrypt(x), o.encrypt(y)
+    pv = w[0]
+    steps = [1, -1, 3, S // 4]
+    checks = [
+        ("add", lambda be, a, b: be.add(a, b)),
+        ("sub", lambda be, a, b: be.sub(a, b)),
+        ("add_pt", lambda be, a, b: be.add(a, pv)),
+        ("sub_pt", lambda be, a, b: be.sub(a, pv)),
+        ("add_const", lambda be, a, b: be.add(a, 0.375)),
+        ("mul_pt", lambda be, a, b: be.mul(a, pv)),
+        ("mul_const", lambda be, a, b: be.mul(a, -1.25)),
+        ("mul_ct", lambda be, a, b: be.mul(a, b)),
+        ("mul_ct_levels", lambda be, a, b: be.mul(be.mul(a, 0.5), b)),
+        ("add_levels", lambda be, a, b: be.add(be.mul(a, 0.5), b)),
+        ("rot", lambda be, a, b: be.rotate(a, 1)),
+        ("rot_neg", lambda be, a, b: be.rotate(a, -3)),
+        ("mac", lambda be, a, b: be.mac_plain([a, b], [pv, w[1]])),
+    ]
+    for name, fn in checks:
+        _same(g, o, fn(g, ga, gb), fn(o, oa, ob), name)
+    for cg, co in zip(g.rotate_many(ga, steps), o.rotate_many(oa, steps)):
+        _same(g, o, cg, co, "hoisted")
+    # values are right, too
+    np.testing.assert_allclose(g.decrypt(g.mul(ga, gb)), x * y, atol=1e-6)
+    np.testing.assert_allclose(g.decrypt(g.rotate(ga, 3)), np.roll(x, -3, axis=1), atol=1e-6)
+
+
+def test_microbench_params_bitexact(gpu_lib):
+    """BASELINE config 2 parameters (24 x 50-bit limbs, dnum 3, alpha 8)."""
+    from oracle.engine import OracleEngine
+    from paper_2409_07751_b200.engine import GpuEngine
+    p = microbench_params()
+    cfg = BackendConfig(slot_count=p.slot_count, depth_budget=p.depth)
+    g = HeBackend(cfg, p, engine=GpuEngine(p))
+    o = HeBackend(cfg, p, engine=OracleEngine(p))
+    x = np.random.default_rng(3).uniform(-1, 1, p.slot_count)
+    ga, oa = g.encrypt(x), o.encrypt(x)
+    _same(g, o, g.mul(ga, ga), o.mul(oa, oa), "mul")
+    _same(g, o, g.rotate(ga, 1 << 14), o.rotate(oa, 1 << 14), "rotate")
