@@ -1,0 +1,518 @@
+#!/usr/bin/env python
+"""Encrypted-KAN throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference]
+                  [--config c1] [--batch B] [--log-n 16]
+
+A step = one encrypted forward pass (`model_forward_he`) of the config's KAN
+over one batch of B ciphertexts (one sample per ciphertext, as
+`encrypt_input`, /root/reference/pkg/src/hekan/inference.py:115-124) on the
+sm_100a RNS-CKKS engine, N = 2^16, depth 36 (L = 37 limbs: the planner total,
+SURVEY §0.3). Inputs are already resident in HBM when the timed region starts;
+each ciphertext batch is 4.7 GB, far larger than the 126 MB L2, so no explicit
+flush is needed between steps. `e2e` times the public API end to end from host
+memory: encrypt_input (host slots -> HBM) + model_forward_he + decrypt (-> host).
+
+Multi-GPU (torchrun): every rank runs its own batch (weak scaling, the path
+shards by ciphertext with no data-path collective); the barrier +
+max-over-ranks device time gives the job time; value = total inferences / s.
+
+`--impl reference` times the CPU implementation of the same path: the
+oracle port (oracle/libckks_oracle.so, OpenMP over all host cores) running the
+identical program on a bounded sample (a prefix of one inference's op stream).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def _peaks():
+    try:
+        with open(PEAKS_PATH) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sms.append(float(parts[1]))
+                    maxes.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, val in zip(names, parts[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        loaded = [s for s in sms if s > 500] or sms
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, value: float, device) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# product arm
+# ---------------------------------------------------------------------------
+def run_product(args):
+    import torch
+
+    from paper_2409_07751_b200 import configs, inference as inf
+    from paper_2409_07751_b200.backend import BackendConfig, make_backend
+    from paper_2409_07751_b200.params import kan_params
+
+    world, rank, local = dist_setup(args.gpus)
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    cfg, model, inputs = configs.workload(args.config)
+    B = args.batch or cfg.batch
+    inputs = inputs[:B] if B <= inputs.shape[0] else np.resize(inputs, (B, inputs.shape[1]))
+    pcfg = inf.PipelineConfig()
+    depth = inf.plan_model(model, pcfg).total
+    params = kan_params(depth, log_n=args.log_n)
+    be = make_backend(BackendConfig(slot_count=params.slot_count, depth_budget=depth, rng_seed=rank),
+                      params=params, device=local)
+    eng = be.engine
+
+    chunk = min(args.chunk or B, B)
+    parts = [inputs[i:i + chunk] for i in range(0, B, chunk)]
+    cts_in = [inf.encrypt_input(x, model, be) for x in parts]
+
+    def step(cts):
+        outs = []
+        for ct in cts:
+            o, st = inf.model_forward_he(model, ct, pcfg)
+            outs.append(o)
+        return outs, st
+
+    outs, stats = step(cts_in)     # generates Galois keys + plaintext caches
+    dec = np.concatenate([be.decrypt(o) for o in outs])[:, :model.n_out]
+    del outs
+    err = None
+    gpath = os.path.join(ROOT, "tests", "golden", f"{args.config}.npz")
+    if os.path.exists(gpath) and args.log_n == 16:
+        gold = np.load(gpath)["mirrored"]
+        n = min(B, gold.shape[0])
+        err = float(np.max(np.abs(dec[:n] - gold[:n])))
+    for _ in range(args.warmup):
+        step(cts_in)
+    torch.cuda.synchronize(device)
+
+    stream = torch.cuda.current_stream(device)
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    barrier(world)
+    torch.cuda.synchronize(device)
+    l0 = eng.lib.hk_launch_count(eng.ctx)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(cts_in)
+    ev1.record(stream)
+    torch.cuda.synchronize(device)
+    barrier(world)
+    launches = int(eng.lib.hk_launch_count(eng.ctx) - l0)
+    ms = max_over_ranks(world, ev0.elapsed_time(ev1), device) / args.steps
+    clk = clocks.stop() if clocks else None
+
+    # ---- e2e through the public API from host memory
+    host_in = torch.from_numpy(np.ascontiguousarray(inputs)).pin_memory()
+    barrier(world)
+    torch.cuda.synchronize(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    host_np = host_in.numpy()
+    for _ in range(max(1, args.steps)):
+        for i in range(0, B, chunk):
+            ct = inf.encrypt_input(host_np[i:i + chunk], model, be)
+            o, _ = inf.model_forward_he(model, ct, pcfg)
+            res = be.decrypt(o)
+            del ct, o
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    e2e_ms = max_over_ranks(world, e0.elapsed_time(e1), device) / max(1, args.steps)
+    S = params.slot_count
+    h2d = B * S * 8          # zero-padded slot rows uploaded by encrypt
+    d2h = B * S * 8          # decrypted slot vectors
+
+    # ---- dominant kernels: NTT and key switch, live CUDA-event timing
+    del cts_in
+    torch.cuda.empty_cache()
+    roof = kernel_rooflines(be, params, chunk, stream) if rank == 0 else None
+
+    if rank != 0:
+        return
+    total_inf = B * world
+    value = total_inf / (ms / 1e3)
+    hbm, hbm_kind = _peaks()
+    line = {
+        "metric": "encrypted KAN inferences/sec",
+        "value": round(value, 4),
+        "unit": "inferences/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64 (RNS residues mod <=50-bit primes)",
+        "data": "synthetic (seeded PCG64, SURVEY §8d)",
+        "config": {"workload": f"{args.config}: KAN {list(cfg.dims)} G={cfg.g} k={cfg.k}, "
+                               f"{B} ciphertexts/GPU in chunks of {chunk}, RNS-CKKS N=2^{args.log_n} L={depth} "
+                               f"dnum={params.dnum} alpha={params.alpha}",
+                   "global_batch": total_inf, "parallelism": f"dp{world} (ciphertext sharding)",
+                   "l2": "inputs 4.7 GB/GPU >> 126 MB L2 (no flush needed)"},
+        "e2e": {"value": round(total_inf / (e2e_ms / 1e3), 4), "unit": "inferences/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "encrypt_input + model_forward_he + decrypt, host slots in/out"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "max_abs_err_vs_reference_mirrored": err,
+        "counts_per_inference": stats.to_json()["total"],
+    }
+    if roof:
+        line["roofline"] = roof["ntt"]
+        line["roofline"]["peak_kind"] = hbm_kind
+        line["kernels"] = roof
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
+    print(json.dumps(line))
+
+
+def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
+    """CUDA-event timings of the two dominant primitives at c1 shapes."""
+    import ctypes as C
+
+    import torch
+    eng = be.engine
+    hbm, _ = _peaks()
+    N = params.n
+    out = {}
+    nl = params.depth + 1
+    buf = eng.alloc_u64(nl * B * N)
+    buf.zero_()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    eng.call("hk_ntt_fwd", eng.addr(buf), 0, nl, B)
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for _ in range(reps):
+        eng.call("hk_ntt_fwd", eng.addr(buf), 0, nl, B)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    t = ev[0].elapsed_time(ev[1]) / reps / 1e3
+    alg = 2.0 * nl * B * N * 8
+    ach = alg / t / 1e9
+    out["ntt"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                  "frac": round(ach / hbm, 4), "traffic": None,
+                  "kernel": f"hk_ntt_fwd (ntt16_fwd_cols + ntt16_fwd_rows), {nl} limbs x {B} polys",
+                  "algorithmic_bytes": alg, "ms": round(t * 1e3, 3)}
+    del buf
+    # key switch via one rotation at the top level (ModUp + IP + ModDown)
+    x = np.zeros((B, params.slot_count))
+    ct = be.encrypt(x)
+    be.rotate(ct, 1)
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for _ in range(reps):
+        be.rotate(ct, 1)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    t = ev[0].elapsed_time(ev[1]) / reps / 1e3
+    l = params.depth
+    alpha, n_p = params.alpha, len(params.p)
+    nd = l // alpha + 1
+    alg = B * 4 * (l + 1) * N * 8 + 2 * nd * (l + 1 + n_p) * N * 8
+    ach = alg / t / 1e9
+    out["keyswitch"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(ach / hbm, 4), "traffic": None,
+                        "kernel": f"hk_rotate (ModUp+KeyIP+ModDown) level {l}, {B} cts",
+                        "algorithmic_bytes": alg, "ms": round(t * 1e3, 3)}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on host cores
+# ---------------------------------------------------------------------------
+def cpu_baseline(args, budget_s: float = 20.0) -> dict:
+    """Oracle port, all host threads, one c1 sample at full N: runs the op
+    stream of one inference until `budget_s` is spent, then scales by the
+    fraction of the (pre-measured on GPU) program completed, counted in
+    logical ops weighted by level (limb count)."""
+    from oracle.engine import OracleEngine
+    from paper_2409_07751_b200 import configs, inference as inf
+    from paper_2409_07751_b200.backend import BackendConfig, HeBackend
+    from paper_2409_07751_b200.params import kan_params
+
+    cores = len(os.sched_getaffinity(0))
+    cfg, model, inputs = configs.workload(args.config, batch=1)
+    pcfg = inf.PipelineConfig()
+    depth = inf.plan_model(model, pcfg).total
+    params = kan_params(depth, log_n=args.log_n)
+    t_setup = time.perf_counter()
+    be = BudgetBackend(BackendConfig(slot_count=params.slot_count, depth_budget=depth), params,
+                       engine=OracleEngine(params))
+    be.prepare_keys_for(model, pcfg)
+    setup = time.perf_counter() - t_setup
+    ct = inf.encrypt_input(inputs, model, be)
+    be.start(budget_s)
+    t0 = time.perf_counter()
+    try:
+        inf.model_forward_he(model, ct, pcfg)
+        done = True
+    except _Budget:
+        done = False
+    el = time.perf_counter() - t0
+    frac = 1.0 if done else be.weight_done / max(be.total_weight(model, pcfg), 1e-9)
+    inf_per_s = frac / el if el > 0 else 0.0
+    return {"value": round(inf_per_s, 6), "unit": "inferences/s", "cores": cores, "kind": "port",
+            "sample": (f"oracle/libckks_oracle.so (OpenMP {cores} threads), {args.config} one ciphertext, "
+                       f"N=2^{args.log_n}; ran {'the full inference' if done else f'{frac:.1%} of one inference (level-weighted op prefix)'} "
+                       f"in {el:.1f} s; keygen/setup {setup:.1f} s untimed")}
+
+
+class _Budget(Exception):
+    pass
+
+
+from paper_2409_07751_b200.backend import HeBackend  # noqa: E402  (torch-free import)
+
+
+class BudgetBackend(HeBackend):
+    """HeBackend with an op-weight meter and a wall-clock budget."""
+
+    weight_done = 0.0
+    _deadline = None
+
+    def start(self, budget_s):
+        self.weight_done = 0.0
+        self._deadline = time.perf_counter() + budget_s
+
+    def _tick(self, w):
+        self.weight_done += w
+        if self._deadline is not None and time.perf_counter() > self._deadline:
+            raise _Budget()
+
+    @staticmethod
+    def op_weight(kind, level):
+        return {"mul_ct": 12.0, "rot": 10.0, "mul_pt": 2.0, "add": 0.3}[kind] * (level + 1)
+
+    def slotwise(self, op_kind, a, b):
+        kind = "mul_ct" if op_kind == "mul_ct" else ("mul_pt" if op_kind == "mul_pt" else "add")
+        out = super().slotwise(op_kind, a, b)
+        self._tick(self.op_weight(kind, a.level))
+        return out
+
+    def rotate(self, a, t):
+        out = super().rotate(a, t)
+        if t:
+            self._tick(self.op_weight("rot", a.level))
+        return out
+
+    def rotate_many(self, a, steps):
+        out = super().rotate_many(a, steps)
+        self._tick(sum(self.op_weight("rot", a.level) for t in steps if t))
+        return out
+
+    def mac_plain(self, babies, plains):
+        out = super().mac_plain(babies, plains)
+        self._tick(len(babies) * self.op_weight("mul_pt", babies[0].level))
+        return out
+
+    def prepare_keys_for(self, model, pcfg):
+        """Generate every Galois key the program needs (untimed)."""
+        from paper_2409_07751_b200 import inference as inf
+        rec = _Recorder(self.config, self.params)
+        inf.model_forward_he(model, rec.encrypt(np.zeros(model.n_in)), pcfg)
+        self.ensure_rotation_keys(sorted(rec.steps))
+        self._program = rec.ops
+
+    def total_weight(self, model, pcfg):
+        return sum(self.op_weight(k, lvl) * n for k, lvl, n in self._program)
+
+
+class _Recorder:
+    """Level-accurate dry run of the op program (no arithmetic)."""
+
+    def __init__(self, config, params):
+        from paper_2409_07751_b200.backend import OpCounter
+        self.config = config
+        self.params = params
+        self.counter = OpCounter()
+        self.steps = set()
+        self.ops = []
+
+    class Ct:
+        def __init__(self, be, level):
+            self.backend, self.level, self.batch, self.batched = be, level, 1, False
+
+        @property
+        def slots(self):
+            return np.zeros(self.backend.config.slot_count)
+
+    def encrypt(self, values, level=None):
+        return self.Ct(self, self.config.depth_budget if level is None else level)
+
+    def _lvl(self, a, b):
+        return min(a.level, b.level) if isinstance(b, self.Ct) else a.level
+
+    def add(self, a, b):
+        self.ops.append(("add", self._lvl(a, b), 1))
+        return self.Ct(self, self._lvl(a, b))
+
+    sub = add
+
+    def mul(self, a, b):
+        lvl = self._lvl(a, b)
+        self.ops.append(("mul_ct" if isinstance(b, self.Ct) else "mul_pt", lvl, 1))
+        return self.Ct(self, lvl - 1)
+
+    def rotate(self, a, t):
+        if t:
+            self.steps.add(t)
+            self.ops.append(("rot", a.level, 1))
+        return a if not t else self.Ct(self, a.level)
+
+    def rotate_many(self, a, steps):
+        return [self.rotate(a, t) for t in steps]
+
+    def mac_plain(self, babies, plains):
+        self.ops.append(("mul_pt", babies[0].level, len(babies)))
+        return self.Ct(self, babies[0].level - 1)
+
+
+def run_reference(args):
+    """--impl reference: the CPU path (oracle port) on host cores, rank 0 only."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(args, budget_s=args.cpu_budget)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            base = r
+    v = statistics.median(vals) if vals else 0.0
+    line = {"metric": "encrypted KAN inferences/sec", "value": v, "unit": "inferences/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 / v, 3) if v else None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)",
+            "data": "synthetic (seeded PCG64, SURVEY §8d)", "impl": "reference",
+            "config": {"workload": f"{args.config} one ciphertext per step sample, N=2^{args.log_n}"},
+            "cpu_baseline": dict(base or {}, value=v),
+            "e2e": {"value": v, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line))
+
+
+def main():
+    os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("product", "reference"), default="product")
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--chunk", type=int, default=32, help="ciphertexts per batched launch")
+    ap.add_argument("--log-n", type=int, default=16)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_product(args)
+
+
+if __name__ == "__main__":
+    main()

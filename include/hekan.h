@@ -107,6 +107,7 @@ int hk_sub(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_
 int hk_add_plain(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *pt, int32_t lp,
                  int32_t pt_batch, int32_t negate, uint64_t *out, int32_t batch);
 /* ct + constant: res[l] = residue of the constant for limb l (hk_encode_const) */
+/* res is a HOST array in both libraries */
 int hk_add_const(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *res,
                  uint64_t *out, int32_t batch);
 
@@ -142,6 +143,8 @@ int hk_mac_plain(hk_ctx *ctx, const uint64_t *const *babies, const uint64_t *con
 
 /* ---- introspection */
 int32_t hk_version(void);
+/* kernels enqueued by this context so far (oracle: 0) — bench evidence */
+uint64_t hk_launch_count(const hk_ctx *ctx);
 
 #ifdef __cplusplus
 }

@@ -141,6 +141,7 @@ static int fail(hk_ctx *c, int code, const char *fmt, ...) {
 
 const char *hk_last_error(const hk_ctx *c) { return c ? c->err : "null context"; }
 int32_t hk_version(void) { return 1; }
+uint64_t hk_launch_count(const hk_ctx *c) { (void)c; return 0; }
 int hk_set_stream(hk_ctx *c, void *s) { (void)c; (void)s; return HK_OK; }
 int hk_sync(hk_ctx *c) { (void)c; return HK_OK; }
 

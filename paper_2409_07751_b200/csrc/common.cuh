@@ -132,6 +132,7 @@ struct hk_ctx {
     uint64_t *d_relin;              // [n_digits][2][n_mod][N]
     std::map<uint32_t, uint64_t *> gal;
     bool have_keys;
+    unsigned long long launches;    // kernels enqueued by this context (bench evidence)
     // scratch workspace (grown on demand, stream-ordered use only)
     void *ws;
     size_t ws_bytes;

@@ -173,11 +173,11 @@ int make_ks_key(hk_ctx *c, uint64_t seed, uint64_t tag, const uint64_t *sprime, 
         uint64_t *bj = key + ((size_t)j * 2 + 0) * nm * N;
         uint64_t *aj = key + ((size_t)j * 2 + 1) * nm * N;
         ks_sample<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bj, aj, seed, ST_KEY_A + tag * 64 + j,
-                                                              ST_KEY_E + tag * 64 + j, c->log_n, nm, c->d_modq);
+                                                              ST_KEY_E + tag * 64 + j, c->log_n, nm, c->d_modq); ++c->launches;
         int rc = ntt_fwd_launch(c, bj, 0, nm, 1, 0);
         if (rc) return rc;
         ks_finish<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bj, aj, c->d_sk, sprime, d_pmod, d0, d1, c->log_n,
-                                                              nm, c->d_modq);
+                                                              nm, c->d_modq); ++c->launches;
     }
     HK_LAUNCH_CHECK(c, "make_ks_key");
     HK_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -189,7 +189,7 @@ int make_ks_key(hk_ctx *c, uint64_t seed, uint64_t tag, const uint64_t *sprime, 
 
 int automorph_launch(hk_ctx *c, const uint64_t *in, uint64_t *out, uint32_t g, long long n_polys) {
     const long long total = n_polys << c->log_n;
-    automorph_polys<<<hk_grid(total, 256), 256, 0, c->stream>>>(in, out, g, c->log_n, total);
+    automorph_polys<<<hk_grid(total, 256), 256, 0, c->stream>>>(in, out, g, c->log_n, total); ++c->launches;
     HK_LAUNCH_CHECK(c, "automorph");
     return HK_OK;
 }
@@ -212,12 +212,12 @@ int hk_keygen(hk_ctx *c, uint64_t seed) {
     HK_CUDA(c, cudaMalloc(&c->d_sk, sizeof(uint64_t) * nm * N));
     HK_CUDA(c, cudaMalloc(&c->d_relin, sizeof(uint64_t) * hk_key_words(c, 1)));
     const long long tot = (long long)nm * N;
-    sample_secret<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c->d_sk, seed, c->log_n, nm, c->d_modq);
+    sample_secret<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c->d_sk, seed, c->log_n, nm, c->d_modq); ++c->launches;
     int rc = ntt_fwd_launch(c, c->d_sk, 0, nm, 1, 0);
     if (rc) return rc;
     uint64_t *s2 = nullptr;
     HK_CUDA(c, cudaMalloc(&s2, sizeof(uint64_t) * nm * N));
-    square_mod<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c->d_sk, s2, c->log_n, nm, c->d_modq);
+    square_mod<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c->d_sk, s2, c->log_n, nm, c->d_modq); ++c->launches;
     rc = make_ks_key(c, seed, 0, s2, c->d_relin);
     cudaFree(s2);
     if (rc) return rc;
@@ -269,10 +269,10 @@ int hk_encrypt(hk_ctx *c, const uint64_t *pt, int32_t level, int32_t B, uint64_t
     const int nl = level + 1;
     const long long tot = (long long)nl * B * c->n;
     uint64_t *c0 = ct, *c1 = ct + tot;
-    enc_sample<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c0, c1, seed, c->log_n, nl, B, c->d_modq);
+    enc_sample<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c0, c1, seed, c->log_n, nl, B, c->d_modq); ++c->launches;
     int rc = ntt_fwd_launch(c, c0, 0, nl, B, 0);
     if (rc) return rc;
-    enc_finish<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c0, c1, pt, c->d_sk, c->log_n, B, c->d_modq, tot);
+    enc_finish<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c0, c1, pt, c->d_sk, c->log_n, B, c->d_modq, tot); ++c->launches;
     HK_LAUNCH_CHECK(c, "encrypt");
     return HK_OK;
 }
@@ -290,7 +290,7 @@ int hk_decrypt(hk_ctx *c, const uint64_t *ct, int32_t level, int32_t B, double s
     double2 *w = (double2 *)(ws + sizeof(uint64_t) * mwords);
     double2 *tmp = w + cwords;
     const long long tot = (long long)use * B * N;
-    dec_phase<<<hk_grid(tot, 256), 256, 0, c->stream>>>(ct, nl, use, B, c->d_sk, c->log_n, c->d_modq, m, tot);
+    dec_phase<<<hk_grid(tot, 256), 256, 0, c->stream>>>(ct, nl, use, B, c->d_sk, c->log_n, c->d_modq, m, tot); ++c->launches;
     int rc = ntt_inv_launch(c, m, 0, use, B, 0);
     if (rc) return rc;
     uint64_t i0 = 0, i1 = 0;
@@ -300,7 +300,7 @@ int hk_decrypt(hk_ctx *c, const uint64_t *ct, int32_t level, int32_t B, double s
         i1 = h_inv(q0 % q1, q1);
     }
     dec_center<<<hk_grid((long long)cwords, 256), 256, 0, c->stream>>>(m, use, B, c->log_n, scale, c->d_modq, i0,
-                                                                        i1, w, (long long)cwords);
+                                                                        i1, w, (long long)cwords); ++c->launches;
     HK_LAUNCH_CHECK(c, "decrypt");
     return hk_decode_launch(c, w, tmp, B, slots);
 }

@@ -117,6 +117,7 @@ extern "C" {
 
 const char *hk_last_error(const hk_ctx *c) { return c ? c->err.c_str() : "null context"; }
 int32_t hk_version(void) { return 1; }
+uint64_t hk_launch_count(const hk_ctx *c) { return c ? c->launches : 0; }
 
 int hk_set_stream(hk_ctx *c, void *s) {
     c->stream = (cudaStream_t)s;
@@ -148,6 +149,7 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     c->have_keys = false;
     c->ws = nullptr;
     c->ws_bytes = 0;
+    c->launches = 0;
     c->d_sk = c->d_relin = nullptr;
     const int N = c->n, nm = c->n_mod;
     std::vector<uint64_t> psi(nm);

@@ -100,11 +100,13 @@ __global__ void store_re(const double2 *__restrict__ a, double *__restrict__ out
 int hk_decode_launch(hk_ctx *c, double2 *w, double2 *tmp, int B, double *slots) {
     const int S = c->slots, M = 2 * c->n, bits = c->log_n - 1;
     const long long all = (long long)B * S, half = (long long)B * (S / 2);
-    bitrev_copy<<<hk_grid(all, 256), 256, 0, c->stream>>>(w, tmp, S, bits, all);
-    for (int len = 2; len <= S; len <<= 1)
+    bitrev_copy<<<hk_grid(all, 256), 256, 0, c->stream>>>(w, tmp, S, bits, all); ++c->launches;
+    for (int len = 2; len <= S; len <<= 1) {
         fft_fwd_stage<<<hk_grid(half, 256), 256, 0, c->stream>>>(tmp, S, len, M, c->d_zeta, c->d_rot_group,
                                                                 half);
-    store_re<<<hk_grid(all, 256), 256, 0, c->stream>>>(tmp, slots, all);
+        ++c->launches;
+    }
+    store_re<<<hk_grid(all, 256), 256, 0, c->stream>>>(tmp, slots, all); ++c->launches;
     HK_LAUNCH_CHECK(c, "decode");
     return HK_OK;
 }
@@ -117,12 +119,14 @@ extern "C" int hk_encode(hk_ctx *c, const double *slots, int32_t B, int32_t leve
     double2 *a = (double2 *)hk_workspace(c, sizeof(double2) * 2 * all);
     if (!a) return hk_fail(c, HK_E_NOMEM, "encode workspace");
     double2 *b2 = a + all;
-    load_slots<<<hk_grid(all, 256), 256, 0, c->stream>>>(slots, a, all);
-    for (int len = S; len >= 2; len >>= 1)
+    load_slots<<<hk_grid(all, 256), 256, 0, c->stream>>>(slots, a, all); ++c->launches;
+    for (int len = S; len >= 2; len >>= 1) {
         fft_inv_stage<<<hk_grid(half, 256), 256, 0, c->stream>>>(a, S, len, M, c->d_zeta, c->d_rot_group, half);
-    bitrev_copy<<<hk_grid(all, 256), 256, 0, c->stream>>>(a, b2, S, bits, all);
+        ++c->launches;
+    }
+    bitrev_copy<<<hk_grid(all, 256), 256, 0, c->stream>>>(a, b2, S, bits, all); ++c->launches;
     round_to_limbs<<<hk_grid(all, 256), 256, 0, c->stream>>>(b2, S, c->log_n, 1.0 / (double)S, scale, level + 1,
-                                                             B, c->d_modq, pt, all);
+                                                             B, c->d_modq, pt, all); ++c->launches;
     HK_LAUNCH_CHECK(c, "encode");
     return ntt_fwd_launch(c, pt, 0, level + 1, B, 0);
 }

@@ -257,13 +257,15 @@ int ntt_fwd_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int B, int)
     if (c->log_n == kLogN16) {
         ntt16_set_attrs();
         dim3 gc(8 * B, n_limbs), gr(8 * B, n_limbs);
-        ntt16_fwd_cols<<<gc, 512, kColSmem, c->stream>>>(buf, limb0, B, c->d_tw, c->d_modq);
-        ntt16_fwd_rows<<<gr, 512, kRowSmem, c->stream>>>(buf, limb0, B, c->d_tw, c->d_modq);
+        ntt16_fwd_cols<<<gc, 512, kColSmem, c->stream>>>(buf, limb0, B, c->d_tw, c->d_modq); ++c->launches;
+        ntt16_fwd_rows<<<gr, 512, kRowSmem, c->stream>>>(buf, limb0, B, c->d_tw, c->d_modq); ++c->launches;
     } else {
         const long long total = (long long)n_limbs * B * (c->n / 2);
-        for (int s = 0; s < c->log_n; ++s)
+        for (int s = 0; s < c->log_n; ++s) {
             ntt_stage_fwd<<<hk_grid(total, 256), 256, 0, c->stream>>>(buf, limb0, B, c->log_n, s, c->d_tw,
                                                                      c->d_modq, total);
+            ++c->launches;
+        }
     }
     HK_LAUNCH_CHECK(c, "ntt_fwd");
     return HK_OK;
@@ -274,16 +276,18 @@ int ntt_inv_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int B, int)
     if (c->log_n == kLogN16) {
         ntt16_set_attrs();
         dim3 gc(8 * B, n_limbs), gr(8 * B, n_limbs);
-        ntt16_inv_rows<<<gr, 512, kRowSmem, c->stream>>>(buf, limb0, B, c->d_itw, c->d_modq);
-        ntt16_inv_cols<<<gc, 512, kColSmem, c->stream>>>(buf, limb0, B, c->d_itw, c->d_ninv, c->d_modq);
+        ntt16_inv_rows<<<gr, 512, kRowSmem, c->stream>>>(buf, limb0, B, c->d_itw, c->d_modq); ++c->launches;
+        ntt16_inv_cols<<<gc, 512, kColSmem, c->stream>>>(buf, limb0, B, c->d_itw, c->d_ninv, c->d_modq); ++c->launches;
     } else {
         const long long total = (long long)n_limbs * B * (c->n / 2);
-        for (int s = c->log_n - 1; s >= 0; --s)
+        for (int s = c->log_n - 1; s >= 0; --s) {
             ntt_stage_inv<<<hk_grid(total, 256), 256, 0, c->stream>>>(buf, limb0, B, c->log_n, s, c->d_itw,
                                                                      c->d_modq, total);
+            ++c->launches;
+        }
         const long long all = (long long)n_limbs * B * c->n;
         scale_ninv<<<hk_grid(all, 256), 256, 0, c->stream>>>(buf, limb0, B, c->log_n, c->d_ninv, c->d_modq,
-                                                              all);
+                                                              all); ++c->launches;
     }
     HK_LAUNCH_CHECK(c, "ntt_inv");
     return HK_OK;

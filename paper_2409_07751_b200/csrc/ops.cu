@@ -254,12 +254,12 @@ int rescale_launch(hk_ctx *c, const uint64_t *in, int l, int B, uint64_t *out, u
                                cudaMemcpyDeviceToDevice, c->stream));
     int rc = ntt_inv_launch(c, L, l, 1, 2 * B, 0);
     if (rc) return rc;
-    k_rs_center<<<hk_grid(2 * BN, 256), 256, 0, c->stream>>>(L, R, l, 2 * BN, c->d_modq);
+    k_rs_center<<<hk_grid(2 * BN, 256), 256, 0, c->stream>>>(L, R, l, 2 * BN, c->d_modq); ++c->launches;
     rc = ntt_fwd_launch(c, R, 0, l, 2 * B, 0);
     if (rc) return rc;
     const long long total = 2LL * l * BN;
     k_rs_finish<<<hk_grid(total, 256), 256, 0, c->stream>>>(in, R, out, l, BN, c->d_rs_qinv + (size_t)l * c->n_q,
-                                                               c->d_modq, total);
+                                                               c->d_modq, total); ++c->launches;
     HK_LAUNCH_CHECK(c, "rescale");
     return HK_OK;
 }
@@ -287,7 +287,7 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const ui
         if (T.n_src > kMaxSrc) return hk_fail(c, HK_E_ARG, "digit of %d primes exceeds %d", T.n_src, kMaxSrc);
         k_conv<<<hk_grid(BN, 128), 128, 0, c->stream>>>(dc + (size_t)d0 * BN, T.n_src, T.d_inv, T.d_inv_sh,
                                                          T.d_hat, T.d_src_mod, T.d_dst_mod, T.n_dst, ej, 0, l,
-                                                         c->n_q, BN, c->d_modq);
+                                                         c->n_q, BN, c->d_modq); ++c->launches;
         HK_LAUNCH_CHECK(c, "modup conv");
         if (d0 > 0 && (rc = ntt_fwd_launch(c, ej, 0, d0, B, 0))) return rc;
         if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
@@ -299,7 +299,7 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const ui
     for (int r = 0; r < n; ++r) {
         const long long tot = (long long)ne * BN;
         k_key_ip<<<hk_grid(tot, 256), 256, 0, c->stream>>>(ext, nd, ne, l, c->n_q, c->n_mod, B, c->log_n, keys[r],
-                                                            gal[r], acc, acc + (size_t)ne * BN, c->d_modq, tot);
+                                                            gal[r], acc, acc + (size_t)ne * BN, c->d_modq, tot); ++c->launches;
         HK_LAUNCH_CHECK(c, "key inner product");
         for (int p = 0; p < 2; ++p) {
             const uint64_t *a = acc + (size_t)p * ne * BN;
@@ -308,13 +308,13 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const ui
             if ((rc = ntt_inv_launch(c, sp, c->n_q, np, B, 0))) return rc;
             const ConvTable &T = c->moddown;
             k_conv<<<hk_grid(BN, 128), 128, 0, c->stream>>>(sp, T.n_src, T.d_inv, T.d_inv_sh, T.d_hat, T.d_src_mod,
-                                                             T.d_dst_mod, l + 1, conv, 1, l, c->n_q, BN, c->d_modq);
+                                                             T.d_dst_mod, l + 1, conv, 1, l, c->n_q, BN, c->d_modq); ++c->launches;
             HK_LAUNCH_CHECK(c, "moddown conv");
             if ((rc = ntt_fwd_launch(c, conv, 0, l + 1, B, 0))) return rc;
             const long long t2 = (long long)(l + 1) * BN;
             k_md_finish<<<hk_grid(t2, 256), 256, 0, c->stream>>>(a, conv, p == 0 ? out0[r] : out1[r],
                                                                   p == 0 ? add0 : nullptr, gal[r], c->log_n, BN,
-                                                                  c->d_pinv, c->d_modq, t2);
+                                                                  c->d_pinv, c->d_modq, t2); ++c->launches;
             HK_LAUNCH_CHECK(c, "moddown finish");
         }
     }
@@ -327,7 +327,7 @@ int hk_add(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "add: level out of range");
     const int lo = std::min(la, lb);
     const long long BN = (long long)B * c->n, total = 2LL * (lo + 1) * BN;
-    k_addsub<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 0, c->d_modq, total);
+    k_addsub<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 0, c->d_modq, total); ++c->launches;
     HK_LAUNCH_CHECK(c, "add");
     return HK_OK;
 }
@@ -336,7 +336,7 @@ int hk_sub(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "sub: level out of range");
     const int lo = std::min(la, lb);
     const long long BN = (long long)B * c->n, total = 2LL * (lo + 1) * BN;
-    k_addsub<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 1, c->d_modq, total);
+    k_addsub<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 1, c->d_modq, total); ++c->launches;
     HK_LAUNCH_CHECK(c, "sub");
     return HK_OK;
 }
@@ -347,7 +347,7 @@ int hk_add_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, i
     if (pb != 1 && pb != B) return hk_fail(c, HK_E_LENGTH, "add_plain: plaintext batch");
     const long long total = 2LL * (la + 1) * B * c->n;
     k_add_plain<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, pt, pb, negate, out, B, c->log_n, c->d_modq,
-                                                              total);
+                                                              total); ++c->launches;
     HK_LAUNCH_CHECK(c, "add_plain");
     return HK_OK;
 }
@@ -357,7 +357,7 @@ int hk_add_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
     Residues r;
     for (int l = 0; l <= la; ++l) r.v[l] = res[l];
     const long long BN = (long long)B * c->n, total = 2LL * (la + 1) * BN;
-    k_add_const<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, r, out, BN, c->d_modq, total);
+    k_add_const<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, r, out, BN, c->d_modq, total); ++c->launches;
     HK_LAUNCH_CHECK(c, "add_const");
     return HK_OK;
 }
@@ -377,7 +377,7 @@ int hk_mul_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, i
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_plain workspace");
-    k_mul_plain<<<hk_grid(tot, 256), 256, 0, c->stream>>>(a, la, pt, pb, ws, B, c->log_n, c->d_modq, tot);
+    k_mul_plain<<<hk_grid(tot, 256), 256, 0, c->stream>>>(a, la, pt, pb, ws, B, c->log_n, c->d_modq, tot); ++c->launches;
     HK_LAUNCH_CHECK(c, "mul_plain");
     return rescale_launch(c, ws, la, B, out, ws + tot);
 }
@@ -390,7 +390,7 @@ int hk_mul_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_const workspace");
-    k_mul_const<<<hk_grid(tot, 256), 256, 0, c->stream>>>(a, la, r, ws, BN, c->d_modq, tot);
+    k_mul_const<<<hk_grid(tot, 256), 256, 0, c->stream>>>(a, la, r, ws, BN, c->d_modq, tot); ++c->launches;
     HK_LAUNCH_CHECK(c, "mul_const");
     return rescale_launch(c, ws, la, B, out, ws + tot);
 }
@@ -409,7 +409,7 @@ int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const
             bl.p[i] = babies[s + i];
             pl.p[i] = pts[s + i];
         }
-        k_mac<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bl, pl, cnt, la, ws, B, c->log_n, s > 0, c->d_modq, tot);
+        k_mac<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bl, pl, cnt, la, ws, B, c->log_n, s > 0, c->d_modq, tot); ++c->launches;
     }
     HK_LAUNCH_CHECK(c, "mac_plain");
     return rescale_launch(c, ws, la, B, out, ws + tot);
@@ -425,7 +425,7 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (5 * pl + extra));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
     uint64_t *d = ws, *ks = ws + 3 * pl, *scr = ws + 5 * pl;
-    k_tensor<<<hk_grid(pl, 256), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq, pl);
+    k_tensor<<<hk_grid(pl, 256), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq, pl); ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");
     uint64_t *o0 = ks, *o1 = ks + pl;
     const uint64_t *keys[1] = {c->d_relin};
@@ -434,7 +434,7 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     if (rc) return rc;
     // d0 += ks0, d1 += ks1 (d0, d1 contiguous = a level-l ciphertext)
     const long long tot = 2 * pl;
-    k_addsub<<<hk_grid(tot, 256), 256, 0, c->stream>>>(d, l, ks, l, d, l, BN, 0, c->d_modq, tot);
+    k_addsub<<<hk_grid(tot, 256), 256, 0, c->stream>>>(d, l, ks, l, d, l, BN, 0, c->d_modq, tot); ++c->launches;
     HK_LAUNCH_CHECK(c, "relin add");
     return rescale_launch(c, d, l, B, out, scr);
 }

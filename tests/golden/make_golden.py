@@ -1,0 +1,134 @@
+"""Generate golden fixtures by running the REFERENCE (`hekan`, imported from
+/root/reference/pkg/src) in this container. Commit the outputs; the GPU box
+has no /root/reference.
+
+Outputs
+  paper_2409_07751_b200/data/composite_sign.json  reference comparator stages
+  tests/golden/c1.npz      c1 model (built with the reference's classes from the
+                           same seeded draws), inputs, reference mirrored and
+                           exact outputs, per-layer logical op counts
+  tests/golden/small.npz   small multi-layer random models + inputs + outputs
+  tests/golden/backend.json known-answer vectors of the backend contract
+
+Run:  python tests/golden/make_golden.py
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+import hekan  # noqa: E402
+from hekan import approx as ra, bspline as rb, inference as ri, model as rm  # noqa: E402
+from hekan.backend import BackendConfig, CleartextBackend  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+DATA = os.path.join(ROOT, "paper_2409_07751_b200", "data")
+
+
+def comparator_json():
+    cs = ra.build_composite_sign(7.0, 2.0 ** -10)
+    doc = {"source": "hekan.approx.build_composite_sign (reference, approx.py:479-508)",
+           "comparators": [{"alpha": 7.0, "target_eps": 2.0 ** -10,
+                            "stages": [list(s.coeffs) for s in cs.stages],
+                            "certified_max_error": cs.certified_max_error()}]}
+    os.makedirs(DATA, exist_ok=True)
+    with open(os.path.join(DATA, "composite_sign.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+    return cs
+
+
+def build_ref_model(dims, g, k, lo, hi, w_std, degree, calib, input_shape, seed=0, explicit_R=False):
+    """SURVEY §8(d) recipe through the reference's own classes."""
+    rng = np.random.default_rng(seed)
+    layers = []
+    x = np.asarray(calib, dtype=float)
+    for n_i, n_o in zip(dims, dims[1:]):
+        grid = rb.GridMatrix.uniform(n_i, g, k, lo, hi)
+        if explicit_R:
+            R = 1.2 * max(float(np.max(np.abs(x))), float(np.max(np.abs(grid.entries))))
+            grid = rb.GridMatrix.uniform(n_i, g, k, lo, hi, R=R)
+        W_b = rng.normal(0.0, w_std, (n_o, n_i))
+        S = rng.normal(0.0, w_std, (n_o, n_i, grid.n_basis))
+        act = ra.estimate_range(x, x_min=float(np.min(x)), x_max=float(np.max(x)), factor=5.0)
+        poly = ra.fit_weighted_ls(rm.silu, act, degree, w=ra.WeightScheme.from_moments(act.mu, act.sigma))
+        layer = rm.KanLayer(W_b=W_b, S=S, grid=grid, silu_poly=poly, act_stats=(act.mu, act.sigma))
+        layers.append(layer)
+        x = np.stack([rm.layer_forward_plain(layer, row, mode="exact") for row in x])
+    return rm.KanModel(layers=layers, input_shape=input_shape)
+
+
+def counts_json(model, depth, path="lazy"):
+    be = CleartextBackend(BackendConfig(slot_count=4096, depth_budget=depth))
+    cfg = ri.PipelineConfig(path=path)
+    x = np.zeros(model.n_in)
+    ct = ri.encrypt_input(x, model, be)
+    out, stats = ri.model_forward_he(model, ct, cfg)
+    return [{"rotations": s.rotations, "ct_mults": s.ct_mults, "pt_mults": s.pt_mults,
+             "adds": s.adds, "depth_consumed": s.depth_consumed} for s in stats.per_layer], out.level
+
+
+def model_arrays(prefix, model):
+    d = {}
+    for i, layer in enumerate(model.layers):
+        d[f"{prefix}L{i}_W_b"] = layer.W_b
+        d[f"{prefix}L{i}_S"] = layer.S
+        d[f"{prefix}L{i}_grid"] = layer.grid.entries
+        d[f"{prefix}L{i}_R"] = np.array(layer.grid.R)
+        d[f"{prefix}L{i}_silu"] = np.array(layer.silu_poly.coeffs)
+    return d
+
+
+def main():
+    cs = comparator_json()
+    # ---- c1
+    rng = np.random.default_rng(1)
+    X = rng.uniform(-1.0, 1.0, (128, 2))
+    model = build_ref_model((2, 5, 1), 5, 3, -1.0, 1.0, 0.1, 10, X, (1, 1, 2))
+    mirrored = np.stack([rm.model_forward_plain(model, x, "mirrored", cs, "lazy") for x in X])
+    exact = np.stack([rm.model_forward_plain(model, x, "exact") for x in X])
+    naive = np.stack([rm.model_forward_plain(model, x, "mirrored", cs, "naive") for x in X])
+    counts, _ = counts_json(model, 36)
+    counts_naive, _ = counts_json(model, 38, "naive")
+    plan = ri.plan_model(model, ri.PipelineConfig())
+    np.savez_compressed(os.path.join(HERE, "c1.npz"), X=X, mirrored=mirrored, exact=exact,
+                        mirrored_naive=naive, plan_total=np.array(plan.total),
+                        counts=np.array(json.dumps({"lazy": counts, "naive": counts_naive})),
+                        **model_arrays("", model))
+    # ---- small random models (reference random_model, uniform weights)
+    small = {}
+    for idx, (dims, g, k) in enumerate([((3, 4), 3, 2), ((4, 3, 2), 4, 3), ((2, 6, 3), 5, 1)]):
+        mdl = rm.random_model(list(dims), g=g, k=k, seed=idx)
+        xr = np.random.default_rng(100 + idx).uniform(-0.9, 0.9, (4, dims[0]))
+        small[f"m{idx}_X"] = xr
+        small[f"m{idx}_mirrored"] = np.stack([rm.model_forward_plain(mdl, x, "mirrored", cs, "lazy") for x in xr])
+        small[f"m{idx}_exact"] = np.stack([rm.model_forward_plain(mdl, x, "exact") for x in xr])
+        small[f"m{idx}_mirrored_exactcmp"] = np.stack(
+            [rm.model_forward_plain(mdl, x, "mirrored", rb.EXACT_COMPARATOR, "lazy") for x in xr])
+        small[f"m{idx}_dims"] = np.array(dims)
+        small[f"m{idx}_gk"] = np.array([g, k])
+        c, _ = counts_json(mdl, ri.plan_model(mdl, ri.PipelineConfig()).total)
+        small[f"m{idx}_counts"] = np.array(json.dumps(c))
+        small.update(model_arrays(f"m{idx}_", mdl))
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **small)
+    # ---- backend known answers (test_backend.py style, via the reference itself)
+    be = CleartextBackend(BackendConfig(slot_count=8, depth_budget=20))
+    a = be.encrypt([1.0, 2.0, 3.0])
+    kat = {"rotate_left_1": be.rotate(a, 1).slots.tolist(),
+           "rotate_right_1": be.rotate(a, -1).slots.tolist(),
+           "bsgs_2x2": ri.bsgs_matvec(np.array([[1.0, 2.0], [3.0, 4.0]]),
+                                      be.encrypt([5.0, 6.0])).slots[:2].tolist(),
+           "pack_example": rb.repeat_pack(be.encrypt([1.0, 2.0]), 1, 1, 2).ct.slots.tolist(),
+           "comparator": {"certified_max_error": cs.certified_max_error(), "depth": cs.depth(),
+                          "degrees": [s.degree for s in cs.stages]}}
+    with open(os.path.join(HERE, "backend.json"), "w") as fh:
+        json.dump(kat, fh, indent=1)
+    print("wrote fixtures; c1 plan depth", plan.total, "counts", counts)
+
+
+if __name__ == "__main__":
+    main()
