@@ -71,6 +71,43 @@ __device__ __forceinline__ uint64_t reduce128_any(uint64_t hi, uint64_t lo, cons
     return add_mod(h, l, m.q);
 }
 
+// 25-bit split multiply-accumulate (all primes are in (2^40, 2^50)): for
+// x, y < 2^50, x*y = x1 y1 2^50 + (x1 y0 + x0 y1) 2^25 + x0 y0 with every
+// partial product < 2^50; each term is one IMAD.WIDE.U32 with fused 64-bit
+// accumulate. Sums of up to 64 products stay below 2^57 per accumulator.
+#define HK_M25 0x1FFFFFFu
+struct Acc3 {
+    uint64_t s0, s1, s2;
+};
+__device__ __forceinline__ void acc3_zero(Acc3 &a) { a.s0 = a.s1 = a.s2 = 0; }
+__device__ __forceinline__ void split25(uint64_t x, uint32_t &x0, uint32_t &x1) {
+    x0 = (uint32_t)x & HK_M25;
+    x1 = (uint32_t)(x >> 25);
+}
+__device__ __forceinline__ void acc3_mac(Acc3 &a, uint32_t x0, uint32_t x1, uint32_t y0, uint32_t y1) {
+    a.s0 += (uint64_t)x0 * y0;
+    a.s1 += (uint64_t)x0 * y1;
+    a.s1 += (uint64_t)x1 * y0;
+    a.s2 += (uint64_t)x1 * y1;
+}
+__device__ __forceinline__ void acc3_mac(Acc3 &a, uint64_t x, uint64_t y) {
+    uint32_t x0, x1, y0, y1;
+    split25(x, x0, x1);
+    split25(y, y0, y1);
+    acc3_mac(a, x0, x1, y0, y1);
+}
+__device__ __forceinline__ uint64_t acc3_reduce(const Acc3 &a, const ModQ &m) {
+    const uint64_t s2 = reduce128(0, a.s2, m);  // < q
+    uint64_t lo = a.s0, hi = 0;
+    uint64_t t = a.s1 << 25;
+    lo += t;
+    hi += (lo < t) + (a.s1 >> 39);
+    t = s2 << 50;
+    lo += t;
+    hi += (lo < t) + (s2 >> 14);
+    return reduce128(hi, lo, m);  // value < 2^101 < 2^(63+k)
+}
+
 __device__ __forceinline__ uint32_t brev_bits(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
 
 // counter-based randomness — identical formulas to the oracle

@@ -25,6 +25,7 @@ constexpr int kRowPad = 272;  // 256 + 16: pad one element every 16
 
 __device__ __forceinline__ int pad16(int c) { return c + (c >> 4); }
 
+// Canonical butterflies (generic per-stage path).
 __device__ __forceinline__ void ct_bfly(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q) {
     const uint64_t U = x, V = mul_shoup(y, w.x, w.y, q);
     x = add_mod(U, V, q);
@@ -35,14 +36,31 @@ __device__ __forceinline__ void gs_bfly(uint64_t &x, uint64_t &y, ulonglong2 w, 
     x = add_mod(U, V, q);
     y = mul_shoup(sub_mod(U, V, q), w.x, w.y, q);
 }
+// Lazy (Harvey) butterflies for the 2^16 path; all primes are < 2^52.
+// Forward: inputs < c q, outputs < (c + 2) q, no reductions at all; after the
+// 16 stages values are < 33 q < 2^58 and get one Barrett reduction at the end.
+__device__ __forceinline__ void ct_lazy(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q2) {
+    const uint64_t T = y * w.x - __umul64hi(y, w.y) * (q2 >> 1);  // [0, 2q)
+    const uint64_t U = x;
+    x = U + T;
+    y = U + q2 - T;
+}
+// Inverse: invariant [0, 2q): X' = U + V folded once, Y' = (U - V + 2q) w.
+__device__ __forceinline__ void gs_lazy(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q2) {
+    const uint64_t U = x, V = y;
+    uint64_t s = U + V;
+    x = s >= q2 ? s - q2 : s;
+    const uint64_t d = U + q2 - V;
+    y = d * w.x - __umul64hi(d, w.y) * (q2 >> 1);
+}
 
 // ---------------------------------------------------------------- forward
-__global__ void __launch_bounds__(512) ntt16_fwd_cols(uint64_t *__restrict__ buf, int limb0, int B,
+__global__ void __launch_bounds__(512, 2) ntt16_fwd_cols(uint64_t *__restrict__ buf, int limb0, int B,
                                                       const ulonglong2 *__restrict__ tw,
                                                       const ModQ *__restrict__ mq) {
     extern __shared__ uint64_t sm[];  // 256 x 32
     const int tile = blockIdx.x & 7, b = blockIdx.x >> 3, l = blockIdx.y, m = limb0 + l;
-    const uint64_t q = mq[m].q;
+    const uint64_t q2 = 2 * mq[m].q;
     const ulonglong2 *T = tw + (size_t)m * kN16;
     uint64_t *poly = buf + ((size_t)l * B + b) * kN16;
     const int c = threadIdx.x & 31, k = threadIdx.x >> 5, col = tile * 32 + c;
@@ -54,7 +72,7 @@ __global__ void __launch_bounds__(512) ntt16_fwd_cols(uint64_t *__restrict__ buf
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) ct_bfly(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], q);
+            if (!(u & d)) ct_lazy(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], q2);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) sm[(k + 16 * u) * 32 + c] = x[u];
@@ -66,18 +84,18 @@ __global__ void __launch_bounds__(512) ntt16_fwd_cols(uint64_t *__restrict__ buf
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) ct_bfly(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], q);
+            if (!(v & d)) ct_lazy(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], q2);
     }
 #pragma unroll
     for (int v = 0; v < 16; ++v) poly[(16 * k + v) * 256 + col] = x[v];
 }
 
-__global__ void __launch_bounds__(512) ntt16_fwd_rows(uint64_t *__restrict__ buf, int limb0, int B,
+__global__ void __launch_bounds__(512, 2) ntt16_fwd_rows(uint64_t *__restrict__ buf, int limb0, int B,
                                                       const ulonglong2 *__restrict__ tw,
                                                       const ModQ *__restrict__ mq) {
     extern __shared__ uint64_t sm[];  // 32 x kRowPad
     const int l = blockIdx.y, m = limb0 + l;
-    const uint64_t q = mq[m].q;
+    const uint64_t q2 = 2 * mq[m].q;
     const ulonglong2 *T = tw + (size_t)m * kN16;
     const int k = threadIdx.x & 15, rs = threadIdx.x >> 4;
     const int job = blockIdx.x * 32 + rs;
@@ -92,7 +110,7 @@ __global__ void __launch_bounds__(512) ntt16_fwd_rows(uint64_t *__restrict__ buf
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) ct_bfly(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], q);
+            if (!(u & d)) ct_lazy(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], q2);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = x[u];
@@ -105,23 +123,24 @@ __global__ void __launch_bounds__(512) ntt16_fwd_rows(uint64_t *__restrict__ buf
 #pragma unroll
         for (int v = 0; v < 16; ++v)
             if (!(v & d))
-                ct_bfly(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], q);
+                ct_lazy(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], q2);
     }
+    const ModQ mm = mq[m];
     __syncwarp();
 #pragma unroll
-    for (int v = 0; v < 16; ++v) srow[pad16(16 * k + v)] = x[v];
+    for (int v = 0; v < 16; ++v) srow[pad16(16 * k + v)] = reduce128(0, x[v], mm);
     __syncwarp();
 #pragma unroll
     for (int u = 0; u < 16; ++u) row[k + 16 * u] = srow[pad16(k + 16 * u)];
 }
 
 // ---------------------------------------------------------------- inverse
-__global__ void __launch_bounds__(512) ntt16_inv_rows(uint64_t *__restrict__ buf, int limb0, int B,
+__global__ void __launch_bounds__(512, 2) ntt16_inv_rows(uint64_t *__restrict__ buf, int limb0, int B,
                                                       const ulonglong2 *__restrict__ itw,
                                                       const ModQ *__restrict__ mq) {
     extern __shared__ uint64_t sm[];  // 32 x kRowPad
     const int l = blockIdx.y, m = limb0 + l;
-    const uint64_t q = mq[m].q;
+    const uint64_t q2 = 2 * mq[m].q;
     const ulonglong2 *T = itw + (size_t)m * kN16;
     const int k = threadIdx.x & 15, rs = threadIdx.x >> 4;
     const int job = blockIdx.x * 32 + rs;
@@ -140,7 +159,7 @@ __global__ void __launch_bounds__(512) ntt16_inv_rows(uint64_t *__restrict__ buf
 #pragma unroll
         for (int v = 0; v < 16; ++v)
             if (!(v & d))
-                gs_bfly(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], q);
+                gs_lazy(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], q2);
     }
     __syncwarp();
 #pragma unroll
@@ -153,19 +172,19 @@ __global__ void __launch_bounds__(512) ntt16_inv_rows(uint64_t *__restrict__ buf
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_bfly(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], q);
+            if (!(u & d)) gs_lazy(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], q2);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) row[k + 16 * u] = x[u];
 }
 
-__global__ void __launch_bounds__(512) ntt16_inv_cols(uint64_t *__restrict__ buf, int limb0, int B,
+__global__ void __launch_bounds__(512, 2) ntt16_inv_cols(uint64_t *__restrict__ buf, int limb0, int B,
                                                       const ulonglong2 *__restrict__ itw,
                                                       const ulonglong2 *__restrict__ ninv,
                                                       const ModQ *__restrict__ mq) {
     extern __shared__ uint64_t sm[];  // 256 x 32
     const int tile = blockIdx.x & 7, b = blockIdx.x >> 3, l = blockIdx.y, m = limb0 + l;
-    const uint64_t q = mq[m].q;
+    const uint64_t q2 = 2 * mq[m].q;
     const ulonglong2 *T = itw + (size_t)m * kN16;
     uint64_t *poly = buf + ((size_t)l * B + b) * kN16;
     const int c = threadIdx.x & 31, k = threadIdx.x >> 5, col = tile * 32 + c;
@@ -177,7 +196,7 @@ __global__ void __launch_bounds__(512) ntt16_inv_cols(uint64_t *__restrict__ buf
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_bfly(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], q);
+            if (!(v & d)) gs_lazy(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], q2);
     }
 #pragma unroll
     for (int v = 0; v < 16; ++v) sm[(16 * k + v) * 32 + c] = x[v];
@@ -189,9 +208,10 @@ __global__ void __launch_bounds__(512) ntt16_inv_cols(uint64_t *__restrict__ buf
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_bfly(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], q);
+            if (!(u & d)) gs_lazy(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], q2);
     }
     const ulonglong2 ni = ninv[m];
+    const uint64_t q = q2 >> 1;
 #pragma unroll
     for (int u = 0; u < 16; ++u) poly[(k + 16 * u) * 256 + col] = mul_shoup(x[u], ni.x, ni.y, q);
 }

@@ -15,7 +15,6 @@ int automorph_launch(hk_ctx *c, const uint64_t *in, uint64_t *out, uint32_t g, l
 
 namespace {
 
-constexpr int kMaxSrc = 48;     // basis-conversion sources per thread (alpha or n_p)
 constexpr int kMacMax = 64;     // operands per mac_plain launch
 
 struct Residues { uint64_t v[HK_MAX_MOD]; };
@@ -28,211 +27,253 @@ __device__ __forceinline__ uint32_t auto_src(uint32_t j, uint32_t g, int log_n) 
     return brev_bits((eg - 1u) >> 1, log_n);
 }
 
+// All element kernels use grid (ceil(B*N / 256), limbs, polys): blockIdx.y is
+// the limb, blockIdx.z the polynomial, x runs over the B*N coefficients of one
+// limb (no 64-bit divisions in index math).
+#define ELEM_INDEX                                                               \
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;       \
+    if (e >= BN) return;                                                         \
+    const int l = blockIdx.y, p = blockIdx.z;
+
 // ------------------------------------------------------------ add / sub
 __global__ void k_addsub(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb,
-                         uint64_t *__restrict__ out, int lo, long long BN, int neg, const ModQ *__restrict__ mq,
-                         long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;  // total = 2 (lo+1) B N
-    const long long pl = gid / BN, e = gid - pl * BN;
-    const int p = (int)(pl / (lo + 1)), l = (int)(pl - (long long)p * (lo + 1));
+                         uint64_t *__restrict__ out, int lo, long long BN, int neg, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
     const uint64_t q = mq[l].q;
     const uint64_t x = a[((long long)p * (la + 1) + l) * BN + e];
     const uint64_t y = b[((long long)p * (lb + 1) + l) * BN + e];
-    out[gid] = neg ? sub_mod(x, y, q) : add_mod(x, y, q);
+    out[((long long)p * (lo + 1) + l) * BN + e] = neg ? sub_mod(x, y, q) : add_mod(x, y, q);
 }
 
 // c0 +/- pt (pt_batch 1 or B), c1 copied
 __global__ void k_add_plain(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ pt, int pb,
-                            int neg, uint64_t *__restrict__ out, int B, int log_n, const ModQ *__restrict__ mq,
-                            long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;  // total = 2 (la+1) B N
-    const long long poly = (long long)(la + 1) * B << log_n;
-    if (gid >= poly) { out[gid] = a[gid]; return; }
+                            int neg, uint64_t *__restrict__ out, long long BN, int log_n,
+                            const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    const long long o = ((long long)p * (la + 1) + l) * BN + e;
+    if (p == 1) { out[o] = a[o]; return; }
     const int N = 1 << log_n;
-    const long long lb_ = gid >> log_n;
-    const int l = (int)(lb_ / B), b = (int)(lb_ - (long long)l * B), k = (int)(gid & (N - 1));
-    const uint64_t y = pt[((long long)l * pb + (pb == 1 ? 0 : b)) * N + k];
+    const long long b = e >> log_n;
+    const uint64_t y = pt[((long long)l * pb + (pb == 1 ? 0 : b)) * N + (e & (N - 1))];
     const uint64_t q = mq[l].q;
-    out[gid] = neg ? sub_mod(a[gid], y, q) : add_mod(a[gid], y, q);
+    out[o] = neg ? sub_mod(a[o], y, q) : add_mod(a[o], y, q);
 }
 
 __global__ void k_add_const(const uint64_t *__restrict__ a, int la, Residues r, uint64_t *__restrict__ out,
-                            long long BN, const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;
-    const long long poly = (long long)(la + 1) * BN;
-    if (gid >= poly) { out[gid] = a[gid]; return; }
-    const int l = (int)(gid / BN);
-    out[gid] = add_mod(a[gid], r.v[l], mq[l].q);
+                            long long BN, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    const long long o = ((long long)p * (la + 1) + l) * BN + e;
+    out[o] = p == 1 ? a[o] : add_mod(a[o], r.v[l], mq[l].q);
 }
 
 // tmp = a (.) pt for both polys (limbs 0..la)
 __global__ void k_mul_plain(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ pt, int pb,
-                            uint64_t *__restrict__ out, int B, int log_n, const ModQ *__restrict__ mq,
-                            long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;
+                            uint64_t *__restrict__ out, long long BN, int log_n, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
     const int N = 1 << log_n;
-    const long long poly = (long long)(la + 1) * B << log_n;
-    const long long e = gid >= poly ? gid - poly : gid;
-    const long long lb_ = e >> log_n;
-    const int l = (int)(lb_ / B), b = (int)(lb_ - (long long)l * B), k = (int)(e & (N - 1));
-    const uint64_t y = pt[((long long)l * pb + (pb == 1 ? 0 : b)) * N + k];
-    out[gid] = mul_mod(a[gid], y, mq[l]);
+    const long long b = e >> log_n;
+    const long long o = ((long long)p * (la + 1) + l) * BN + e;
+    const uint64_t y = pt[((long long)l * pb + (pb == 1 ? 0 : b)) * N + (e & (N - 1))];
+    out[o] = mul_mod(a[o], y, mq[l]);
 }
 
 __global__ void k_mul_const(const uint64_t *__restrict__ a, int la, Residues r, uint64_t *__restrict__ out,
-                            long long BN, const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;
-    const long long poly = (long long)(la + 1) * BN;
-    const long long e = gid >= poly ? gid - poly : gid;
-    const int l = (int)(e / BN);
-    out[gid] = mul_mod(a[gid], r.v[l], mq[l]);
+                            long long BN, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    const long long o = ((long long)p * (la + 1) + l) * BN + e;
+    out[o] = mul_mod(a[o], r.v[l], mq[l]);
 }
 
 // out = sum_i babies[i] (.) pts[i], both polys; `init` adds the previous out
-__global__ void k_mac(PtrList babies, PtrList pts, int n, int la, uint64_t *__restrict__ out, int B, int log_n,
-                      int init, const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;
+__global__ void k_mac(PtrList babies, PtrList pts, int n, int la, uint64_t *__restrict__ out, long long BN,
+                      int log_n, int init, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
     const int N = 1 << log_n;
-    const long long poly = (long long)(la + 1) * B << log_n;
-    const long long e = gid >= poly ? gid - poly : gid;
-    const int l = (int)((e >> log_n) / B), k = (int)(e & (N - 1));
-    uint64_t hi = 0, lo = init ? out[gid] : 0;
-    for (int i = 0; i < n; ++i) mac128(hi, lo, babies.p[i][gid], pts.p[i][(size_t)l * N + k]);
-    out[gid] = reduce128(hi, lo, mq[l]);
+    const long long o = ((long long)p * (la + 1) + l) * BN + e;
+    const long long pe = (long long)l * N + (e & (N - 1));
+    Acc3 acc;
+    acc3_zero(acc);
+    if (init) acc.s0 = out[o];
+    for (int i = 0; i < n; ++i) acc3_mac(acc, babies.p[i][o], pts.p[i][pe]);
+    out[o] = acc3_reduce(acc, mq[l]);
 }
 
 // ------------------------------------------------------------ rescale
-// R[i][pb][k] = centered(L[pb][k] mod q_l) mod q_i, i < l
+// R[i][pb][k] = centered(L[pb][k] mod q_l) mod q_i, i < l ; grid (BN2 / 256, l)
 __global__ void k_rs_center(const uint64_t *__restrict__ L, uint64_t *__restrict__ R, int l, long long BN2,
                             const ModQ *__restrict__ mq) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= BN2) return;
-    const uint64_t ql = mq[l].q, x = L[gid];
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= BN2) return;
+    const int i = blockIdx.y;
+    const uint64_t ql = mq[l].q, x = L[e];
     const bool neg = x > (ql >> 1);
     const uint64_t mag = neg ? ql - x : x;
-    for (int i = 0; i < l; ++i) {
-        const uint64_t q = mq[i].q;
-        const uint64_t r = mag >= q ? mag % q : mag;
-        R[(long long)i * BN2 + gid] = neg ? (r ? q - r : 0) : r;
-    }
-}
-
-// out[p][i] = (in[p][i] - R[i][p]) * q_l^-1 ; in at level l, out at level l-1
-__global__ void k_rs_finish(const uint64_t *__restrict__ in, const uint64_t *__restrict__ R,
-                            uint64_t *__restrict__ out, int l, long long BN, const ulonglong2 *__restrict__ qinv,
-                            const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;  // 2 * l * BN
-    const long long pl = gid / BN, e = gid - pl * BN;
-    const int p = (int)(pl / l), i = (int)(pl - (long long)p * l);
-    const uint64_t q = mq[i].q;
-    const ulonglong2 w = qinv[i];
-    const uint64_t x = in[((long long)p * (l + 1) + i) * BN + e];
-    const uint64_t y = R[(long long)i * 2 * BN + (long long)p * BN + e];
-    out[gid] = mul_shoup(sub_mod(x, y, q), w.x, w.y, q);
-}
-
-// ------------------------------------------------------------ tensor product
-__global__ void k_tensor(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb, int l,
-                         uint64_t *__restrict__ d, long long BN, const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;  // (l+1) BN
-    const int i = (int)(gid / BN);
     const ModQ m = mq[i];
-    const uint64_t a0 = a[gid], a1 = a[(long long)(la + 1) * BN + gid];
-    const uint64_t b0 = b[gid], b1 = b[(long long)(lb + 1) * BN + gid];
-    const long long pl = (long long)(l + 1) * BN;
-    d[gid] = mul_mod(a0, b0, m);
+    const uint64_t r = reduce128(0, mag, m);
+    R[(long long)i * BN2 + e] = neg ? (r ? m.q - r : 0) : r;
+}
+
+// out[p][i] = (in[p][i] - R[i][p]) * q_l^-1 ; grid (BN / 256, l, 2)
+__global__ void k_rs_finish(const uint64_t *__restrict__ in, const uint64_t *__restrict__ R,
+                            uint64_t *__restrict__ out, int lvl, long long BN, const ulonglong2 *__restrict__ qinv,
+                            const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    const uint64_t q = mq[l].q;
+    const ulonglong2 w = qinv[l];
+    const uint64_t x = in[((long long)p * (lvl + 1) + l) * BN + e];
+    const uint64_t y = R[(long long)l * 2 * BN + (long long)p * BN + e];
+    out[((long long)p * lvl + l) * BN + e] = mul_shoup(sub_mod(x, y, q), w.x, w.y, q);
+}
+
+// ------------------------------------------------------------ tensor product ; grid (BN/256, l+1)
+__global__ void k_tensor(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb, int lt,
+                         uint64_t *__restrict__ d, long long BN, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    (void)p;
+    const ModQ m = mq[l];
+    const long long o = (long long)l * BN + e;
+    const uint64_t a0 = a[o], a1 = a[(long long)(la + 1) * BN + o];
+    const uint64_t b0 = b[o], b1 = b[(long long)(lb + 1) * BN + o];
+    const long long pl = (long long)(lt + 1) * BN;
+    d[o] = mul_mod(a0, b0, m);
     uint64_t hi = 0, lo = 0;
     mac128(hi, lo, a0, b1);
     mac128(hi, lo, a1, b0);
-    d[pl + gid] = reduce128(hi, lo, m);
-    d[2 * pl + gid] = mul_mod(a1, b1, m);
+    d[pl + o] = reduce128(hi, lo, m);
+    d[2 * pl + o] = mul_mod(a1, b1, m);
 }
 
 // ------------------------------------------------------------ key switching
-// fast basis conversion: dst[t] = sum_i [src_i * inv_i]_{q_i} * hat[t][i] mod q_t
-// mode 0 (ModUp): dst limb index of chain prime m = (m <= l ? m : l + 1 + m - n_q)
-// mode 1 (ModDown): dst limb index = target position d
-__global__ void k_conv(const uint64_t *__restrict__ src, int n_src, const uint64_t *__restrict__ inv,
-                       const uint64_t *__restrict__ inv_sh, const uint64_t *__restrict__ hat,
-                       const int32_t *__restrict__ src_mod, const int32_t *__restrict__ dst_mod, int n_dst,
-                       uint64_t *__restrict__ dst, int mode, int l, int n_q, long long BN,
-                       const ModQ *__restrict__ mq) {
+// Fast basis conversion: dst[t] = sum_i [src_i * inv_i]_{q_i} * hat[t][i] mod q_t.
+// The source residues of one coefficient stay in registers (NS >= n_src), the
+// hat matrix and target moduli sit in shared memory (broadcast reads).
+// mode 0 (ModUp): dst limb of chain prime m = (m <= l ? m : l + 1 + m - n_q)
+// mode 1 (ModDown): dst limb = target position d
+template <int NS>
+__global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, int n_src,
+                                              const uint64_t *__restrict__ inv, const uint64_t *__restrict__ inv_sh,
+                                              const uint64_t *__restrict__ hat, const int32_t *__restrict__ src_mod,
+                                              const int32_t *__restrict__ dst_mod, int n_dst,
+                                              uint64_t *__restrict__ dst, int mode, int l, int n_q, long long BN,
+                                              const ModQ *__restrict__ mq) {
+    extern __shared__ uint64_t sh[];  // hat [n_dst][n_src] as (h0 | h1 << 32), ModQ [n_dst], out index [n_dst]
+    ModQ *smq = (ModQ *)(sh + n_dst * n_src);
+    int *sidx = (int *)(smq + n_dst);
+    for (int i = threadIdx.x; i < n_dst * n_src; i += blockDim.x) {
+        const uint64_t h = hat[i];
+        sh[i] = ((uint64_t)(uint32_t)(h >> 25) << 32) | ((uint32_t)h & HK_M25);
+    }
+    for (int d = threadIdx.x; d < n_dst; d += blockDim.x) {
+        const int m = dst_mod[d];
+        smq[d] = mq[m];
+        sidx[d] = mode == 0 ? (m <= l ? m : l + 1 + m - n_q) : d;
+    }
+    __syncthreads();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= BN) return;
-    uint64_t v[kMaxSrc];
-#pragma unroll 4
-    for (int i = 0; i < n_src; ++i) {
-        const uint64_t qi = mq[src_mod[i]].q;
-        v[i] = mul_shoup(src[(long long)i * BN + e], inv[i], inv_sh[i], qi);
+    uint32_t v0[NS], v1[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        if (i < n_src) {
+            const uint64_t qi = mq[src_mod[i]].q;
+            split25(mul_shoup(src[(long long)i * BN + e], inv[i], inv_sh[i], qi), v0[i], v1[i]);
+        }
     }
     for (int d = 0; d < n_dst; ++d) {
-        const int m = dst_mod[d];
-        const ModQ mt = mq[m];
-        const uint64_t *h = hat + (long long)d * n_src;
-        uint64_t hi = 0, lo = 0;
-        for (int i = 0; i < n_src; ++i) mac128(hi, lo, v[i], h[i]);
-        const int out_idx = mode == 0 ? (m <= l ? m : l + 1 + m - n_q) : d;
-        dst[(long long)out_idx * BN + e] = reduce128(hi, lo, mt);
+        const uint2 *h = (const uint2 *)(sh + d * n_src);
+        Acc3 acc;
+        acc3_zero(acc);
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+            if (i < n_src) {
+                const uint2 hv = h[i];
+                acc3_mac(acc, v0[i], v1[i], hv.x, hv.y);
+            }
+        dst[(long long)sidx[d] * BN + e] = acc3_reduce(acc, smq[d]);
     }
 }
 
-// acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][chain(t)]  (t over l+1+n_p limbs)
-__global__ void k_key_ip(const uint64_t *__restrict__ ext, int nd, int ne, int l, int n_q, int nm, int B,
-                         int log_n, const uint64_t *__restrict__ key, uint32_t g, uint64_t *__restrict__ acc0,
-                         uint64_t *__restrict__ acc1, const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;  // ne * B * N
+// acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][chain(t)] ; grid (BN/256, ne)
+__global__ void k_key_ip(const uint64_t *__restrict__ ext, int nd, int ne, int l, int n_q, int nm, int log_n,
+                         const uint64_t *__restrict__ key, uint32_t g, uint64_t *__restrict__ acc0,
+                         uint64_t *__restrict__ acc1, const ModQ *__restrict__ mq, long long BN) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= BN) return;
+    const int t = blockIdx.y;
     const int N = 1 << log_n;
-    const long long BN = (long long)B << log_n;
-    const int t = (int)(gid / BN);
-    const long long e = gid - (long long)t * BN;
     const int k = (int)(e & (N - 1));
     const long long src_e = g == 1u ? e : (e - k + auto_src((uint32_t)k, g, log_n));
     const int m = t <= l ? t : n_q + (t - l - 1);
     const ModQ mm = mq[m];
-    uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    Acc3 a0, a1;
+    acc3_zero(a0);
+    acc3_zero(a1);
     for (int j = 0; j < nd; ++j) {
-        const uint64_t x = ext[((long long)j * ne + t) * BN + src_e];
+        uint32_t x0, x1, y0, y1;
+        split25(ext[((long long)j * ne + t) * BN + src_e], x0, x1);
         const uint64_t *kj = key + ((size_t)j * 2 * nm + m) * N;
-        mac128(h0, l0, x, kj[k]);
-        mac128(h1, l1, x, kj[(size_t)nm * N + k]);
+        split25(kj[k], y0, y1);
+        acc3_mac(a0, x0, x1, y0, y1);
+        split25(kj[(size_t)nm * N + k], y0, y1);
+        acc3_mac(a1, x0, x1, y0, y1);
     }
-    acc0[gid] = reduce128(h0, l0, mm);
-    acc1[gid] = reduce128(h1, l1, mm);
+    acc0[(long long)t * BN + e] = acc3_reduce(a0, mm);
+    acc1[(long long)t * BN + e] = acc3_reduce(a1, mm);
 }
 
-// out_i = (acc_i - conv_i) * P^-1 (+ optional addend, optionally automorphed)
+// out_i = (acc_i - conv_i) * P^-1 (+ optional addend, optionally automorphed) ; grid (BN/256, l+1)
 __global__ void k_md_finish(const uint64_t *__restrict__ acc, const uint64_t *__restrict__ conv,
                             uint64_t *__restrict__ out, const uint64_t *__restrict__ addend, uint32_t g,
                             int log_n, long long BN, const ulonglong2 *__restrict__ pinv,
-                            const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;  // (l+1) BN
-    const int i = (int)(gid / BN);
-    const uint64_t q = mq[i].q;
-    const ulonglong2 w = pinv[i];
-    uint64_t r = mul_shoup(sub_mod(acc[gid], conv[gid], q), w.x, w.y, q);
+                            const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    (void)p;
+    const uint64_t q = mq[l].q;
+    const ulonglong2 w = pinv[l];
+    const long long o = (long long)l * BN + e;
+    uint64_t r = mul_shoup(sub_mod(acc[o], conv[o], q), w.x, w.y, q);
     if (addend) {
-        long long src = gid;
+        long long src = o;
         if (g != 1u) {
             const int N = 1 << log_n;
-            const int k = (int)(gid & (N - 1));
-            src = gid - k + auto_src((uint32_t)k, g, log_n);
+            const int k = (int)(e & (N - 1));
+            src = o - k + auto_src((uint32_t)k, g, log_n);
         }
         r = add_mod(r, addend[src], q);
     }
-    out[gid] = r;
+    out[o] = r;
 }
 
 }  // namespace
+
+static dim3 egrid(long long BN, int limbs, int polys) {
+    return dim3((unsigned)((BN + 255) / 256), (unsigned)limbs, (unsigned)polys);
+}
+
+// basis conversion launcher: picks the register-array size, stages hat in smem
+static int conv_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l,
+                       long long BN, int n_dst = -1) {
+    if (n_dst < 0) n_dst = T.n_dst;
+    const size_t smem = sizeof(uint64_t) * (size_t)n_dst * T.n_src + sizeof(ModQ) * n_dst + sizeof(int) * n_dst;
+    const dim3 grid((unsigned)((BN + 127) / 128));
+#define CONV_CASE(NSV)                                                                                        \
+    if (T.n_src <= NSV) {                                                                                     \
+        if (smem > 48 * 1024)                                                                                 \
+            cudaFuncSetAttribute(k_conv<NSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+        k_conv<NSV><<<grid, 128, smem, c->stream>>>(src, T.n_src, T.d_inv, T.d_inv_sh, T.d_hat, T.d_src_mod, \
+                                                     T.d_dst_mod, n_dst, dst, mode, l, c->n_q, BN, c->d_modq); \
+        ++c->launches;                                                                                        \
+        HK_LAUNCH_CHECK(c, "basis conversion");                                                              \
+        return HK_OK;                                                                                         \
+    }
+    CONV_CASE(4)
+    CONV_CASE(8)
+    CONV_CASE(16)
+    CONV_CASE(32)
+    CONV_CASE(48)
+#undef CONV_CASE
+    return hk_fail(c, HK_E_ARG, "basis conversion with %d sources exceeds 48", T.n_src);
+}
 
 // words of scratch the key switch at level l needs
 static size_t ks_scratch_words(const hk_ctx *c, int l, int B) {
@@ -254,12 +295,12 @@ int rescale_launch(hk_ctx *c, const uint64_t *in, int l, int B, uint64_t *out, u
                                cudaMemcpyDeviceToDevice, c->stream));
     int rc = ntt_inv_launch(c, L, l, 1, 2 * B, 0);
     if (rc) return rc;
-    k_rs_center<<<hk_grid(2 * BN, 256), 256, 0, c->stream>>>(L, R, l, 2 * BN, c->d_modq); ++c->launches;
+    k_rs_center<<<egrid(2 * BN, l, 1), 256, 0, c->stream>>>(L, R, l, 2 * BN, c->d_modq); ++c->launches;
     rc = ntt_fwd_launch(c, R, 0, l, 2 * B, 0);
     if (rc) return rc;
-    const long long total = 2LL * l * BN;
-    k_rs_finish<<<hk_grid(total, 256), 256, 0, c->stream>>>(in, R, out, l, BN, c->d_rs_qinv + (size_t)l * c->n_q,
-                                                               c->d_modq, total); ++c->launches;
+    k_rs_finish<<<egrid(BN, l, 2), 256, 0, c->stream>>>(in, R, out, l, BN, c->d_rs_qinv + (size_t)l * c->n_q,
+                                                        c->d_modq);
+    ++c->launches;
     HK_LAUNCH_CHECK(c, "rescale");
     return HK_OK;
 }
@@ -284,10 +325,7 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const ui
         const ConvTable &T = c->modup[l][j];
         const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, l + 1);
         uint64_t *ej = ext + (size_t)j * ne * BN;
-        if (T.n_src > kMaxSrc) return hk_fail(c, HK_E_ARG, "digit of %d primes exceeds %d", T.n_src, kMaxSrc);
-        k_conv<<<hk_grid(BN, 128), 128, 0, c->stream>>>(dc + (size_t)d0 * BN, T.n_src, T.d_inv, T.d_inv_sh,
-                                                         T.d_hat, T.d_src_mod, T.d_dst_mod, T.n_dst, ej, 0, l,
-                                                         c->n_q, BN, c->d_modq); ++c->launches;
+        if ((rc = conv_launch(c, T, dc + (size_t)d0 * BN, ej, 0, l, BN))) return rc;
         HK_LAUNCH_CHECK(c, "modup conv");
         if (d0 > 0 && (rc = ntt_fwd_launch(c, ej, 0, d0, B, 0))) return rc;
         if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
@@ -297,9 +335,9 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const ui
     }
     // per key: inner product, ModDown of both halves
     for (int r = 0; r < n; ++r) {
-        const long long tot = (long long)ne * BN;
-        k_key_ip<<<hk_grid(tot, 256), 256, 0, c->stream>>>(ext, nd, ne, l, c->n_q, c->n_mod, B, c->log_n, keys[r],
-                                                            gal[r], acc, acc + (size_t)ne * BN, c->d_modq, tot); ++c->launches;
+        k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(ext, nd, ne, l, c->n_q, c->n_mod, c->log_n, keys[r],
+                                                          gal[r], acc, acc + (size_t)ne * BN, c->d_modq, BN);
+        ++c->launches;
         HK_LAUNCH_CHECK(c, "key inner product");
         for (int p = 0; p < 2; ++p) {
             const uint64_t *a = acc + (size_t)p * ne * BN;
@@ -307,14 +345,14 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const ui
                                        cudaMemcpyDeviceToDevice, c->stream));
             if ((rc = ntt_inv_launch(c, sp, c->n_q, np, B, 0))) return rc;
             const ConvTable &T = c->moddown;
-            k_conv<<<hk_grid(BN, 128), 128, 0, c->stream>>>(sp, T.n_src, T.d_inv, T.d_inv_sh, T.d_hat, T.d_src_mod,
-                                                             T.d_dst_mod, l + 1, conv, 1, l, c->n_q, BN, c->d_modq); ++c->launches;
+            if ((rc = conv_launch(c, T, sp, conv, 1, l, BN, l + 1))) return rc;
             HK_LAUNCH_CHECK(c, "moddown conv");
             if ((rc = ntt_fwd_launch(c, conv, 0, l + 1, B, 0))) return rc;
             const long long t2 = (long long)(l + 1) * BN;
-            k_md_finish<<<hk_grid(t2, 256), 256, 0, c->stream>>>(a, conv, p == 0 ? out0[r] : out1[r],
-                                                                  p == 0 ? add0 : nullptr, gal[r], c->log_n, BN,
-                                                                  c->d_pinv, c->d_modq, t2); ++c->launches;
+            k_md_finish<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, conv, p == 0 ? out0[r] : out1[r],
+                                                                   p == 0 ? add0 : nullptr, gal[r], c->log_n, BN,
+                                                                   c->d_pinv, c->d_modq);
+            ++c->launches;
             HK_LAUNCH_CHECK(c, "moddown finish");
         }
     }
@@ -326,8 +364,8 @@ extern "C" {
 int hk_add(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *o, int32_t B) {
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "add: level out of range");
     const int lo = std::min(la, lb);
-    const long long BN = (long long)B * c->n, total = 2LL * (lo + 1) * BN;
-    k_addsub<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 0, c->d_modq, total); ++c->launches;
+    const long long BN = (long long)B * c->n;
+    k_addsub<<<egrid(BN, lo + 1, 2), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 0, c->d_modq); ++c->launches;
     HK_LAUNCH_CHECK(c, "add");
     return HK_OK;
 }
@@ -335,8 +373,8 @@ int hk_add(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
 int hk_sub(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *o, int32_t B) {
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "sub: level out of range");
     const int lo = std::min(la, lb);
-    const long long BN = (long long)B * c->n, total = 2LL * (lo + 1) * BN;
-    k_addsub<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 1, c->d_modq, total); ++c->launches;
+    const long long BN = (long long)B * c->n;
+    k_addsub<<<egrid(BN, lo + 1, 2), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 1, c->d_modq); ++c->launches;
     HK_LAUNCH_CHECK(c, "sub");
     return HK_OK;
 }
@@ -345,9 +383,9 @@ int hk_add_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, i
                  int32_t negate, uint64_t *out, int32_t B) {
     if (la < 0 || la >= c->n_q || lp < la) return hk_fail(c, HK_E_ARG, "add_plain: level mismatch");
     if (pb != 1 && pb != B) return hk_fail(c, HK_E_LENGTH, "add_plain: plaintext batch");
-    const long long total = 2LL * (la + 1) * B * c->n;
-    k_add_plain<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, pt, pb, negate, out, B, c->log_n, c->d_modq,
-                                                              total); ++c->launches;
+    const long long BN = (long long)B * c->n;
+    k_add_plain<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, pt, pb, negate, out, BN, c->log_n, c->d_modq);
+    ++c->launches;
     HK_LAUNCH_CHECK(c, "add_plain");
     return HK_OK;
 }
@@ -356,8 +394,8 @@ int hk_add_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
     if (la < 0 || la >= c->n_q) return hk_fail(c, HK_E_ARG, "add_const: level");
     Residues r;
     for (int l = 0; l <= la; ++l) r.v[l] = res[l];
-    const long long BN = (long long)B * c->n, total = 2LL * (la + 1) * BN;
-    k_add_const<<<hk_grid(total, 256), 256, 0, c->stream>>>(a, la, r, out, BN, c->d_modq, total); ++c->launches;
+    const long long BN = (long long)B * c->n;
+    k_add_const<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, r, out, BN, c->d_modq); ++c->launches;
     HK_LAUNCH_CHECK(c, "add_const");
     return HK_OK;
 }
@@ -377,7 +415,7 @@ int hk_mul_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, i
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_plain workspace");
-    k_mul_plain<<<hk_grid(tot, 256), 256, 0, c->stream>>>(a, la, pt, pb, ws, B, c->log_n, c->d_modq, tot); ++c->launches;
+    k_mul_plain<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, pt, pb, ws, BN, c->log_n, c->d_modq); ++c->launches;
     HK_LAUNCH_CHECK(c, "mul_plain");
     return rescale_launch(c, ws, la, B, out, ws + tot);
 }
@@ -390,7 +428,7 @@ int hk_mul_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_const workspace");
-    k_mul_const<<<hk_grid(tot, 256), 256, 0, c->stream>>>(a, la, r, ws, BN, c->d_modq, tot); ++c->launches;
+    k_mul_const<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, r, ws, BN, c->d_modq); ++c->launches;
     HK_LAUNCH_CHECK(c, "mul_const");
     return rescale_launch(c, ws, la, B, out, ws + tot);
 }
@@ -409,7 +447,7 @@ int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const
             bl.p[i] = babies[s + i];
             pl.p[i] = pts[s + i];
         }
-        k_mac<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bl, pl, cnt, la, ws, B, c->log_n, s > 0, c->d_modq, tot); ++c->launches;
+        k_mac<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(bl, pl, cnt, la, ws, BN, c->log_n, s > 0, c->d_modq); ++c->launches;
     }
     HK_LAUNCH_CHECK(c, "mac_plain");
     return rescale_launch(c, ws, la, B, out, ws + tot);
@@ -425,7 +463,7 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (5 * pl + extra));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
     uint64_t *d = ws, *ks = ws + 3 * pl, *scr = ws + 5 * pl;
-    k_tensor<<<hk_grid(pl, 256), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq, pl); ++c->launches;
+    k_tensor<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq); ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");
     uint64_t *o0 = ks, *o1 = ks + pl;
     const uint64_t *keys[1] = {c->d_relin};
@@ -433,8 +471,7 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     int rc = keyswitch(c, d + 2 * pl, l, B, 1, keys, g1, &o0, &o1, nullptr, scr);
     if (rc) return rc;
     // d0 += ks0, d1 += ks1 (d0, d1 contiguous = a level-l ciphertext)
-    const long long tot = 2 * pl;
-    k_addsub<<<hk_grid(tot, 256), 256, 0, c->stream>>>(d, l, ks, l, d, l, BN, 0, c->d_modq, tot); ++c->launches;
+    k_addsub<<<egrid(BN, l + 1, 2), 256, 0, c->stream>>>(d, l, ks, l, d, l, BN, 0, c->d_modq); ++c->launches;
     HK_LAUNCH_CHECK(c, "relin add");
     return rescale_launch(c, d, l, B, out, scr);
 }

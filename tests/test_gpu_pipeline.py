@@ -1,0 +1,93 @@
+"""Encrypted KAN on the sm_100a engine: bit-exact vs the oracle running the
+same program, and within 1e-4 of the reference's decrypted outputs at the
+benchmark ring degree N = 2^16 (size-independent properties at full size)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2409_07751_b200 import configs, inference as inf
+from paper_2409_07751_b200.backend import BackendConfig, HeBackend
+from paper_2409_07751_b200.params import kan_params, make_params
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gpu(p, depth, seed=0):
+    from paper_2409_07751_b200.engine import GpuEngine
+    return HeBackend(BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=seed), p,
+                     engine=GpuEngine(p))
+
+
+def test_c1_pipeline_bitexact_vs_oracle(gpu_lib):
+    from oracle.engine import OracleEngine
+    _, model, X = configs.workload("c1")
+    p = make_params(8, 36)
+    bc = BackendConfig(slot_count=p.slot_count, depth_budget=36)
+    g, o = _gpu(p, 36), HeBackend(bc, p, engine=OracleEngine(p))
+    cfg = inf.PipelineConfig()
+    og, sg = inf.model_forward_he(model, inf.encrypt_input(X[:5], model, g), cfg)
+    oo, so = inf.model_forward_he(model, inf.encrypt_input(X[:5], model, o), cfg)
+    assert np.array_equal(g.export_ct(og), o.export_ct(oo))
+    assert sg.to_json()["total"]["rotations"] == so.to_json()["total"]["rotations"]
+    gold = np.load(os.path.join(GOLD, "c1.npz"))["mirrored"][:5]
+    assert np.abs(g.decrypt(og)[:, :1] - gold).max() < 1e-4
+
+
+def test_small_models_bitexact_vs_oracle(gpu_lib):
+    from oracle.engine import OracleEngine
+    from tests.test_pipeline import model_from_golden
+    gz = np.load(os.path.join(GOLD, "small.npz"))
+    for idx in range(3):
+        dims = tuple(int(v) for v in gz[f"m{idx}_dims"])
+        model = model_from_golden(gz, f"m{idx}_", dims)
+        depth = inf.plan_model(model, inf.PipelineConfig()).total
+        p = make_params(9, depth)
+        bc = BackendConfig(slot_count=p.slot_count, depth_budget=depth)
+        g, o = _gpu(p, depth), HeBackend(bc, p, engine=OracleEngine(p))
+        X = gz[f"m{idx}_X"]
+        og, _ = inf.model_forward_he(model, inf.encrypt_input(X, model, g), inf.PipelineConfig())
+        oo, _ = inf.model_forward_he(model, inf.encrypt_input(X, model, o), inf.PipelineConfig())
+        assert np.array_equal(g.export_ct(og), o.export_ct(oo)), idx
+        assert np.abs(g.decrypt(og)[:, :dims[-1]] - gz[f"m{idx}_mirrored"]).max() < 1e-4
+
+
+def test_c1_full_ring_degree_matches_reference(gpu_lib):
+    g_ = np.load(os.path.join(GOLD, "c1.npz"))
+    _, model, X = configs.workload("c1")
+    p = kan_params(36)
+    be = _gpu(p, 36)
+    B = 16
+    out, stats = inf.model_forward_he(model, inf.encrypt_input(X[:B], model, be), inf.PipelineConfig())
+    assert out.level == 0
+    dec = be.decrypt(out)[:, :1]
+    assert np.abs(dec - g_["mirrored"][:B]).max() < 1e-4
+    ref = json.loads(str(g_["counts"]))["lazy"]
+    assert [s.rotations for s in stats.per_layer] == [r["rotations"] for r in ref]
+    assert [s.ct_mults for s in stats.per_layer] == [r["ct_mults"] for r in ref]
+
+
+def test_full_size_properties(gpu_lib):
+    """N = 2^16, 37 limbs: rotation group law, linearity, exact level rule."""
+    p = kan_params(36)
+    be = _gpu(p, 36)
+    S = p.slot_count
+    rng = np.random.default_rng(5)
+    x, y = rng.uniform(-1, 1, (2, S)), rng.uniform(-1, 1, (2, S))
+    a, b = be.encrypt(x), be.encrypt(y)
+    r1 = be.rotate(be.rotate(a, 7), 1 << 10)
+    r2 = be.rotate(a, 7 + (1 << 10))
+    assert np.abs(r1.slots - r2.slots).max() < 1e-6
+    assert np.abs(r1.slots - np.roll(x, -(7 + (1 << 10)), axis=1)).max() < 1e-6
+    lin = be.sub(be.add(be.mul(a, 0.5), be.mul(b, 0.25)), be.mul(be.add(a, b), 0.25))
+    assert np.abs(lin.slots - (0.25 * x)).max() < 1e-6
+    m = be.mul(a, b)
+    assert m.level == 35 and np.abs(m.slots - x * y).max() < 1e-6
+    # deep chain to level 0 keeps precision
+    c = a
+    for _ in range(36):
+        c = be.mul(c, 1.0)
+    assert c.level == 0 and np.abs(c.slots - x).max() < 1e-5
