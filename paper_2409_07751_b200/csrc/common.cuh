@@ -84,11 +84,16 @@ __device__ __forceinline__ void split25(uint64_t x, uint32_t &x0, uint32_t &x1) 
     x0 = (uint32_t)x & HK_M25;
     x1 = (uint32_t)(x >> 25);
 }
+__device__ __forceinline__ uint64_t mad_wide(uint32_t x, uint32_t y, uint64_t acc) {
+    uint64_t r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(x), "r"(y), "l"(acc));
+    return r;
+}
 __device__ __forceinline__ void acc3_mac(Acc3 &a, uint32_t x0, uint32_t x1, uint32_t y0, uint32_t y1) {
-    a.s0 += (uint64_t)x0 * y0;
-    a.s1 += (uint64_t)x0 * y1;
-    a.s1 += (uint64_t)x1 * y0;
-    a.s2 += (uint64_t)x1 * y1;
+    a.s0 = mad_wide(x0, y0, a.s0);
+    a.s1 = mad_wide(x0, y1, a.s1);
+    a.s1 = mad_wide(x1, y0, a.s1);
+    a.s2 = mad_wide(x1, y1, a.s2);
 }
 __device__ __forceinline__ void acc3_mac(Acc3 &a, uint64_t x, uint64_t y) {
     uint32_t x0, x1, y0, y1;
