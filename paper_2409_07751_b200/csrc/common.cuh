@@ -161,6 +161,10 @@ struct hk_ctx {
     ulonglong2 *d_tw;      // [n_mod][N] {psi^brv(k), shoup}
     ulonglong2 *d_itw;     // [n_mod][N] {psi^-brv(k), shoup}
     ulonglong2 *d_ninv;    // [n_mod] {N^-1, shoup}
+    double2 *d_twf;        // [n_mod][N] {psi^brv(k), psi^brv(k)/q} as float64 (fused 2^16 NTT)
+    double2 *d_itwf;       // [n_mod][N] inverse twiddles, float64
+    double2 *d_ninvf;      // [n_mod] {N^-1, N^-1/q}
+    double2 *d_fmod;       // [n_mod] {q, 1/q}
     double2 *d_zeta;       // [2N]
     uint32_t *d_rot_group; // [S]
     // rescale: qinv[l][i] = q_l^-1 mod q_i (i < l), Shoup pairs

@@ -187,6 +187,23 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     c->d_tw = upload(tw);
     c->d_itw = upload(itw);
     c->d_ninv = upload(ninv);
+    {
+        std::vector<double2> twf((size_t)nm * N), itwf((size_t)nm * N), ninvf(nm), fmod(nm);
+        for (int m = 0; m < nm; ++m) {
+            const double qd = (double)c->mod_h[m];
+            for (int k = 0; k < N; ++k) {
+                const size_t o = (size_t)m * N + k;
+                twf[o] = make_double2((double)tw[o].x, (double)tw[o].x / qd);
+                itwf[o] = make_double2((double)itw[o].x, (double)itw[o].x / qd);
+            }
+            ninvf[m] = make_double2((double)ninv[m].x, (double)ninv[m].x / qd);
+            fmod[m] = make_double2(qd, 1.0 / qd);
+        }
+        c->d_twf = upload(twf);
+        c->d_itwf = upload(itwf);
+        c->d_ninvf = upload(ninvf);
+        c->d_fmod = upload(fmod);
+    }
     // canonical-embedding tables (same formulas as the oracle)
     const int M = 2 * N;
     std::vector<double2> zeta(M);
@@ -254,6 +271,10 @@ void hk_ctx_destroy(hk_ctx *c) {
     cudaFree(c->d_tw);
     cudaFree(c->d_itw);
     cudaFree(c->d_ninv);
+    cudaFree(c->d_twf);
+    cudaFree(c->d_itwf);
+    cudaFree(c->d_ninvf);
+    cudaFree(c->d_fmod);
     cudaFree(c->d_zeta);
     cudaFree(c->d_rot_group);
     cudaFree(c->d_rs_qinv);

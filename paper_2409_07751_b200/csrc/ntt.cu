@@ -5,16 +5,21 @@
 // (0..logN-1) pairs (j, j + N/2^(s+1)) with twiddle psi^brv(2^s + (j >> (logN-s)));
 // inverse = Gentleman-Sande in reverse stage order with psi^-brv, then * N^-1.
 //
-// N = 2^16 fast path: the 16 stages split as 256 x 256.
-//   stages 0..7  act along rows r of the 256x256 view j = 256 r + c  -> "column"
-//                kernel: one CTA = 32 columns x 256 rows of one polynomial,
-//                4 radix-2 stages in registers, one shared-memory transpose,
-//                4 more stages in registers; all global accesses are 256 B
-//                coalesced row segments.
-//   stages 8..15 act within a row -> "row" kernel: one CTA = 32 rows, a
-//                half-warp per row; the two exchanges stay inside a warp
-//                (__syncwarp) through a bank-conflict-free padded tile.
-// Other N (parity tests at small sizes): one launch per stage.
+// N = 2^16 fast path: one 8-CTA thread-block cluster per polynomial.
+//   stages 0..7 act along rows r of the 256x256 view j = 256 r + c -> column
+//     phase: CTA c owns columns [32c, 32c+32): 4 radix-2 stages in registers,
+//     one shared-memory transpose, 4 more stages; 256 B coalesced row segments;
+//   a cluster barrier (release/acquire) publishes the in-place intermediate,
+//     which stays in L2 (512 KiB live per cluster);
+//   stages 8..15 act within a row -> row phase: CTA c owns rows [32c, 32c+32),
+//     a half-warp per row, both exchanges inside a warp (__syncwarp) through a
+//     bank-conflict-free padded tile.
+// DRAM therefore sees one read and one write per coefficient.
+// Arithmetic: lazy Harvey butterflies with an approximate-quotient Shoup
+// multiply (3 IMAD.WIDE for the quotient instead of a 64-bit mulhi).
+// Other N (parity tests at small sizes): one canonical launch per stage.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -36,43 +41,82 @@ __device__ __forceinline__ void gs_bfly(uint64_t &x, uint64_t &y, ulonglong2 w, 
     x = add_mod(U, V, q);
     y = mul_shoup(sub_mod(U, V, q), w.x, w.y, q);
 }
-// Lazy (Harvey) butterflies for the 2^16 path; all primes are < 2^52.
-// Forward: inputs < c q, outputs < (c + 2) q, no reductions at all; after the
-// 16 stages values are < 33 q < 2^58 and get one Barrett reduction at the end.
-__device__ __forceinline__ void ct_lazy(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q2) {
-    const uint64_t T = y * w.x - __umul64hi(y, w.y) * (q2 >> 1);  // [0, 2q)
-    const uint64_t U = x;
-    x = U + T;
-    y = U + q2 - T;
+
+// ---------------------------------------------------------------- FP64 arithmetic
+// Inside the fused kernels residues live in float64 registers as exact
+// integers (|x| < 2^51). The DFMA/DMUL pipe (64/clk/SM on B200, otherwise idle
+// here) carries the modular arithmetic:
+//   y*w = h + l exactly (two-product), t = round(y*w/q) via y*(w/q) + M - M,
+//   r = (h - t q) + l exactly, |r| <= 1.5 q                      (6 FP64 ops).
+// Small primes (q < 2^47): a phase of 8 stages from |x| < q stays below 13 q <
+// 2^51, so no reductions are needed inside a phase; the column->row boundary
+// recentres (|x| <= q/2). Large primes (q_0 ~ 2^50): recentre after every stage.
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;  // 2^52
+constexpr uint64_t kSmallPrime = 1ull << 47;
+
+struct FpMod {
+    double q, qinv;
+};
+
+__device__ __forceinline__ double f_round(double x) { return __dsub_rn(__fma_rn(x, 1.0, kMagic), kMagic); }
+__device__ __forceinline__ double f_mulmod(double y, double w, double wq, double q) {
+    const double h = __dmul_rn(y, w);
+    const double l = __fma_rn(y, w, -h);
+    const double t = __dsub_rn(__fma_rn(y, wq, kMagic), kMagic);
+    return __dadd_rn(__fma_rn(-t, q, h), l);
 }
-// Inverse: invariant [0, 2q): X' = U + V folded once, Y' = (U - V + 2q) w.
-__device__ __forceinline__ void gs_lazy(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q2) {
-    const uint64_t U = x, V = y;
-    uint64_t s = U + V;
-    x = s >= q2 ? s - q2 : s;
-    const uint64_t d = U + q2 - V;
-    y = d * w.x - __umul64hi(d, w.y) * (q2 >> 1);
+// centred reduction: |result| <= q/2 (+1)
+__device__ __forceinline__ double f_center(double x, const FpMod &m) {
+    const double t = __dsub_rn(__fma_rn(x, m.qinv, kMagic), kMagic);
+    return __fma_rn(-t, m.q, x);
+}
+__device__ __forceinline__ double u2d(uint64_t x) {  // exact for x < 2^52
+    return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), kTwo52);
+}
+// centred value -> canonical residue as u64
+__device__ __forceinline__ uint64_t d2canon(double x, const FpMod &m) {
+    double c = f_center(x, m);
+    c = c < 0.0 ? __dadd_rn(c, m.q) : c;
+    c = c >= m.q ? __dsub_rn(c, m.q) : c;
+    return (uint64_t)__double_as_longlong(__dadd_rn(c, kTwo52)) & 0xFFFFFFFFFFFFFull;
 }
 
-// ---------------------------------------------------------------- forward
-__global__ void __launch_bounds__(512, 2) ntt16_fwd_cols(uint64_t *__restrict__ buf, int limb0, int B,
-                                                      const ulonglong2 *__restrict__ tw,
-                                                      const ModQ *__restrict__ mq) {
-    extern __shared__ uint64_t sm[];  // 256 x 32
-    const int tile = blockIdx.x & 7, b = blockIdx.x >> 3, l = blockIdx.y, m = limb0 + l;
-    const uint64_t q2 = 2 * mq[m].q;
-    const ulonglong2 *T = tw + (size_t)m * kN16;
-    uint64_t *poly = buf + ((size_t)l * B + b) * kN16;
+template <bool kBig>
+__device__ __forceinline__ void ct_f(double &x, double &y, double2 w, const FpMod &m) {
+    const double r = f_mulmod(y, w.x, w.y, m.q);
+    const double U = x;
+    x = __dadd_rn(U, r);
+    y = __dsub_rn(U, r);
+    if (kBig) {
+        x = f_center(x, m);
+        y = f_center(y, m);
+    }
+}
+template <bool kBig>
+__device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMod &m) {
+    const double U = x, V = y;
+    x = f_center(__dadd_rn(U, V), m);
+    y = f_mulmod(__dsub_rn(U, V), w.x, w.y, m.q);
+    if (kBig) y = f_center(y, m);
+}
+
+// ---------------------------------------------------------------- phases
+// column phase, forward: stages 0..7 on columns [32 tile, 32 tile + 32);
+// canonical u64 in, recentred doubles out (in place)
+template <bool kBig>
+__device__ __forceinline__ void fwd_cols(uint64_t *poly, int tile, const double2 *__restrict__ T, const FpMod &m,
+                                         double *sm) {
     const int c = threadIdx.x & 31, k = threadIdx.x >> 5, col = tile * 32 + c;
-    uint64_t x[16];
+    double x[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) x[u] = poly[(k + 16 * u) * 256 + col];
+    for (int u = 0; u < 16; ++u) x[u] = u2d(poly[(k + 16 * u) * 256 + col]);
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) ct_lazy(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], q2);
+            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) sm[(k + 16 * u) * 32 + c] = x[u];
@@ -84,33 +128,28 @@ __global__ void __launch_bounds__(512, 2) ntt16_fwd_cols(uint64_t *__restrict__ 
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) ct_lazy(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], q2);
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m);
     }
+    double *pd = reinterpret_cast<double *>(poly);
 #pragma unroll
-    for (int v = 0; v < 16; ++v) poly[(16 * k + v) * 256 + col] = x[v];
+    for (int v = 0; v < 16; ++v) pd[(16 * k + v) * 256 + col] = kBig ? x[v] : f_center(x[v], m);
 }
 
-__global__ void __launch_bounds__(512, 2) ntt16_fwd_rows(uint64_t *__restrict__ buf, int limb0, int B,
-                                                      const ulonglong2 *__restrict__ tw,
-                                                      const ModQ *__restrict__ mq) {
-    extern __shared__ uint64_t sm[];  // 32 x kRowPad
-    const int l = blockIdx.y, m = limb0 + l;
-    const uint64_t q2 = 2 * mq[m].q;
-    const ulonglong2 *T = tw + (size_t)m * kN16;
-    const int k = threadIdx.x & 15, rs = threadIdx.x >> 4;
-    const int job = blockIdx.x * 32 + rs;
-    const int r = job / B, b = job - r * B;
-    uint64_t *row = buf + ((size_t)l * B + b) * kN16 + r * 256;
-    uint64_t *srow = sm + rs * kRowPad;
-    uint64_t x[16];
+// row phase, forward: stages 8..15 of row r (16 threads per row), canonical out
+template <bool kBig>
+__device__ __forceinline__ void fwd_row(uint64_t *row, int r, const double2 *__restrict__ T, const FpMod &m,
+                                        double *srow) {
+    const int k = threadIdx.x & 15;
+    const double *rd = reinterpret_cast<const double *>(row);
+    double x[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) x[u] = row[k + 16 * u];
+    for (int u = 0; u < 16; ++u) x[u] = __ldcg(rd + k + 16 * u);
 #pragma unroll
     for (int sp = 0; sp < 4; ++sp) {
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) ct_lazy(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], q2);
+            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], m);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = x[u];
@@ -123,33 +162,25 @@ __global__ void __launch_bounds__(512, 2) ntt16_fwd_rows(uint64_t *__restrict__ 
 #pragma unroll
         for (int v = 0; v < 16; ++v)
             if (!(v & d))
-                ct_lazy(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], q2);
+                ct_f<kBig>(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], m);
     }
-    const ModQ mm = mq[m];
+    __syncwarp();
+    uint64_t *su = reinterpret_cast<uint64_t *>(srow);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) su[pad16(16 * k + v)] = d2canon(x[v], m);
     __syncwarp();
 #pragma unroll
-    for (int v = 0; v < 16; ++v) srow[pad16(16 * k + v)] = reduce128(0, x[v], mm);
-    __syncwarp();
-#pragma unroll
-    for (int u = 0; u < 16; ++u) row[k + 16 * u] = srow[pad16(k + 16 * u)];
+    for (int u = 0; u < 16; ++u) row[k + 16 * u] = su[pad16(k + 16 * u)];
 }
 
-// ---------------------------------------------------------------- inverse
-__global__ void __launch_bounds__(512, 2) ntt16_inv_rows(uint64_t *__restrict__ buf, int limb0, int B,
-                                                      const ulonglong2 *__restrict__ itw,
-                                                      const ModQ *__restrict__ mq) {
-    extern __shared__ uint64_t sm[];  // 32 x kRowPad
-    const int l = blockIdx.y, m = limb0 + l;
-    const uint64_t q2 = 2 * mq[m].q;
-    const ulonglong2 *T = itw + (size_t)m * kN16;
-    const int k = threadIdx.x & 15, rs = threadIdx.x >> 4;
-    const int job = blockIdx.x * 32 + rs;
-    const int r = job / B, b = job - r * B;
-    uint64_t *row = buf + ((size_t)l * B + b) * kN16 + r * 256;
-    uint64_t *srow = sm + rs * kRowPad;
-    uint64_t x[16];
+// row phase, inverse: stages 15..8 of row r; canonical u64 in, centred doubles out
+template <bool kBig>
+__device__ __forceinline__ void inv_row(uint64_t *row, int r, const double2 *__restrict__ T, const FpMod &m,
+                                        double *srow) {
+    const int k = threadIdx.x & 15;
+    double x[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = row[k + 16 * u];
+    for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = u2d(row[k + 16 * u]);
     __syncwarp();
 #pragma unroll
     for (int v = 0; v < 16; ++v) x[v] = srow[pad16(16 * k + v)];
@@ -159,7 +190,7 @@ __global__ void __launch_bounds__(512, 2) ntt16_inv_rows(uint64_t *__restrict__ 
 #pragma unroll
         for (int v = 0; v < 16; ++v)
             if (!(v & d))
-                gs_lazy(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], q2);
+                gs_f<kBig>(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], m);
     }
     __syncwarp();
 #pragma unroll
@@ -172,31 +203,28 @@ __global__ void __launch_bounds__(512, 2) ntt16_inv_rows(uint64_t *__restrict__ 
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_lazy(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], q2);
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], m);
     }
+    double *rd = reinterpret_cast<double *>(row);
 #pragma unroll
-    for (int u = 0; u < 16; ++u) row[k + 16 * u] = x[u];
+    for (int u = 0; u < 16; ++u) rd[k + 16 * u] = kBig ? x[u] : f_center(x[u], m);
 }
 
-__global__ void __launch_bounds__(512, 2) ntt16_inv_cols(uint64_t *__restrict__ buf, int limb0, int B,
-                                                      const ulonglong2 *__restrict__ itw,
-                                                      const ulonglong2 *__restrict__ ninv,
-                                                      const ModQ *__restrict__ mq) {
-    extern __shared__ uint64_t sm[];  // 256 x 32
-    const int tile = blockIdx.x & 7, b = blockIdx.x >> 3, l = blockIdx.y, m = limb0 + l;
-    const uint64_t q2 = 2 * mq[m].q;
-    const ulonglong2 *T = itw + (size_t)m * kN16;
-    uint64_t *poly = buf + ((size_t)l * B + b) * kN16;
+// column phase, inverse: stages 7..0, times N^-1, canonical out
+template <bool kBig>
+__device__ __forceinline__ void inv_cols(uint64_t *poly, int tile, const double2 *__restrict__ T, double2 ni,
+                                         const FpMod &m, double *sm) {
     const int c = threadIdx.x & 31, k = threadIdx.x >> 5, col = tile * 32 + c;
-    uint64_t x[16];
+    const double *pd = reinterpret_cast<const double *>(poly);
+    double x[16];
 #pragma unroll
-    for (int v = 0; v < 16; ++v) x[v] = poly[(16 * k + v) * 256 + col];
+    for (int v = 0; v < 16; ++v) x[v] = __ldcg(pd + (16 * k + v) * 256 + col);
 #pragma unroll
     for (int s = 7; s >= 4; --s) {
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_lazy(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], q2);
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m);
     }
 #pragma unroll
     for (int v = 0; v < 16; ++v) sm[(16 * k + v) * 32 + c] = x[v];
@@ -208,18 +236,65 @@ __global__ void __launch_bounds__(512, 2) ntt16_inv_cols(uint64_t *__restrict__ 
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_lazy(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], q2);
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m);
     }
-    const ulonglong2 ni = ninv[m];
-    const uint64_t q = q2 >> 1;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) poly[(k + 16 * u) * 256 + col] = mul_shoup(x[u], ni.x, ni.y, q);
+    for (int u = 0; u < 16; ++u)
+        poly[(k + 16 * u) * 256 + col] = d2canon(f_mulmod(x[u], ni.x, ni.y, m.q), m);
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- fused kernels
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
+    ntt16_fwd_fused(uint64_t *__restrict__ buf, int limb0, int B, const double2 *__restrict__ tw,
+                    const FpMod *__restrict__ fm) {
+    extern __shared__ double smd[];
+    const int c = blockIdx.x & 7;
+    const long long P = blockIdx.x >> 3;  // polynomial index = l * B + b
+    const int mi = limb0 + (int)(P / B);
+    const FpMod m = fm[mi];
+    const double2 *T = tw + (size_t)mi * kN16;
+    uint64_t *poly = buf + P * kN16;
+    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
+    if (m.q < (double)kSmallPrime) {
+        fwd_cols<false>(poly, c, T, m, smd);
+        cluster_sync_all();
+        fwd_row<false>(poly + r * 256, r, T, m, smd + rs * kRowPad);
+    } else {
+        fwd_cols<true>(poly, c, T, m, smd);
+        cluster_sync_all();
+        fwd_row<true>(poly + r * 256, r, T, m, smd + rs * kRowPad);
+    }
+}
+
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
+    ntt16_inv_fused(uint64_t *__restrict__ buf, int limb0, int B, const double2 *__restrict__ itw,
+                    const double2 *__restrict__ ninv, const FpMod *__restrict__ fm) {
+    extern __shared__ double smd[];
+    const int c = blockIdx.x & 7;
+    const long long P = blockIdx.x >> 3;
+    const int mi = limb0 + (int)(P / B);
+    const FpMod m = fm[mi];
+    const double2 *T = itw + (size_t)mi * kN16;
+    uint64_t *poly = buf + P * kN16;
+    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
+    if (m.q < (double)kSmallPrime) {
+        inv_row<false>(poly + r * 256, r, T, m, smd + rs * kRowPad);
+        cluster_sync_all();
+        inv_cols<false>(poly, c, T, ninv[mi], m, smd);
+    } else {
+        inv_row<true>(poly + r * 256, r, T, m, smd + rs * kRowPad);
+        cluster_sync_all();
+        inv_cols<true>(poly, c, T, ninv[mi], m, smd);
+    }
 }
 
 // ---------------------------------------------------------------- generic N
 __global__ void ntt_stage_fwd(uint64_t *__restrict__ buf, int limb0, int B, int log_n, int s,
-                              const ulonglong2 *__restrict__ tw, const ModQ *__restrict__ mq,
-                              long long total) {
+                              const ulonglong2 *__restrict__ tw, const ModQ *__restrict__ mq, long long total) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= total) return;
     const int N = 1 << log_n, half = N >> 1;
@@ -233,8 +308,7 @@ __global__ void ntt_stage_fwd(uint64_t *__restrict__ buf, int limb0, int B, int 
 }
 
 __global__ void ntt_stage_inv(uint64_t *__restrict__ buf, int limb0, int B, int log_n, int s,
-                              const ulonglong2 *__restrict__ itw, const ModQ *__restrict__ mq,
-                              long long total) {
+                              const ulonglong2 *__restrict__ itw, const ModQ *__restrict__ mq, long long total) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= total) return;
     const int N = 1 << log_n, half = N >> 1;
@@ -247,9 +321,8 @@ __global__ void ntt_stage_inv(uint64_t *__restrict__ buf, int limb0, int B, int 
     gs_bfly(a[j], a[j + t], itw[(size_t)m * N + (1 << s) + i], mq[m].q);
 }
 
-__global__ void scale_ninv(uint64_t *__restrict__ buf, int limb0, int B, int log_n,
-                           const ulonglong2 *__restrict__ ninv, const ModQ *__restrict__ mq,
-                           long long total) {
+__global__ void scale_ninv(uint64_t *__restrict__ buf, int limb0, int B, int log_n, const ulonglong2 *__restrict__ ninv,
+                           const ModQ *__restrict__ mq, long long total) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= total) return;
     const int m = limb0 + (int)(gid >> log_n) / B;
@@ -257,16 +330,13 @@ __global__ void scale_ninv(uint64_t *__restrict__ buf, int limb0, int B, int log
     buf[gid] = mul_shoup(buf[gid], ni.x, ni.y, mq[m].q);
 }
 
-constexpr int kColSmem = 256 * 32 * 8;
-constexpr int kRowSmem = 32 * kRowPad * 8;
+constexpr int kFusedSmem = 32 * kRowPad * 8;  // >= 256 * 32 * 8 for the column phase
 
 void ntt16_set_attrs() {
     static bool done = false;
     if (done) return;
-    cudaFuncSetAttribute(ntt16_fwd_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmem);
-    cudaFuncSetAttribute(ntt16_inv_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, kColSmem);
-    cudaFuncSetAttribute(ntt16_fwd_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmem);
-    cudaFuncSetAttribute(ntt16_inv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, kRowSmem);
+    cudaFuncSetAttribute(ntt16_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem);
+    cudaFuncSetAttribute(ntt16_inv_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedSmem);
     done = true;
 }
 
@@ -276,9 +346,10 @@ int ntt_fwd_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int B, int)
     if (n_limbs <= 0 || B <= 0) return HK_OK;
     if (c->log_n == kLogN16) {
         ntt16_set_attrs();
-        dim3 gc(8 * B, n_limbs), gr(8 * B, n_limbs);
-        ntt16_fwd_cols<<<gc, 512, kColSmem, c->stream>>>(buf, limb0, B, c->d_tw, c->d_modq); ++c->launches;
-        ntt16_fwd_rows<<<gr, 512, kRowSmem, c->stream>>>(buf, limb0, B, c->d_tw, c->d_modq); ++c->launches;
+        const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
+        ntt16_fwd_fused<<<blocks, 512, kFusedSmem, c->stream>>>(buf, limb0, B, (const double2 *)c->d_twf,
+                                                                 (const FpMod *)c->d_fmod);
+        ++c->launches;
     } else {
         const long long total = (long long)n_limbs * B * (c->n / 2);
         for (int s = 0; s < c->log_n; ++s) {
@@ -295,9 +366,10 @@ int ntt_inv_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int B, int)
     if (n_limbs <= 0 || B <= 0) return HK_OK;
     if (c->log_n == kLogN16) {
         ntt16_set_attrs();
-        dim3 gc(8 * B, n_limbs), gr(8 * B, n_limbs);
-        ntt16_inv_rows<<<gr, 512, kRowSmem, c->stream>>>(buf, limb0, B, c->d_itw, c->d_modq); ++c->launches;
-        ntt16_inv_cols<<<gc, 512, kColSmem, c->stream>>>(buf, limb0, B, c->d_itw, c->d_ninv, c->d_modq); ++c->launches;
+        const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
+        ntt16_inv_fused<<<blocks, 512, kFusedSmem, c->stream>>>(buf, limb0, B, (const double2 *)c->d_itwf,
+                                                                 (const double2 *)c->d_ninvf, (const FpMod *)c->d_fmod);
+        ++c->launches;
     } else {
         const long long total = (long long)n_limbs * B * (c->n / 2);
         for (int s = c->log_n - 1; s >= 0; --s) {
@@ -306,8 +378,8 @@ int ntt_inv_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int B, int)
             ++c->launches;
         }
         const long long all = (long long)n_limbs * B * c->n;
-        scale_ninv<<<hk_grid(all, 256), 256, 0, c->stream>>>(buf, limb0, B, c->log_n, c->d_ninv, c->d_modq,
-                                                              all); ++c->launches;
+        scale_ninv<<<hk_grid(all, 256), 256, 0, c->stream>>>(buf, limb0, B, c->log_n, c->d_ninv, c->d_modq, all);
+        ++c->launches;
     }
     HK_LAUNCH_CHECK(c, "ntt_inv");
     return HK_OK;

@@ -10,9 +10,10 @@ This module supplies the chain that the reference's level maps onto:
 * every multiplication drops ``q_l`` by rescaling, exactly mirroring
   ``level -= 1`` in `HeBackend.slotwise` (`backend.py:215-224`);
 * ``q_0`` is ~50 bits and the rescaling primes sit next to the scale
-  (~2^46), after the paper's 51/46/51 chain (`PAPER.md:321`). All primes are
-  kept below 2^50 so 4q fits comfortably in 64 bits and lazy reductions are
-  cheap on the GPU.
+  (~2^46), after the paper's 51/46/51 chain (`PAPER.md:321`); the special
+  primes sit just below 2^47 (alpha of them: P / Q_digit >= 2^13). Every prime
+  is in (2^40, 2^50) (25-bit split MACs) and all but q_0 are below 2^47, which
+  keeps the GPU's float64 NTT free of intra-phase reductions.
 
 Canonical scales. Ciphertexts at level ``l`` always carry scale
 ``Delta_l``. The chain is built top-down with ``Delta_L = 2^scale_bits`` and
@@ -166,7 +167,7 @@ class CkksParams:
 
 
 def make_params(log_n: int, depth: int, scale_bits: int = 46, q0_bits: int = 50,
-                special_bits: int = 50, dnum: int = 3, n_special: int | None = None,
+                special_bits: int = 47, dnum: int = 3, n_special: int | None = None,
                 label: str = "") -> CkksParams:
     """Scale-stable chain: q_0 just below 2^q0_bits, rescaling primes chosen
     top-down so the canonical scale never drifts from 2^scale_bits."""
@@ -201,7 +202,7 @@ def make_params(log_n: int, depth: int, scale_bits: int = 46, q0_bits: int = 50,
 
 def kan_params(depth: int, log_n: int = 16, dnum: int = 3) -> CkksParams:
     """Encrypted-KAN chain (paper-style 50/46/50 bits, `PAPER.md:321`)."""
-    return make_params(log_n, depth, scale_bits=46, q0_bits=50, special_bits=50,
+    return make_params(log_n, depth, scale_bits=46, q0_bits=50, special_bits=47,
                        dnum=dnum, label=f"kan-L{depth}")
 
 
