@@ -1,0 +1,311 @@
+// ntt16.cuh — fused N = 2^16 negacyclic NTT kernels with prologue/epilogue hooks.
+//
+// One 8-CTA thread-block cluster per polynomial (see ntt.cu for the stage
+// split). The first phase reads its inputs through a prologue functor and the
+// second phase hands canonical outputs to an epilogue functor, so element-wise
+// work that surrounds an NTT in CKKS (basis conversion, the rescale
+// remainder broadcast, plaintext products, the ModDown / rescale finish) runs
+// inside the NTT's own global loads/stores instead of as separate passes.
+//
+//   Pro: __device__ uint64_t operator()(int l, long long P, int idx) const
+//        canonical residue (mod the launch's prime l) of input element idx of
+//        polynomial P (= l * B + b within the launch)
+//   Epi: __device__ void operator()(int l, long long P, int idx, uint64_t v) const
+//        consume canonical output v
+// `inter` ([limbs][B][N] words) holds the between-phase data; it may alias the
+// epilogue's output.
+//
+// Residues live in float64 registers as exact integers (|x| < 2^51): the
+// DFMA/DMUL pipe (64/clk/SM on B200) carries the modular multiply as an exact
+// two-product Shoup step. Small primes (q < 2^47) need no reduction inside a
+// phase (8 stages from |x| < q stay below 13 q < 2^51); the phase boundary
+// recentres. Large primes (q_0 ~ 2^50) recentre after every stage.
+#pragma once
+
+#include "common.cuh"
+
+namespace ntt16 {
+
+constexpr int kLogN = 16;
+constexpr int kN = 1 << kLogN;
+constexpr int kRowPad = 272;                 // 256 + 16: pad one element every 16
+constexpr int kSmem = 32 * kRowPad * 8;      // >= 256 * 32 * 8 for the column phase
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;  // 2^52
+constexpr uint64_t kSmallPrime = 1ull << 47;
+
+struct FpMod {
+    double q, qinv;
+};
+
+__device__ __forceinline__ int pad16(int c) { return c + (c >> 4); }
+
+__device__ __forceinline__ double f_mulmod(double y, double w, double wq, double q) {
+    const double h = __dmul_rn(y, w);
+    const double l = __fma_rn(y, w, -h);
+    const double t = __dsub_rn(__fma_rn(y, wq, kMagic), kMagic);
+    return __dadd_rn(__fma_rn(-t, q, h), l);
+}
+__device__ __forceinline__ double f_center(double x, const FpMod &m) {
+    const double t = __dsub_rn(__fma_rn(x, m.qinv, kMagic), kMagic);
+    return __fma_rn(-t, m.q, x);
+}
+__device__ __forceinline__ double u2d(uint64_t x) {  // exact for x < 2^52
+    return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), kTwo52);
+}
+__device__ __forceinline__ uint64_t d2canon(double x, const FpMod &m) {
+    double c = f_center(x, m);
+    c = c < 0.0 ? __dadd_rn(c, m.q) : c;
+    c = c >= m.q ? __dsub_rn(c, m.q) : c;
+    return (uint64_t)__double_as_longlong(__dadd_rn(c, kTwo52)) & 0xFFFFFFFFFFFFFull;
+}
+
+template <bool kBig>
+__device__ __forceinline__ void ct_f(double &x, double &y, double2 w, const FpMod &m) {
+    const double r = f_mulmod(y, w.x, w.y, m.q);
+    const double U = x;
+    x = __dadd_rn(U, r);
+    y = __dsub_rn(U, r);
+    if (kBig) {
+        x = f_center(x, m);
+        y = f_center(y, m);
+    }
+}
+template <bool kBig>
+__device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMod &m) {
+    const double U = x, V = y;
+    x = f_center(__dadd_rn(U, V), m);
+    y = f_mulmod(__dsub_rn(U, V), w.x, w.y, m.q);
+    if (kBig) y = f_center(y, m);
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- forward
+template <bool kBig, class Pro>
+__device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, double *inter, int tile,
+                                         const double2 *__restrict__ T, const FpMod &m, double *sm) {
+    const int c = threadIdx.x & 31, k = threadIdx.x >> 5, col = tile * 32 + c;
+    double x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = u2d(pro(l, P, (k + 16 * u) * 256 + col));
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int d = 8 >> s;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) sm[(k + 16 * u) * 32 + c] = x[u];
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = sm[(16 * k + v) * 32 + c];
+#pragma unroll
+    for (int s = 4; s < 8; ++s) {
+        const int d = 128 >> s;
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m);
+    }
+#pragma unroll
+    for (int v = 0; v < 16; ++v) inter[(16 * k + v) * 256 + col] = kBig ? x[v] : f_center(x[v], m);
+}
+
+template <bool kBig, class Epi>
+__device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, const double *inter, int r,
+                                        const double2 *__restrict__ T, const FpMod &m, double *srow) {
+    const int k = threadIdx.x & 15;
+    const double *rd = inter + r * 256;
+    double x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = __ldcg(rd + k + 16 * u);
+#pragma unroll
+    for (int sp = 0; sp < 4; ++sp) {
+        const int d = 8 >> sp;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], m);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = x[u];
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = srow[pad16(16 * k + v)];
+#pragma unroll
+    for (int sp = 4; sp < 8; ++sp) {
+        const int d = 128 >> sp;
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+            if (!(v & d))
+                ct_f<kBig>(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], m);
+    }
+    __syncwarp();
+    uint64_t *su = reinterpret_cast<uint64_t *>(srow);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) su[pad16(16 * k + v)] = d2canon(x[v], m);
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) epi(l, P, r * 256 + k + 16 * u, su[pad16(k + 16 * u)]);
+}
+
+template <class Pro, class Epi>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
+    fwd_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ tw,
+               const FpMod *__restrict__ fm, Pro pro, Epi epi) {
+    extern __shared__ double smd[];
+    const int c = blockIdx.x & 7;
+    const long long P = blockIdx.x >> 3;
+    const int l = (int)(P / B), mi = limb0 + l;
+    const FpMod m = fm[mi];
+    const double2 *T = tw + (size_t)mi * kN;
+    double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
+    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
+    if (m.q < (double)kSmallPrime) {
+        fwd_cols<false>(pro, l, P, inter, c, T, m, smd);
+        cluster_sync_all();
+        fwd_row<false>(epi, l, P, inter, r, T, m, smd + rs * kRowPad);
+    } else {
+        fwd_cols<true>(pro, l, P, inter, c, T, m, smd);
+        cluster_sync_all();
+        fwd_row<true>(epi, l, P, inter, r, T, m, smd + rs * kRowPad);
+    }
+}
+
+// ---------------------------------------------------------------- inverse
+template <bool kBig, class Pro>
+__device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, double *inter, int r,
+                                        const double2 *__restrict__ T, const FpMod &m, double *srow) {
+    const int k = threadIdx.x & 15;
+    double x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = u2d(pro(l, P, r * 256 + k + 16 * u));
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = srow[pad16(16 * k + v)];
+#pragma unroll
+    for (int sp = 7; sp >= 4; --sp) {
+        const int d = 128 >> sp;
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+            if (!(v & d))
+                gs_f<kBig>(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], m);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) srow[pad16(16 * k + v)] = x[v];
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = srow[pad16(k + 16 * u)];
+#pragma unroll
+    for (int sp = 3; sp >= 0; --sp) {
+        const int d = 8 >> sp;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], m);
+    }
+    double *rd = inter + r * 256;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) rd[k + 16 * u] = kBig ? x[u] : f_center(x[u], m);
+}
+
+template <bool kBig, class Epi>
+__device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, const double *inter, int tile,
+                                         const double2 *__restrict__ T, double2 ni, const FpMod &m, double *sm) {
+    const int c = threadIdx.x & 31, k = threadIdx.x >> 5, col = tile * 32 + c;
+    double x[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = __ldcg(inter + (16 * k + v) * 256 + col);
+#pragma unroll
+    for (int s = 7; s >= 4; --s) {
+        const int d = 128 >> s;
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m);
+    }
+#pragma unroll
+    for (int v = 0; v < 16; ++v) sm[(16 * k + v) * 32 + c] = x[v];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = sm[(k + 16 * u) * 32 + c];
+#pragma unroll
+    for (int s = 3; s >= 0; --s) {
+        const int d = 8 >> s;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) epi(l, P, (k + 16 * u) * 256 + col, d2canon(f_mulmod(x[u], ni.x, ni.y, m.q), m));
+}
+
+template <class Pro, class Epi>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
+    inv_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ itw,
+               const double2 *__restrict__ ninv, const FpMod *__restrict__ fm, Pro pro, Epi epi) {
+    extern __shared__ double smd[];
+    const int c = blockIdx.x & 7;
+    const long long P = blockIdx.x >> 3;
+    const int l = (int)(P / B), mi = limb0 + l;
+    const FpMod m = fm[mi];
+    const double2 *T = itw + (size_t)mi * kN;
+    double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
+    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
+    if (m.q < (double)kSmallPrime) {
+        inv_row<false>(pro, l, P, inter, r, T, m, smd + rs * kRowPad);
+        cluster_sync_all();
+        inv_cols<false>(epi, l, P, inter, c, T, ninv[mi], m, smd);
+    } else {
+        inv_row<true>(pro, l, P, inter, r, T, m, smd + rs * kRowPad);
+        cluster_sync_all();
+        inv_cols<true>(epi, l, P, inter, c, T, ninv[mi], m, smd);
+    }
+}
+
+// ---------------------------------------------------------------- functors
+struct ProPlain {  // in[P][idx]
+    const uint64_t *in;
+    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const { return in[P * kN + idx]; }
+};
+struct EpiPlain {  // out[P][idx] = v
+    uint64_t *out;
+    __device__ __forceinline__ void operator()(int, long long P, int idx, uint64_t v) const { out[P * kN + idx] = v; }
+};
+
+// ---------------------------------------------------------------- launchers
+template <class Pro, class Epi>
+inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
+    if (n_limbs <= 0 || B <= 0) return HK_OK;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fwd_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        attr = true;
+    }
+    const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
+    fwd_kernel<Pro, Epi><<<blocks, 512, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_twf,
+                                                             (const FpMod *)c->d_fmod, pro, epi);
+    ++c->launches;
+    HK_LAUNCH_CHECK(c, "ntt16 fwd");
+    return HK_OK;
+}
+
+template <class Pro, class Epi>
+inline int launch_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
+    if (n_limbs <= 0 || B <= 0) return HK_OK;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(inv_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        attr = true;
+    }
+    const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
+    inv_kernel<Pro, Epi><<<blocks, 512, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_itwf,
+                                                             (const double2 *)c->d_ninvf, (const FpMod *)c->d_fmod,
+                                                             pro, epi);
+    ++c->launches;
+    HK_LAUNCH_CHECK(c, "ntt16 inv");
+    return HK_OK;
+}
+
+}  // namespace ntt16

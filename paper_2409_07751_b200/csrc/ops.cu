@@ -8,8 +8,9 @@
 // basis conversion + NTT), key inner product (128-bit lazy accumulation over
 // digits, one Barrett reduction), ModDown by the special primes P.
 #include <algorithm>
+#include <cstring>
 
-#include "common.cuh"
+#include "ntt16.cuh"
 
 int automorph_launch(hk_ctx *c, const uint64_t *in, uint64_t *out, uint32_t g, long long n_polys);
 
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
                                               const uint64_t *__restrict__ hat, const int32_t *__restrict__ src_mod,
                                               const int32_t *__restrict__ dst_mod, int n_dst,
                                               uint64_t *__restrict__ dst, int mode, int l, int n_q, long long BN,
-                                              const ModQ *__restrict__ mq) {
+                                              const ModQ *__restrict__ mq, int prescaled) {
     extern __shared__ uint64_t sh[];  // hat [n_dst][n_src] as (h0 | h1 << 32), ModQ [n_dst], out index [n_dst]
     ModQ *smq = (ModQ *)(sh + n_dst * n_src);
     int *sidx = (int *)(smq + n_dst);
@@ -175,8 +176,8 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         if (i < n_src) {
-            const uint64_t qi = mq[src_mod[i]].q;
-            split25(mul_shoup(src[(long long)i * BN + e], inv[i], inv_sh[i], qi), v0[i], v1[i]);
+            const uint64_t x = src[(long long)i * BN + e];
+            split25(prescaled ? x : mul_shoup(x, inv[i], inv_sh[i], mq[src_mod[i]].q), v0[i], v1[i]);
         }
     }
     for (int d = 0; d < n_dst; ++d) {
@@ -194,9 +195,10 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
 }
 
 // acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][chain(t)] ; grid (BN/256, ne)
-__global__ void k_key_ip(const uint64_t *__restrict__ ext, int nd, int ne, int l, int n_q, int nm, int log_n,
-                         const uint64_t *__restrict__ key, uint32_t g, uint64_t *__restrict__ acc0,
-                         uint64_t *__restrict__ acc1, const ModQ *__restrict__ mq, long long BN) {
+__global__ void k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d, int alpha, int nd, int ne,
+                         int l, int n_q, int nm, int log_n, const uint64_t *__restrict__ key, uint32_t g,
+                         uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1, const ModQ *__restrict__ mq,
+                         long long BN) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= BN) return;
     const int t = blockIdx.y;
@@ -210,7 +212,8 @@ __global__ void k_key_ip(const uint64_t *__restrict__ ext, int nd, int ne, int l
     acc3_zero(a1);
     for (int j = 0; j < nd; ++j) {
         uint32_t x0, x1, y0, y1;
-        split25(ext[((long long)j * ne + t) * BN + src_e], x0, x1);
+        const bool own = t >= j * alpha && t < (j + 1) * alpha && t <= l;  // digit's own limb: NTT form of d
+        split25(own ? d[(long long)t * BN + src_e] : ext[((long long)j * ne + t) * BN + src_e], x0, x1);
         const uint64_t *kj = key + ((size_t)j * 2 * nm + m) * N;
         split25(kj[k], y0, y1);
         acc3_mac(a0, x0, x1, y0, y1);
@@ -244,6 +247,146 @@ __global__ void k_md_finish(const uint64_t *__restrict__ acc, const uint64_t *__
     out[o] = r;
 }
 
+
+// ---------------------------------------------------------------------------
+// N = 2^16 fused flows: prologue/epilogue functors for ntt16::launch_fwd/inv
+// ---------------------------------------------------------------------------
+enum { SRC_PLAIN = 0, SRC_MULPT = 1, SRC_MULCONST = 2, SRC_MAC = 3, SRC_SUM2 = 4 };
+
+// Value X(p, l, b, idx) of the ciphertext about to be rescaled, produced on
+// the fly: a, a (.) pt, a * k, sum_i babies_i (.) pts_i, or a + a2.
+template <int KIND>
+struct RsSrc {
+    const uint64_t *a;
+    const uint64_t *a2;
+    const uint64_t *pt;
+    int la, pb, n, log_n;
+    long long BN;
+    const ModQ *mq;
+    Residues k;
+    PtrList babies, pts;
+    __device__ __forceinline__ uint64_t operator()(int p, int l, int b, int idx) const {
+        const long long o = ((long long)p * (la + 1) + l) * BN + ((long long)b << log_n) + idx;
+        if (KIND == SRC_PLAIN) return a[o];
+        if (KIND == SRC_SUM2) return add_mod(a[o], a2[o], mq[l].q);
+        if (KIND == SRC_MULCONST) return mul_mod(a[o], k.v[l], mq[l]);
+        if (KIND == SRC_MULPT)
+            return mul_mod(a[o], pt[(((long long)l * pb + (pb == 1 ? 0 : b)) << log_n) + idx], mq[l]);
+        Acc3 acc;
+        acc3_zero(acc);
+        const long long pe = ((long long)l << log_n) + idx;
+        for (int i = 0; i < n; ++i) acc3_mac(acc, babies.p[i][o], pts.p[i][pe]);
+        return acc3_reduce(acc, mq[l]);
+    }
+};
+
+// iNTT prologue for the dropped limb: launch P = p * B + b, prime index la
+template <int KIND>
+struct ProLast {
+    RsSrc<KIND> src;
+    int B;
+    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
+        const int pb = (int)P, p = pb >= B ? 1 : 0;
+        return src(p, src.la, pb - p * B, idx);
+    }
+};
+
+// NTT prologue: centred remainder of the dropped limb, reduced mod q_l
+struct ProRsBcast {
+    const uint64_t *L;
+    uint64_t ql;
+    int B2, log_n;
+    const ModQ *mq;
+    __device__ __forceinline__ uint64_t operator()(int l, long long P, int idx) const {
+        const long long pb = P - (long long)l * B2;
+        const uint64_t x = L[(pb << log_n) + idx];
+        const bool neg = x > (ql >> 1);
+        const uint64_t mag = neg ? ql - x : x;
+        const ModQ m = mq[l];
+        const uint64_t r = reduce128(0, mag, m);
+        return neg ? (r ? m.q - r : 0) : r;
+    }
+};
+
+// NTT epilogue: out[p][l][b] = (X - v) * q_la^-1
+template <int KIND>
+struct EpiRescale {
+    RsSrc<KIND> src;
+    uint64_t *out;
+    const ulonglong2 *qinv;
+    int B;
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        const int pb = (int)(P - (long long)l * 2 * B), p = pb >= B ? 1 : 0, b = pb - p * B;
+        const uint64_t q = src.mq[l].q;
+        const ulonglong2 w = qinv[l];
+        const uint64_t x = src(p, l, b, idx);
+        out[((long long)p * src.la + l) * src.BN + ((long long)b << src.log_n) + idx] =
+            mul_shoup(sub_mod(x, v, q), w.x, w.y, q);
+    }
+};
+
+// iNTT epilogue: scale by a per-limb constant (basis-conversion inv_i)
+struct EpiScale {
+    uint64_t *out;
+    const uint64_t *inv, *inv_sh;
+    const ModQ *mq;
+    int mi0;
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        out[P * ntt16::kN + idx] = mul_shoup(v, inv[l], inv_sh[l], mq[mi0 + l].q);
+    }
+};
+// same, per-digit tables (ModUp sources at one level)
+struct EpiScaleDigits {
+    uint64_t *out;
+    const uint64_t *inv[8], *inv_sh[8];
+    int alpha;
+    const ModQ *mq;
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        const int j = l / alpha, i = l - j * alpha;
+        out[P * ntt16::kN + idx] = mul_shoup(v, inv[j][i], inv_sh[j][i], mq[l].q);
+    }
+};
+
+// NTT prologue: fast basis conversion from pre-scaled sources (launch limb l
+// is target row `row0 + l` of the conversion table)
+struct ProConv {
+    const uint64_t *src;  // [n_src][B][N], already multiplied by inv_i
+    const uint64_t *hat;  // [n_dst][n_src]
+    int n_src, row0, B, mi0, log_n;
+    long long BN;
+    const ModQ *mq;
+    __device__ __forceinline__ uint64_t operator()(int l, long long P, int idx) const {
+        const long long e = ((P - (long long)l * B) << log_n) + idx;
+        const uint64_t *h = hat + (long long)(row0 + l) * n_src;
+        Acc3 acc;
+        acc3_zero(acc);
+        for (int i = 0; i < n_src; ++i) acc3_mac(acc, src[i * BN + e], h[i]);
+        return acc3_reduce(acc, mq[mi0 + l]);
+    }
+};
+
+// NTT epilogue: ModDown finish (acc - v) * P^-1 (+ sigma_g(addend))
+struct EpiModDown {
+    const uint64_t *acc, *addend;
+    uint64_t *out;
+    const ulonglong2 *pinv;
+    const ModQ *mq;
+    uint32_t g;
+    int B, log_n;
+    long long BN;
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 w = pinv[l];
+        uint64_t r = mul_shoup(sub_mod(acc[o], v, q), w.x, w.y, q);
+        if (addend) {
+            const long long src = g == 1u ? o : o - idx + auto_src((uint32_t)idx, g, log_n);
+            r = add_mod(r, addend[src], q);
+        }
+        out[o] = r;
+    }
+};
+
 }  // namespace
 
 static dim3 egrid(long long BN, int limbs, int polys) {
@@ -252,7 +395,7 @@ static dim3 egrid(long long BN, int limbs, int polys) {
 
 // basis conversion launcher: picks the register-array size, stages hat in smem
 static int conv_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l,
-                       long long BN, int n_dst = -1) {
+                       long long BN, int n_dst = -1, int prescaled = 0) {
     if (n_dst < 0) n_dst = T.n_dst;
     const size_t smem = sizeof(uint64_t) * (size_t)n_dst * T.n_src + sizeof(ModQ) * n_dst + sizeof(int) * n_dst;
     const dim3 grid((unsigned)((BN + 127) / 128));
@@ -261,7 +404,8 @@ static int conv_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint6
         if (smem > 48 * 1024)                                                                                 \
             cudaFuncSetAttribute(k_conv<NSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
         k_conv<NSV><<<grid, 128, smem, c->stream>>>(src, T.n_src, T.d_inv, T.d_inv_sh, T.d_hat, T.d_src_mod, \
-                                                     T.d_dst_mod, n_dst, dst, mode, l, c->n_q, BN, c->d_modq); \
+                                                     T.d_dst_mod, n_dst, dst, mode, l, c->n_q, BN, c->d_modq,    \
+                                                     prescaled);                                              \
         ++c->launches;                                                                                        \
         HK_LAUNCH_CHECK(c, "basis conversion");                                                              \
         return HK_OK;                                                                                         \
@@ -307,9 +451,14 @@ int rescale_launch(hk_ctx *c, const uint64_t *in, int l, int B, uint64_t *out, u
 
 // Key switch d (NTT, [l+1][B][N]) under n keys; for key r writes
 //   out0[r] = ks0 (+ sigma_g(add0) if add0) and out1[r] = ks1, each [l+1][B][N].
+static int keyswitch_fused(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
+                           const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
+                           uint64_t *scratch);
+
 static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
                      const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
                      uint64_t *scratch) {
+    if (c->log_n == ntt16::kLogN) return keyswitch_fused(c, d, l, B, n, keys, gal, out0, out1, add0, scratch);
     const int N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
     const long long BN = (long long)B * N;
     uint64_t *dc = scratch;
@@ -330,13 +479,11 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const ui
         if (d0 > 0 && (rc = ntt_fwd_launch(c, ej, 0, d0, B, 0))) return rc;
         if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
         if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
-        HK_CUDA(c, cudaMemcpyAsync(ej + (size_t)d0 * BN, d + (size_t)d0 * BN, sizeof(uint64_t) * (d1 - d0) * BN,
-                                   cudaMemcpyDeviceToDevice, c->stream));
     }
     // per key: inner product, ModDown of both halves
     for (int r = 0; r < n; ++r) {
-        k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(ext, nd, ne, l, c->n_q, c->n_mod, c->log_n, keys[r],
-                                                          gal[r], acc, acc + (size_t)ne * BN, c->d_modq, BN);
+        k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(ext, d, c->alpha, nd, ne, l, c->n_q, c->n_mod, c->log_n,
+                                                          keys[r], gal[r], acc, acc + (size_t)ne * BN, c->d_modq, BN);
         ++c->launches;
         HK_LAUNCH_CHECK(c, "key inner product");
         for (int p = 0; p < 2; ++p) {
@@ -354,6 +501,84 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const ui
                                                                    c->d_pinv, c->d_modq);
             ++c->launches;
             HK_LAUNCH_CHECK(c, "moddown finish");
+        }
+    }
+    return HK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fused rescale / key switch (N = 2^16)
+// ---------------------------------------------------------------------------
+template <int KIND>
+static int rescale_fused(hk_ctx *c, const RsSrc<KIND> &src, int l, int B, uint64_t *out, uint64_t *scratch) {
+    const long long BN = (long long)B * c->n;
+    uint64_t *L = scratch, *inter = scratch + 2 * BN;
+    int rc = ntt16::launch_inv(c, L, l, 1, 2 * B, ProLast<KIND>{src, B}, ntt16::EpiPlain{L});
+    if (rc) return rc;
+    ProRsBcast pro{L, c->mod_h[l], 2 * B, c->log_n, c->d_modq};
+    EpiRescale<KIND> epi{src, out, c->d_rs_qinv + (size_t)l * c->n_q, B};
+    return ntt16::launch_fwd(c, inter, 0, l, 2 * B, pro, epi);
+}
+
+template <int KIND>
+static RsSrc<KIND> make_src(hk_ctx *c, const uint64_t *a, int la, int B) {
+    RsSrc<KIND> s;
+    memset(&s, 0, sizeof s);
+    s.a = a;
+    s.la = la;
+    s.log_n = c->log_n;
+    s.BN = (long long)B * c->n;
+    s.mq = c->d_modq;
+    return s;
+}
+
+static int keyswitch_fused(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
+                           const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
+                           uint64_t *scratch) {
+    const int N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
+    const long long BN = (long long)B * N;
+    uint64_t *dc = scratch;
+    uint64_t *ext = dc + (size_t)(l + 1) * BN;
+    uint64_t *acc = ext + (size_t)nd * ne * BN;
+    uint64_t *sp = acc + (size_t)2 * ne * BN;
+    uint64_t *conv = sp + (size_t)np * BN;
+    // ModUp: coefficient form of d, scaled by each digit's (Q_D / q_i)^-1
+    EpiScaleDigits esd;
+    memset(&esd, 0, sizeof esd);
+    esd.out = dc;
+    esd.alpha = c->alpha;
+    esd.mq = c->d_modq;
+    if (nd > 8) return hk_fail(c, HK_E_ARG, "more than 8 key-switching digits");
+    for (int j = 0; j < nd; ++j) {
+        esd.inv[j] = c->modup[l][j].d_inv;
+        esd.inv_sh[j] = c->modup[l][j].d_inv_sh;
+    }
+    int rc = ntt16::launch_inv(c, dc, 0, l + 1, B, ntt16::ProPlain{d}, esd);
+    if (rc) return rc;
+    for (int j = 0; j < nd; ++j) {
+        const ConvTable &T = c->modup[l][j];
+        const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, l + 1);
+        uint64_t *ej = ext + (size_t)j * ne * BN;
+        if ((rc = conv_launch(c, T, dc + (size_t)d0 * BN, ej, 0, l, BN, -1, 1))) return rc;
+        if (d0 > 0 && (rc = ntt_fwd_launch(c, ej, 0, d0, B, 0))) return rc;
+        if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
+        if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
+    }
+    for (int r = 0; r < n; ++r) {
+        k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(ext, d, c->alpha, nd, ne, l, c->n_q, c->n_mod, c->log_n,
+                                                          keys[r], gal[r], acc, acc + (size_t)ne * BN, c->d_modq, BN);
+        ++c->launches;
+        HK_LAUNCH_CHECK(c, "key inner product");
+        for (int p = 0; p < 2; ++p) {
+            const uint64_t *a = acc + (size_t)p * ne * BN;
+            const ConvTable &T = c->moddown;
+            EpiScale es{sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q};
+            if ((rc = ntt16::launch_inv(c, sp, c->n_q, np, B, ntt16::ProPlain{a + (size_t)(l + 1) * BN}, es)))
+                return rc;
+            if ((rc = conv_launch(c, T, sp, conv, 1, l, BN, l + 1, 1))) return rc;
+            EpiModDown epi{a, p == 0 ? add0 : nullptr, p == 0 ? out0[r] : out1[r], c->d_pinv, c->d_modq, gal[r], B,
+                           c->log_n, BN};
+            if ((rc = ntt16::launch_fwd(c, conv, 0, l + 1, B, ntt16::ProPlain{conv}, epi))) return rc;
         }
     }
     return HK_OK;
@@ -404,6 +629,7 @@ int hk_rescale(hk_ctx *c, const uint64_t *a, int32_t la, uint64_t *out, int32_t 
     if (la < 1 || la >= c->n_q) return hk_fail(c, HK_E_DEPTH, "rescale at level %d", la);
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "rescale workspace");
+    if (c->log_n == ntt16::kLogN) return rescale_fused(c, make_src<SRC_PLAIN>(c, a, la, B), la, B, out, ws);
     return rescale_launch(c, a, la, B, out, ws);
 }
 
@@ -413,6 +639,14 @@ int hk_mul_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, i
     if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
     if (pb != 1 && pb != B) return hk_fail(c, HK_E_LENGTH, "mul_plain: plaintext batch");
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
+    if (c->log_n == ntt16::kLogN) {
+        uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
+        if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_plain workspace");
+        RsSrc<SRC_MULPT> src = make_src<SRC_MULPT>(c, a, la, B);
+        src.pt = pt;
+        src.pb = pb;
+        return rescale_fused(c, src, la, B, out, ws);
+    }
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_plain workspace");
     k_mul_plain<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, pt, pb, ws, BN, c->log_n, c->d_modq); ++c->launches;
@@ -426,6 +660,13 @@ int hk_mul_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
     Residues r;
     for (int l = 0; l <= la; ++l) r.v[l] = res[l];
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
+    if (c->log_n == ntt16::kLogN) {
+        uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
+        if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_const workspace");
+        RsSrc<SRC_MULCONST> src = make_src<SRC_MULCONST>(c, a, la, B);
+        src.k = r;
+        return rescale_fused(c, src, la, B, out, ws);
+    }
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_const workspace");
     k_mul_const<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, r, ws, BN, c->d_modq); ++c->launches;
@@ -438,6 +679,17 @@ int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const
     if (la < 0 || la >= c->n_q || lp < la || n < 1) return hk_fail(c, HK_E_ARG, "mac_plain: args");
     if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
+    if (c->log_n == ntt16::kLogN && n <= kMacMax) {
+        uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
+        if (!ws) return hk_fail(c, HK_E_NOMEM, "mac_plain workspace");
+        RsSrc<SRC_MAC> src = make_src<SRC_MAC>(c, babies[0], la, B);
+        src.n = n;
+        for (int i = 0; i < n; ++i) {
+            src.babies.p[i] = babies[i];
+            src.pts.p[i] = pts[i];
+        }
+        return rescale_fused(c, src, la, B, out, ws);
+    }
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mac_plain workspace");
     for (int s = 0; s < n; s += kMacMax) {
@@ -470,6 +722,11 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     const uint32_t g1[1] = {1u};
     int rc = keyswitch(c, d + 2 * pl, l, B, 1, keys, g1, &o0, &o1, nullptr, scr);
     if (rc) return rc;
+    if (c->log_n == ntt16::kLogN) {  // rescale(d + ks) with the sum formed on the fly
+        RsSrc<SRC_SUM2> src = make_src<SRC_SUM2>(c, d, l, B);
+        src.a2 = ks;
+        return rescale_fused(c, src, l, B, out, scr);
+    }
     // d0 += ks0, d1 += ks1 (d0, d1 contiguous = a level-l ciphertext)
     k_addsub<<<egrid(BN, l + 1, 2), 256, 0, c->stream>>>(d, l, ks, l, d, l, BN, 0, c->d_modq); ++c->launches;
     HK_LAUNCH_CHECK(c, "relin add");
