@@ -860,6 +860,69 @@ static void moddown(const hk_ctx *c, const uint64_t *acc, int l, int B, uint64_t
     free(sp);
 }
 
+/* ModDown merged with the rescale that follows a relinearisation: with
+ * Y = acc + P*d over Q_l*P, divide by M = P*q_l in one fast basis conversion
+ * from the sources {p_0..p_{K-1}, q_l}:
+ *   out_t = (Y_t - conv_t(Y mod M)) * M^-1 mod q_t,   t < l.               */
+static void moddown_rescale(const hk_ctx *c, const uint64_t *acc, const uint64_t *dp, int l, int B, uint64_t *out) {
+    const int N = c->n, np = c->n_p, ns = np + 1;
+    uint64_t smod_[64];
+    for (int k = 0; k < np; ++k) smod_[k] = c->mod[c->n_q + k];
+    smod_[np] = c->mod[l];
+    uint64_t Pm_l = 1;
+    for (int k = 0; k < np; ++k) Pm_l = mulmod(Pm_l, smod_[k] % c->mod[l], c->mod[l]);
+    /* sources in coefficient form: specials, then y = acc_l + P d_l */
+    uint64_t *src = malloc(sizeof(uint64_t) * (size_t)ns * B * N);
+    memcpy(src, acc + (size_t)(l + 1) * B * N, sizeof(uint64_t) * (size_t)np * B * N);
+    for (size_t k = 0; k < (size_t)B * N; ++k) {
+        const size_t o = (size_t)l * B * N + k;
+        src[(size_t)np * B * N + k] = addmod(acc[o], mulmod(Pm_l, dp[o], c->mod[l]), c->mod[l]);
+    }
+    for (int s = 0; s < ns; ++s)
+        for (int b = 0; b < B; ++b) ntt_inv_1(c, src + ((size_t)s * B + b) * N, s < np ? c->n_q + s : l);
+    uint64_t inv[64];
+    for (int s = 0; s < ns; ++s) {
+        uint64_t prod = 1;
+        for (int r = 0; r < ns; ++r)
+            if (r != s) prod = mulmod(prod, smod_[r] % smod_[s], smod_[s]);
+        inv[s] = invmod(prod, smod_[s]);
+    }
+    #pragma omp parallel for schedule(dynamic)
+    for (int t = 0; t < l; ++t) {
+        const uint64_t q = c->mod[t];
+        uint64_t hat[64], M = 1, P = 1;
+        for (int s = 0; s < ns; ++s) {
+            uint64_t prod = 1;
+            for (int r = 0; r < ns; ++r)
+                if (r != s) prod = mulmod(prod, smod_[r] % q, q);
+            hat[s] = prod;
+            M = mulmod(M, smod_[s] % q, q);
+        }
+        for (int k = 0; k < np; ++k) P = mulmod(P, smod_[k] % q, q);
+        const uint64_t Minv = invmod(M, q);
+        uint64_t *conv = malloc(sizeof(uint64_t) * N);
+        for (int b = 0; b < B; ++b) {
+            for (int n = 0; n < N; ++n) {
+                uint64_t acc2 = 0;
+                for (int s = 0; s < ns; ++s) {
+                    const uint64_t v = mulmod(src[((size_t)s * B + b) * N + n], inv[s], smod_[s]);
+                    acc2 = addmod(acc2, mulmod(v % q, hat[s], q), q);
+                }
+                conv[n] = acc2;
+            }
+            ntt_fwd_1(c, conv, t);
+            const size_t o = ((size_t)t * B + b) * N;
+            uint64_t *z = out + ((size_t)t * B + b) * N;
+            for (int n = 0; n < N; ++n) {
+                const uint64_t y = addmod(acc[o + n], mulmod(P, dp[o + n], q), q);
+                z[n] = mulmod(submod(y, conv[n], q), Minv, q);
+            }
+        }
+        free(conv);
+    }
+    free(src);
+}
+
 int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {
     if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return fail(c, HK_E_ARG, "mul: level");
@@ -883,20 +946,11 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     uint64_t *acc = malloc(sizeof(uint64_t) * 2 * (size_t)ne * B * N);
     modup(c, d + 2 * pl, l, B, ext);
     key_ip(c, ext, l, B, c->relin, 1u, acc);
-    uint64_t *ks = malloc(sizeof(uint64_t) * 2 * pl);
-    moddown(c, acc, l, B, ks);
-    moddown(c, acc + (size_t)ne * B * N, l, B, ks + pl);
-    for (int i = 0; i <= l; ++i) {
-        const uint64_t q = c->mod[i];
-        for (size_t k = 0; k < (size_t)B * N; ++k) {
-            const size_t o = (size_t)i * B * N + k;
-            d[o] = addmod(d[o], ks[o], q);
-            d[pl + o] = addmod(d[pl + o], ks[pl + o], q);
-        }
-    }
-    int rc = hk_rescale(c, d, l, out, B);
-    free(d); free(ext); free(acc); free(ks);
-    return rc;
+    const size_t po = (size_t)l * B * N;
+    moddown_rescale(c, acc, d, l, B, out);
+    moddown_rescale(c, acc + (size_t)ne * B * N, d + pl, l, B, out + po);
+    free(d); free(ext); free(acc);
+    return HK_OK;
 }
 
 int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *gs, int32_t n,

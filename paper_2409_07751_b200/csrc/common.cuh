@@ -173,6 +173,11 @@ struct hk_ctx {
     std::vector<std::vector<ConvTable>> modup;  // [level][digit]
     ConvTable moddown;                          // sources: specials, targets: q_0..q_{n_q-1}
     ulonglong2 *d_pinv;                         // [n_q] P^-1 mod q_i
+    // ModDown merged with rescale (hk_mul): per level l >= 1, sources
+    // {p_0..p_{K-1}, q_l} -> targets q_0..q_{l-1}
+    std::vector<ConvTable> mdrs;                // [n_q] (entry 0 unused)
+    ulonglong2 *d_pmod;                         // [n_q] P mod q_i (Shoup pairs)
+    ulonglong2 *d_mqinv;                        // [n_q][n_q] (P q_l)^-1 mod q_t
     // keys
     uint64_t *d_sk;                 // [n_mod][N]
     uint64_t *d_relin;              // [n_digits][2][n_mod][N]

@@ -253,6 +253,29 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
             pinv[i] = make_ulonglong2(v, h_shoup(v, q));
         }
         c->d_pinv = upload(pinv);
+        // merged ModDown + rescale tables
+        c->mdrs.resize(c->n_q);
+        std::vector<ulonglong2> pmod(c->n_q), mqinv((size_t)c->n_q * c->n_q, make_ulonglong2(0, 0));
+        for (int i = 0; i < c->n_q; ++i) {
+            const uint64_t q = c->mod_h[i];
+            uint64_t P = 1;
+            for (int k = 0; k < c->n_p; ++k) P = h_mulmod(P, c->mod_h[c->n_q + k] % q, q);
+            pmod[i] = make_ulonglong2(P, h_shoup(P, q));
+        }
+        for (int l = 1; l < c->n_q; ++l) {
+            std::vector<int> s2, d2;
+            for (int k = 0; k < c->n_p; ++k) s2.push_back(c->n_q + k);
+            s2.push_back(l);
+            for (int t = 0; t < l; ++t) d2.push_back(t);
+            c->mdrs[l] = make_conv(c->mod_h, s2, d2);
+            for (int t = 0; t < l; ++t) {
+                const uint64_t q = c->mod_h[t];
+                const uint64_t v = h_inv(h_mulmod(pmod[t].x, c->mod_h[l] % q, q), q);
+                mqinv[(size_t)l * c->n_q + t] = make_ulonglong2(v, h_shoup(v, q));
+            }
+        }
+        c->d_pmod = upload(pmod);
+        c->d_mqinv = upload(mqinv);
     }
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -282,6 +305,9 @@ void hk_ctx_destroy(hk_ctx *c) {
     for (auto &lv : c->modup)
         for (auto &t : lv) free_conv(t);
     free_conv(c->moddown);
+    for (size_t l = 1; l < c->mdrs.size(); ++l) free_conv(c->mdrs[l]);
+    cudaFree(c->d_pmod);
+    cudaFree(c->d_mqinv);
     cudaFree(c->d_sk);
     cudaFree(c->d_relin);
     for (auto &kv : c->gal) cudaFree(kv.second);

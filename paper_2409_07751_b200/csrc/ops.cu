@@ -387,6 +387,57 @@ struct EpiModDown {
     }
 };
 
+// merged ModDown + rescale helpers
+__global__ void k_mdrs_y(const uint64_t *__restrict__ acc_l, const uint64_t *__restrict__ d_l, uint64_t *__restrict__ y,
+                         const ulonglong2 *__restrict__ pmod_l, const ModQ *__restrict__ mq_l, long long BN) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= BN) return;
+    const uint64_t q = mq_l->q;
+    const ulonglong2 P = *pmod_l;
+    y[e] = add_mod(acc_l[e], mul_shoup(d_l[e], P.x, P.y, q), q);
+}
+__global__ void k_mdrs_finish(const uint64_t *__restrict__ acc, const uint64_t *__restrict__ d,
+                              const uint64_t *__restrict__ conv, uint64_t *__restrict__ out,
+                              const ulonglong2 *__restrict__ pmod, const ulonglong2 *__restrict__ mqinv,
+                              const ModQ *__restrict__ mq, long long BN) {
+    ELEM_INDEX
+    (void)p;
+    const long long o = (long long)l * BN + e;
+    const uint64_t q = mq[l].q;
+    const ulonglong2 P = pmod[l], w = mqinv[l];
+    const uint64_t y = add_mod(acc[o], mul_shoup(d[o], P.x, P.y, q), q);
+    out[o] = mul_shoup(sub_mod(y, conv[o], q), w.x, w.y, q);
+}
+// iNTT prologue: y = acc_l + P d_l (prime l)
+struct ProMdY {
+    const uint64_t *acc_l, *d_l;
+    const ulonglong2 *pmod;
+    const ModQ *mq;
+    int l;
+    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
+        const long long o = P * ntt16::kN + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 Pm = pmod[l];
+        return add_mod(acc_l[o], mul_shoup(d_l[o], Pm.x, Pm.y, q), q);
+    }
+};
+// NTT epilogue: out_t = (acc_t + P d_t - v) * (P q_l)^-1
+struct EpiMdRs {
+    const uint64_t *acc, *d;
+    uint64_t *out;
+    const ulonglong2 *pmod, *mqinv;
+    const ModQ *mq;
+    int B, log_n;
+    long long BN;
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 Pm = pmod[l], w = mqinv[l];
+        const uint64_t y = add_mod(acc[o], mul_shoup(d[o], Pm.x, Pm.y, q), q);
+        out[o] = mul_shoup(sub_mod(y, v, q), w.x, w.y, q);
+    }
+};
+
 }  // namespace
 
 static dim3 egrid(long long BN, int limbs, int polys) {
@@ -420,11 +471,6 @@ static int conv_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint6
 }
 
 // words of scratch the key switch at level l needs
-static size_t ks_scratch_words(const hk_ctx *c, int l, int B) {
-    const size_t BN = (size_t)B * c->n;
-    const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
-    return BN * ((size_t)(l + 1) + (size_t)nd * ne + 2 * (size_t)ne + c->n_p + (l + 1));
-}
 
 static size_t rs_scratch_words(const hk_ctx *c, int l, int B) {
     return (size_t)B * c->n * (2 + 2 * (size_t)l);
@@ -446,63 +492,6 @@ int rescale_launch(hk_ctx *c, const uint64_t *in, int l, int B, uint64_t *out, u
                                                         c->d_modq);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "rescale");
-    return HK_OK;
-}
-
-// Key switch d (NTT, [l+1][B][N]) under n keys; for key r writes
-//   out0[r] = ks0 (+ sigma_g(add0) if add0) and out1[r] = ks1, each [l+1][B][N].
-static int keyswitch_fused(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
-                           const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
-                           uint64_t *scratch);
-
-static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
-                     const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
-                     uint64_t *scratch) {
-    if (c->log_n == ntt16::kLogN) return keyswitch_fused(c, d, l, B, n, keys, gal, out0, out1, add0, scratch);
-    const int N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
-    const long long BN = (long long)B * N;
-    uint64_t *dc = scratch;
-    uint64_t *ext = dc + (size_t)(l + 1) * BN;
-    uint64_t *acc = ext + (size_t)nd * ne * BN;
-    uint64_t *sp = acc + (size_t)2 * ne * BN;
-    uint64_t *conv = sp + (size_t)np * BN;
-    // ModUp
-    HK_CUDA(c, cudaMemcpyAsync(dc, d, sizeof(uint64_t) * (l + 1) * BN, cudaMemcpyDeviceToDevice, c->stream));
-    int rc = ntt_inv_launch(c, dc, 0, l + 1, B, 0);
-    if (rc) return rc;
-    for (int j = 0; j < nd; ++j) {
-        const ConvTable &T = c->modup[l][j];
-        const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, l + 1);
-        uint64_t *ej = ext + (size_t)j * ne * BN;
-        if ((rc = conv_launch(c, T, dc + (size_t)d0 * BN, ej, 0, l, BN))) return rc;
-        HK_LAUNCH_CHECK(c, "modup conv");
-        if (d0 > 0 && (rc = ntt_fwd_launch(c, ej, 0, d0, B, 0))) return rc;
-        if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
-        if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
-    }
-    // per key: inner product, ModDown of both halves
-    for (int r = 0; r < n; ++r) {
-        k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(ext, d, c->alpha, nd, ne, l, c->n_q, c->n_mod, c->log_n,
-                                                          keys[r], gal[r], acc, acc + (size_t)ne * BN, c->d_modq, BN);
-        ++c->launches;
-        HK_LAUNCH_CHECK(c, "key inner product");
-        for (int p = 0; p < 2; ++p) {
-            const uint64_t *a = acc + (size_t)p * ne * BN;
-            HK_CUDA(c, cudaMemcpyAsync(sp, a + (size_t)(l + 1) * BN, sizeof(uint64_t) * np * BN,
-                                       cudaMemcpyDeviceToDevice, c->stream));
-            if ((rc = ntt_inv_launch(c, sp, c->n_q, np, B, 0))) return rc;
-            const ConvTable &T = c->moddown;
-            if ((rc = conv_launch(c, T, sp, conv, 1, l, BN, l + 1))) return rc;
-            HK_LAUNCH_CHECK(c, "moddown conv");
-            if ((rc = ntt_fwd_launch(c, conv, 0, l + 1, B, 0))) return rc;
-            const long long t2 = (long long)(l + 1) * BN;
-            k_md_finish<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, conv, p == 0 ? out0[r] : out1[r],
-                                                                   p == 0 ? add0 : nullptr, gal[r], c->log_n, BN,
-                                                                   c->d_pinv, c->d_modq);
-            ++c->launches;
-            HK_LAUNCH_CHECK(c, "moddown finish");
-        }
-    }
     return HK_OK;
 }
 
@@ -532,54 +521,150 @@ static RsSrc<KIND> make_src(hk_ctx *c, const uint64_t *a, int la, int B) {
     return s;
 }
 
-static int keyswitch_fused(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
-                           const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
-                           uint64_t *scratch) {
-    const int N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
-    const long long BN = (long long)B * N;
-    uint64_t *dc = scratch;
-    uint64_t *ext = dc + (size_t)(l + 1) * BN;
-    uint64_t *acc = ext + (size_t)nd * ne * BN;
-    uint64_t *sp = acc + (size_t)2 * ne * BN;
-    uint64_t *conv = sp + (size_t)np * BN;
-    // ModUp: coefficient form of d, scaled by each digit's (Q_D / q_i)^-1
-    EpiScaleDigits esd;
-    memset(&esd, 0, sizeof esd);
-    esd.out = dc;
-    esd.alpha = c->alpha;
-    esd.mq = c->d_modq;
-    if (nd > 8) return hk_fail(c, HK_E_ARG, "more than 8 key-switching digits");
-    for (int j = 0; j < nd; ++j) {
-        esd.inv[j] = c->modup[l][j].d_inv;
-        esd.inv_sh[j] = c->modup[l][j].d_inv_sh;
+// ---------------------------------------------------------------------------
+// hybrid key switching, staged: ModUp -> key inner product -> ModDown
+// (or ModDown merged with the following rescale for relinearisation)
+// scratch layout: dc [l+1] | ext [nd][ne] | acc [2][ne] | sp [K+1] | conv [l+1]   (units of B*N words)
+// ---------------------------------------------------------------------------
+struct KsBufs {
+    uint64_t *dc, *ext, *acc, *sp, *conv;
+};
+
+static size_t ks_words(const hk_ctx *c, int l, int B) {
+    const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    return (size_t)B * c->n * ((size_t)(l + 1) + (size_t)nd * ne + 2 * (size_t)ne + (c->n_p + 1) + (l + 1));
+}
+
+static KsBufs ks_bufs(const hk_ctx *c, int l, int B, uint64_t *scratch) {
+    const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    const size_t BN = (size_t)B * c->n;
+    KsBufs k;
+    k.dc = scratch;
+    k.ext = k.dc + (size_t)(l + 1) * BN;
+    k.acc = k.ext + (size_t)nd * ne * BN;
+    k.sp = k.acc + 2 * (size_t)ne * BN;
+    k.conv = k.sp + (size_t)(c->n_p + 1) * BN;
+    return k;
+}
+
+// ModUp of d (NTT, [l+1][B][N]) into ext [nd][ne][B][N] (own-digit limbs are
+// not copied: the key inner product reads them from d)
+static int ks_modup(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb) {
+    const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
+    const long long BN = (long long)B * c->n;
+    const bool fused = c->log_n == ntt16::kLogN;
+    int rc;
+    if (fused) {
+        EpiScaleDigits esd;
+        memset(&esd, 0, sizeof esd);
+        esd.out = kb.dc;
+        esd.alpha = c->alpha;
+        esd.mq = c->d_modq;
+        if (nd > 8) return hk_fail(c, HK_E_ARG, "more than 8 key-switching digits");
+        for (int j = 0; j < nd; ++j) {
+            esd.inv[j] = c->modup[l][j].d_inv;
+            esd.inv_sh[j] = c->modup[l][j].d_inv_sh;
+        }
+        if ((rc = ntt16::launch_inv(c, kb.dc, 0, l + 1, B, ntt16::ProPlain{d}, esd))) return rc;
+    } else {
+        HK_CUDA(c, cudaMemcpyAsync(kb.dc, d, sizeof(uint64_t) * (l + 1) * BN, cudaMemcpyDeviceToDevice, c->stream));
+        if ((rc = ntt_inv_launch(c, kb.dc, 0, l + 1, B, 0))) return rc;
     }
-    int rc = ntt16::launch_inv(c, dc, 0, l + 1, B, ntt16::ProPlain{d}, esd);
-    if (rc) return rc;
     for (int j = 0; j < nd; ++j) {
         const ConvTable &T = c->modup[l][j];
         const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, l + 1);
-        uint64_t *ej = ext + (size_t)j * ne * BN;
-        if ((rc = conv_launch(c, T, dc + (size_t)d0 * BN, ej, 0, l, BN, -1, 1))) return rc;
+        uint64_t *ej = kb.ext + (size_t)j * ne * BN;
+        if ((rc = conv_launch(c, T, kb.dc + (size_t)d0 * BN, ej, 0, l, BN, -1, fused ? 1 : 0))) return rc;
         if (d0 > 0 && (rc = ntt_fwd_launch(c, ej, 0, d0, B, 0))) return rc;
         if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
         if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
     }
+    return HK_OK;
+}
+
+static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, const uint64_t *key, uint32_t g) {
+    const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    const long long BN = (long long)B * c->n;
+    k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(kb.ext, d, c->alpha, nd, ne, l, c->n_q, c->n_mod, c->log_n, key, g,
+                                                      kb.acc, kb.acc + (size_t)ne * BN, c->d_modq, BN);
+    ++c->launches;
+    HK_LAUNCH_CHECK(c, "key inner product");
+    return HK_OK;
+}
+
+// ModDown of one half acc_p ([ne][B][N]) into out ([l+1][B][N]); adds sigma_g(add0) if given
+static int ks_moddown(hk_ctx *c, const uint64_t *a, int l, int B, const KsBufs &kb, uint64_t *out,
+                      const uint64_t *add0, uint32_t g) {
+    const int np = c->n_p;
+    const long long BN = (long long)B * c->n;
+    const ConvTable &T = c->moddown;
+    int rc;
+    if (c->log_n == ntt16::kLogN) {
+        EpiScale es{kb.sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q};
+        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{a + (size_t)(l + 1) * BN}, es))) return rc;
+        if ((rc = conv_launch(c, T, kb.sp, kb.conv, 1, l, BN, l + 1, 1))) return rc;
+        EpiModDown epi{a, add0, out, c->d_pinv, c->d_modq, g, B, c->log_n, BN};
+        return ntt16::launch_fwd(c, kb.conv, 0, l + 1, B, ntt16::ProPlain{kb.conv}, epi);
+    }
+    HK_CUDA(c, cudaMemcpyAsync(kb.sp, a + (size_t)(l + 1) * BN, sizeof(uint64_t) * np * BN, cudaMemcpyDeviceToDevice,
+                               c->stream));
+    if ((rc = ntt_inv_launch(c, kb.sp, c->n_q, np, B, 0))) return rc;
+    if ((rc = conv_launch(c, T, kb.sp, kb.conv, 1, l, BN, l + 1))) return rc;
+    if ((rc = ntt_fwd_launch(c, kb.conv, 0, l + 1, B, 0))) return rc;
+    k_md_finish<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, kb.conv, out, add0, g, c->log_n, BN, c->d_pinv,
+                                                           c->d_modq);
+    ++c->launches;
+    HK_LAUNCH_CHECK(c, "moddown finish");
+    return HK_OK;
+}
+
+// ModDown merged with rescale: out ([l][B][N]) = (acc_p + P d_p) / (P q_l)
+static int ks_moddown_rescale(hk_ctx *c, const uint64_t *a, const uint64_t *dp, int l, int B, const KsBufs &kb,
+                              uint64_t *out) {
+    const int np = c->n_p;
+    const long long BN = (long long)B * c->n;
+    const ConvTable &T = c->mdrs[l];
+    const ulonglong2 *mqinv = c->d_mqinv + (size_t)l * c->n_q;
+    int rc;
+    if (c->log_n == ntt16::kLogN) {
+        EpiScale es{kb.sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q};
+        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{a + (size_t)(l + 1) * BN}, es))) return rc;
+        ProMdY py{a + (size_t)l * BN, dp + (size_t)l * BN, c->d_pmod, c->d_modq, l};
+        EpiScale es2{kb.sp + (size_t)np * BN, T.d_inv + np, T.d_inv_sh + np, c->d_modq, l};
+        if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * BN, l, 1, B, py, es2))) return rc;
+        if ((rc = conv_launch(c, T, kb.sp, kb.conv, 1, l, BN, l, 1))) return rc;
+        EpiMdRs epi{a, dp, out, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN};
+        return ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv}, epi);
+    }
+    HK_CUDA(c, cudaMemcpyAsync(kb.sp, a + (size_t)(l + 1) * BN, sizeof(uint64_t) * np * BN, cudaMemcpyDeviceToDevice,
+                               c->stream));
+    k_mdrs_y<<<egrid(BN, 1, 1), 256, 0, c->stream>>>(a + (size_t)l * BN, dp + (size_t)l * BN, kb.sp + (size_t)np * BN,
+                                                     c->d_pmod + l, c->d_modq + l, BN);
+    ++c->launches;
+    if ((rc = ntt_inv_launch(c, kb.sp, c->n_q, np, B, 0))) return rc;
+    if ((rc = ntt_inv_launch(c, kb.sp + (size_t)np * BN, l, 1, B, 0))) return rc;
+    if ((rc = conv_launch(c, T, kb.sp, kb.conv, 1, l, BN, l))) return rc;
+    if ((rc = ntt_fwd_launch(c, kb.conv, 0, l, B, 0))) return rc;
+    k_mdrs_finish<<<egrid(BN, l, 1), 256, 0, c->stream>>>(a, dp, kb.conv, out, c->d_pmod, mqinv, c->d_modq, BN);
+    ++c->launches;
+    HK_LAUNCH_CHECK(c, "moddown-rescale finish");
+    return HK_OK;
+}
+
+// Key switch d under n keys (hoisted ModUp); for key r writes
+//   out0[r] = ks0 (+ sigma_g(add0) if add0) and out1[r] = ks1, each [l+1][B][N].
+static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
+                     const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
+                     uint64_t *scratch) {
+    const KsBufs kb = ks_bufs(c, l, B, scratch);
+    const int ne = l + 1 + c->n_p;
+    const long long BN = (long long)B * c->n;
+    int rc = ks_modup(c, d, l, B, kb);
+    if (rc) return rc;
     for (int r = 0; r < n; ++r) {
-        k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(ext, d, c->alpha, nd, ne, l, c->n_q, c->n_mod, c->log_n,
-                                                          keys[r], gal[r], acc, acc + (size_t)ne * BN, c->d_modq, BN);
-        ++c->launches;
-        HK_LAUNCH_CHECK(c, "key inner product");
-        for (int p = 0; p < 2; ++p) {
-            const uint64_t *a = acc + (size_t)p * ne * BN;
-            const ConvTable &T = c->moddown;
-            EpiScale es{sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q};
-            if ((rc = ntt16::launch_inv(c, sp, c->n_q, np, B, ntt16::ProPlain{a + (size_t)(l + 1) * BN}, es)))
-                return rc;
-            if ((rc = conv_launch(c, T, sp, conv, 1, l, BN, l + 1, 1))) return rc;
-            EpiModDown epi{a, p == 0 ? add0 : nullptr, p == 0 ? out0[r] : out1[r], c->d_pinv, c->d_modq, gal[r], B,
-                           c->log_n, BN};
-            if ((rc = ntt16::launch_fwd(c, conv, 0, l + 1, B, ntt16::ProPlain{conv}, epi))) return rc;
-        }
+        if ((rc = ks_ip(c, d, l, B, kb, keys[r], gal[r]))) return rc;
+        if ((rc = ks_moddown(c, kb.acc, l, B, kb, out0[r], add0, gal[r]))) return rc;
+        if ((rc = ks_moddown(c, kb.acc + (size_t)ne * BN, l, B, kb, out1[r], nullptr, gal[r]))) return rc;
     }
     return HK_OK;
 }
@@ -711,26 +796,19 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     const int l = std::min(la, lb);
     if (l < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", l);
     const long long BN = (long long)B * c->n, pl = (long long)(l + 1) * BN;
-    const size_t extra = std::max(ks_scratch_words(c, l, B), rs_scratch_words(c, l, B));
-    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (5 * pl + extra));
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (3 * pl + ks_words(c, l, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
-    uint64_t *d = ws, *ks = ws + 3 * pl, *scr = ws + 5 * pl;
-    k_tensor<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq); ++c->launches;
+    uint64_t *d = ws;
+    const KsBufs kb = ks_bufs(c, l, B, ws + 3 * pl);
+    k_tensor<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq);
+    ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");
-    uint64_t *o0 = ks, *o1 = ks + pl;
-    const uint64_t *keys[1] = {c->d_relin};
-    const uint32_t g1[1] = {1u};
-    int rc = keyswitch(c, d + 2 * pl, l, B, 1, keys, g1, &o0, &o1, nullptr, scr);
-    if (rc) return rc;
-    if (c->log_n == ntt16::kLogN) {  // rescale(d + ks) with the sum formed on the fly
-        RsSrc<SRC_SUM2> src = make_src<SRC_SUM2>(c, d, l, B);
-        src.a2 = ks;
-        return rescale_fused(c, src, l, B, out, scr);
-    }
-    // d0 += ks0, d1 += ks1 (d0, d1 contiguous = a level-l ciphertext)
-    k_addsub<<<egrid(BN, l + 1, 2), 256, 0, c->stream>>>(d, l, ks, l, d, l, BN, 0, c->d_modq); ++c->launches;
-    HK_LAUNCH_CHECK(c, "relin add");
-    return rescale_launch(c, d, l, B, out, scr);
+    int rc = ks_modup(c, d + 2 * pl, l, B, kb);
+    if (!rc) rc = ks_ip(c, d + 2 * pl, l, B, kb, c->d_relin, 1u);
+    const int ne = l + 1 + c->n_p;
+    if (!rc) rc = ks_moddown_rescale(c, kb.acc, d, l, B, kb, out);
+    if (!rc) rc = ks_moddown_rescale(c, kb.acc + (size_t)ne * BN, d + pl, l, B, kb, out + (size_t)l * BN);
+    return rc;
 }
 
 int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *gs, int32_t n,
@@ -748,7 +826,7 @@ int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *
         o0[i] = outs[i];
         o1[i] = outs[i] + pl;
     }
-    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * ks_scratch_words(c, la, B));
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * ks_words(c, la, B));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "rotate workspace");
     return keyswitch(c, a + pl, la, B, n, keys.data(), gs, o0.data(), o1.data(), a, ws);
 }
