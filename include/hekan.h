@@ -17,7 +17,7 @@
  *
  * Conventions
  *   N = 2^log_n coefficients, S = N/2 complex slots (real payloads only).
- *   Every prime lies in (2^40, 2^50) and is 1 mod 2N (hk_ctx_create rejects others):
+ *   Every prime lies in (2^44, 2^50) and is 1 mod 2N (hk_ctx_create rejects others):
  *   the GPU keeps 25-bit limb splits and lazy NTT residues inside 64-bit words.
  *   A ciphertext at reference level l has l+1 RNS limbs (primes q_0..q_l) and
  *   layout u64 [2][l+1][B][N]  (poly, limb, batch, coefficient), NTT domain,

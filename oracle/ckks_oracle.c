@@ -166,7 +166,7 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     for (int i = 0; i < pr->n_p; ++i) { c->mod[pr->n_q + i] = pr->p[i]; psi[pr->n_q + i] = pr->psi_p[i]; }
     for (int i = 0; i < nm; ++i) {
         uint64_t q = c->mod[i];
-        if (q >= (1ull << 50) || q <= (1ull << 40) || (q - 1) % (2ull * N) != 0 || powmod(psi[i], N, q) != q - 1) {
+        if (q >= (1ull << 50) || q <= (1ull << 44) || (q - 1) % (2ull * N) != 0 || powmod(psi[i], N, q) != q - 1) {
             free(psi);
             hk_ctx_destroy(c);
             return HK_E_ARG;

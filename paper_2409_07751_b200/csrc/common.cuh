@@ -101,16 +101,27 @@ __device__ __forceinline__ void acc3_mac(Acc3 &a, uint64_t x, uint64_t y) {
     split25(y, y0, y1);
     acc3_mac(a, x0, x1, y0, y1);
 }
+// X = s2 2^50 + s1 2^25 + s0 < 64 * 2^100 = 2^106 < 2^(63+k) for every prime
+// (q > 2^44, so k >= 45): one Barrett step suffices.
 __device__ __forceinline__ uint64_t acc3_reduce(const Acc3 &a, const ModQ &m) {
-    const uint64_t s2 = reduce128(0, a.s2, m);  // < q
     uint64_t lo = a.s0, hi = 0;
     uint64_t t = a.s1 << 25;
     lo += t;
     hi += (lo < t) + (a.s1 >> 39);
-    t = s2 << 50;
+    t = a.s2 << 50;
     lo += t;
-    hi += (lo < t) + (s2 >> 14);
-    return reduce128(hi, lo, m);  // value < 2^101 < 2^(63+k)
+    hi += (lo < t) + (a.s2 >> 14);
+    return reduce128(hi, lo, m);
+}
+// Shoup multiply with a 3 x IMAD.WIDE quotient estimate (undershoot <= 2),
+// canonical result. w < q < 2^50, wp = floor(w 2^64 / q), any y < 2^64.
+__device__ __forceinline__ uint64_t mul_shoup_fast(uint64_t y, uint64_t w, uint64_t wp, uint64_t q) {
+    const uint32_t y0 = (uint32_t)y, y1 = (uint32_t)(y >> 32);
+    const uint32_t w0 = (uint32_t)wp, w1 = (uint32_t)(wp >> 32);
+    const uint64_t Q = ((uint64_t)y1 * w1) + (((uint64_t)y1 * w0) >> 32) + (((uint64_t)y0 * w1) >> 32);
+    uint64_t r = y * w - Q * q;  // [0, 4q)
+    r = r >= 2 * q ? r - 2 * q : r;
+    return r >= q ? r - q : r;
 }
 
 __device__ __forceinline__ uint32_t brev_bits(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }

@@ -263,15 +263,22 @@ struct RsSrc {
     int la, pb, n, log_n;
     long long BN;
     const ModQ *mq;
-    Residues k;
+    const double2 *fmod;  // {q, 1/q} per prime
+    Residues k, ksh;    // constant residues and Shoup companions (SRC_MULCONST)
     PtrList babies, pts;
     __device__ __forceinline__ uint64_t operator()(int p, int l, int b, int idx) const {
         const long long o = ((long long)p * (la + 1) + l) * BN + ((long long)b << log_n) + idx;
         if (KIND == SRC_PLAIN) return a[o];
         if (KIND == SRC_SUM2) return add_mod(a[o], a2[o], mq[l].q);
-        if (KIND == SRC_MULCONST) return mul_mod(a[o], k.v[l], mq[l]);
-        if (KIND == SRC_MULPT)
-            return mul_mod(a[o], pt[(((long long)l * pb + (pb == 1 ? 0 : b)) << log_n) + idx], mq[l]);
+        if (KIND == SRC_MULCONST) return mul_shoup_fast(a[o], k.v[l], ksh.v[l], mq[l].q);
+        if (KIND == SRC_MULPT) {
+            // FP64 two-product Shoup step (pt/q formed in-register)
+            const uint64_t y = pt[(((long long)l * pb + (pb == 1 ? 0 : b)) << log_n) + idx];
+            const double2 f = fmod[l];
+            const ntt16::FpMod fm{f.x, f.y};
+            const double yd = ntt16::u2d(y);
+            return ntt16::d2canon(ntt16::f_mulmod(ntt16::u2d(a[o]), yd, __dmul_rn(yd, fm.qinv), fm.q), fm);
+        }
         Acc3 acc;
         acc3_zero(acc);
         const long long pe = ((long long)l << log_n) + idx;
@@ -518,6 +525,7 @@ static RsSrc<KIND> make_src(hk_ctx *c, const uint64_t *a, int la, int B) {
     s.log_n = c->log_n;
     s.BN = (long long)B * c->n;
     s.mq = c->d_modq;
+    s.fmod = c->d_fmod;
     return s;
 }
 
@@ -750,6 +758,7 @@ int hk_mul_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
         if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_const workspace");
         RsSrc<SRC_MULCONST> src = make_src<SRC_MULCONST>(c, a, la, B);
         src.k = r;
+        for (int l = 0; l <= la; ++l) src.ksh.v[l] = (uint64_t)(((u128)r.v[l] << 64) / c->mod_h[l]);
         return rescale_fused(c, src, la, B, out, ws);
     }
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (tot + rs_scratch_words(c, la, B)));

@@ -12,7 +12,7 @@ This module supplies the chain that the reference's level maps onto:
 * ``q_0`` is ~50 bits and the rescaling primes sit next to the scale
   (~2^46), after the paper's 51/46/51 chain (`PAPER.md:321`); the special
   primes sit just below 2^47 (alpha of them: P / Q_digit >= 2^13). Every prime
-  is in (2^40, 2^50) (25-bit split MACs) and all but q_0 are below 2^47, which
+  is in (2^44, 2^50) (25-bit split MACs) and all but q_0 are below 2^47, which
   keeps the GPU's float64 NTT free of intra-phase reductions.
 
 Canonical scales. Ciphertexts at level ``l`` always carry scale

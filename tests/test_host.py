@@ -22,7 +22,7 @@ def test_kan_params_chain():
     allp = list(p.q) + list(p.p)
     assert len(set(allp)) == len(allp)
     for q in allp:
-        assert is_prime(q) and (q - 1) % two_n == 0 and 2 ** 40 < q < 2 ** 50
+        assert is_prime(q) and (q - 1) % two_n == 0 and 2 ** 44 < q < 2 ** 50
     for s in p.scales:
         assert abs(s / 2 ** 46 - 1) < 1e-6
     for lvl in range(1, p.depth + 1):  # ct x ct lands on the canonical scale
