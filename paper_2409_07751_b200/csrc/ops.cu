@@ -157,10 +157,11 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
                                               const int32_t *__restrict__ dst_mod, int n_dst,
                                               uint64_t *__restrict__ dst, int mode, int l, int n_q, long long BN,
                                               const ModQ *__restrict__ mq, int prescaled) {
-    extern __shared__ uint64_t sh[];  // hat [n_dst][n_src] as (h0 | h1 << 32), ModQ [n_dst], out index [n_dst]
-    ModQ *smq = (ModQ *)(sh + n_dst * n_src);
+    // NS == n_src exactly (one instantiation per source count): no guards
+    extern __shared__ uint64_t sh[];  // hat [n_dst][NS] as (h0 | h1 << 32), ModQ [n_dst], out index [n_dst]
+    ModQ *smq = (ModQ *)(sh + n_dst * NS);
     int *sidx = (int *)(smq + n_dst);
-    for (int i = threadIdx.x; i < n_dst * n_src; i += blockDim.x) {
+    for (int i = threadIdx.x; i < n_dst * NS; i += blockDim.x) {
         const uint64_t h = hat[i];
         sh[i] = ((uint64_t)(uint32_t)(h >> 25) << 32) | ((uint32_t)h & HK_M25);
     }
@@ -175,22 +176,35 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
     uint32_t v0[NS], v1[NS];
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
-        if (i < n_src) {
-            const uint64_t x = src[(long long)i * BN + e];
-            split25(prescaled ? x : mul_shoup(x, inv[i], inv_sh[i], mq[src_mod[i]].q), v0[i], v1[i]);
-        }
+        const uint64_t x = src[(long long)i * BN + e];
+        split25(prescaled ? x : mul_shoup(x, inv[i], inv_sh[i], mq[src_mod[i]].q), v0[i], v1[i]);
     }
-    for (int d = 0; d < n_dst; ++d) {
-        const uint2 *h = (const uint2 *)(sh + d * n_src);
-        Acc3 acc;
-        acc3_zero(acc);
+    int d = 0;
+    for (; d + 1 < n_dst; d += 2) {  // two targets in flight
+        const uint2 *h0 = (const uint2 *)(sh + d * NS);
+        const uint2 *h1 = (const uint2 *)(sh + (d + 1) * NS);
+        Acc3 a0, a1;
+        acc3_zero(a0);
+        acc3_zero(a1);
 #pragma unroll
-        for (int i = 0; i < NS; ++i)
-            if (i < n_src) {
-                const uint2 hv = h[i];
-                acc3_mac(acc, v0[i], v1[i], hv.x, hv.y);
-            }
-        dst[(long long)sidx[d] * BN + e] = acc3_reduce(acc, smq[d]);
+        for (int i = 0; i < NS; ++i) {
+            const uint2 x = h0[i], y = h1[i];
+            acc3_mac(a0, v0[i], v1[i], x.x, x.y);
+            acc3_mac(a1, v0[i], v1[i], y.x, y.y);
+        }
+        dst[(long long)sidx[d] * BN + e] = acc3_reduce(a0, smq[d]);
+        dst[(long long)sidx[d + 1] * BN + e] = acc3_reduce(a1, smq[d + 1]);
+    }
+    if (d < n_dst) {
+        const uint2 *h0 = (const uint2 *)(sh + d * NS);
+        Acc3 a0;
+        acc3_zero(a0);
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+            const uint2 x = h0[i];
+            acc3_mac(a0, v0[i], v1[i], x.x, x.y);
+        }
+        dst[(long long)sidx[d] * BN + e] = acc3_reduce(a0, smq[d]);
     }
 }
 
@@ -458,23 +472,23 @@ static int conv_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint6
     const size_t smem = sizeof(uint64_t) * (size_t)n_dst * T.n_src + sizeof(ModQ) * n_dst + sizeof(int) * n_dst;
     const dim3 grid((unsigned)((BN + 127) / 128));
 #define CONV_CASE(NSV)                                                                                        \
-    if (T.n_src <= NSV) {                                                                                     \
+    case NSV:                                                                                                 \
         if (smem > 48 * 1024)                                                                                 \
             cudaFuncSetAttribute(k_conv<NSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
         k_conv<NSV><<<grid, 128, smem, c->stream>>>(src, T.n_src, T.d_inv, T.d_inv_sh, T.d_hat, T.d_src_mod, \
-                                                     T.d_dst_mod, n_dst, dst, mode, l, c->n_q, BN, c->d_modq,    \
+                                                     T.d_dst_mod, n_dst, dst, mode, l, c->n_q, BN, c->d_modq, \
                                                      prescaled);                                              \
         ++c->launches;                                                                                        \
         HK_LAUNCH_CHECK(c, "basis conversion");                                                              \
-        return HK_OK;                                                                                         \
+        return HK_OK;
+    switch (T.n_src) {
+        CONV_CASE(1) CONV_CASE(2) CONV_CASE(3) CONV_CASE(4) CONV_CASE(5) CONV_CASE(6) CONV_CASE(7) CONV_CASE(8)
+        CONV_CASE(9) CONV_CASE(10) CONV_CASE(11) CONV_CASE(12) CONV_CASE(13) CONV_CASE(14) CONV_CASE(15)
+        CONV_CASE(16) CONV_CASE(17) CONV_CASE(18) CONV_CASE(19) CONV_CASE(20)
+        default: break;
     }
-    CONV_CASE(4)
-    CONV_CASE(8)
-    CONV_CASE(16)
-    CONV_CASE(32)
-    CONV_CASE(48)
 #undef CONV_CASE
-    return hk_fail(c, HK_E_ARG, "basis conversion with %d sources exceeds 48", T.n_src);
+    return hk_fail(c, HK_E_ARG, "basis conversion with %d sources exceeds 20", T.n_src);
 }
 
 // words of scratch the key switch at level l needs
