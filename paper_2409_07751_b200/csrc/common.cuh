@@ -195,6 +195,7 @@ struct hk_ctx {
     std::map<uint32_t, uint64_t *> gal;
     bool have_keys;
     unsigned long long launches;    // kernels enqueued by this context (bench evidence)
+    bool persistent_ntt;            // persistent software-pipelined NTT kernels (HK_NTT_PERSISTENT=1; measured slower)
     // scratch workspace (grown on demand, stream-ordered use only)
     void *ws;
     size_t ws_bytes;

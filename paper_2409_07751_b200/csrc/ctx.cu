@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -150,6 +151,10 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     c->ws = nullptr;
     c->ws_bytes = 0;
     c->launches = 0;
+    {
+        const char *e = getenv("HK_NTT_PERSISTENT");  // opt-in: slower than hardware-scheduled clusters
+        c->persistent_ntt = e && e[0] == '1';
+    }
     c->d_sk = c->d_relin = nullptr;
     const int N = c->n, nm = c->n_mod;
     std::vector<uint64_t> psi(nm);

@@ -82,6 +82,22 @@ __device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMo
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_id_x() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned n_clusters_x() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
 
 // ---------------------------------------------------------------- forward
 template <bool kBig, class Pro>
@@ -174,6 +190,53 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
     }
 }
 
+// Persistent, software-pipelined variant: each cluster walks polynomials
+// P = cluster, cluster + n_clusters, ...; the barrier is split so the next
+// polynomial's column phase (DRAM loads + compute) overlaps the wait for the
+// current one's column phase on the other CTAs.
+template <bool kBig, class Pro, class Epi>
+__device__ __forceinline__ void fwd_persistent(uint64_t *inter_base, int limb0, int B, long long p_begin,
+                                               long long n_polys, const double2 *__restrict__ tw,
+                                               const FpMod *__restrict__ fm, const Pro &pro, const Epi &epi,
+                                               double *smd) {
+    const int c = blockIdx.x & 7;
+    const long long stride = n_clusters_x();
+    long long P = p_begin + cluster_id_x();
+    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
+    double *const ib = reinterpret_cast<double *>(inter_base);
+    {
+        const int l = (int)(P / B), mi = limb0 + l;
+        fwd_cols<kBig>(pro, l, P, ib + P * kN, c, tw + (size_t)mi * kN, fm[mi], smd);
+    }
+    cluster_arrive();
+    while (true) {
+        const long long Pn = P + stride;
+        __syncthreads();
+        if (Pn < n_polys) {
+            const int l = (int)(Pn / B), mi = limb0 + l;
+            fwd_cols<kBig>(pro, l, Pn, ib + Pn * kN, c, tw + (size_t)mi * kN, fm[mi], smd);
+        }
+        __syncthreads();
+        cluster_wait();
+        {
+            const int l = (int)(P / B), mi = limb0 + l;
+            fwd_row<kBig>(epi, l, P, ib + P * kN, r, tw + (size_t)mi * kN, fm[mi], smd + rs * kRowPad);
+        }
+        if (Pn >= n_polys) break;
+        cluster_arrive();
+        P = Pn;
+    }
+}
+
+template <class Pro, class Epi>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
+    fwd_kernel_p(uint64_t *__restrict__ inter_base, int limb0, int B, long long p_begin, long long p_end,
+                 const double2 *__restrict__ tw, const FpMod *__restrict__ fm, int big, Pro pro, Epi epi) {
+    extern __shared__ double smd[];
+    if (big) fwd_persistent<true>(inter_base, limb0, B, p_begin, p_end, tw, fm, pro, epi, smd);
+    else fwd_persistent<false>(inter_base, limb0, B, p_begin, p_end, tw, fm, pro, epi, smd);
+}
+
 // ---------------------------------------------------------------- inverse
 template <bool kBig, class Pro>
 __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, double *inter, int r,
@@ -264,6 +327,50 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
     }
 }
 
+template <bool kBig, class Pro, class Epi>
+__device__ __forceinline__ void inv_persistent(uint64_t *inter_base, int limb0, int B, long long p_begin,
+                                               long long n_polys, const double2 *__restrict__ itw,
+                                               const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
+                                               const Pro &pro, const Epi &epi, double *smd) {
+    const int c = blockIdx.x & 7;
+    const long long stride = n_clusters_x();
+    long long P = p_begin + cluster_id_x();
+    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
+    double *const ib = reinterpret_cast<double *>(inter_base);
+    {
+        const int l = (int)(P / B), mi = limb0 + l;
+        inv_row<kBig>(pro, l, P, ib + P * kN, r, itw + (size_t)mi * kN, fm[mi], smd + rs * kRowPad);
+    }
+    cluster_arrive();
+    while (true) {
+        const long long Pn = P + stride;
+        __syncthreads();
+        if (Pn < n_polys) {
+            const int l = (int)(Pn / B), mi = limb0 + l;
+            inv_row<kBig>(pro, l, Pn, ib + Pn * kN, r, itw + (size_t)mi * kN, fm[mi], smd + rs * kRowPad);
+        }
+        __syncthreads();
+        cluster_wait();
+        {
+            const int l = (int)(P / B), mi = limb0 + l;
+            inv_cols<kBig>(epi, l, P, ib + P * kN, c, itw + (size_t)mi * kN, ninv[mi], fm[mi], smd);
+        }
+        if (Pn >= n_polys) break;
+        cluster_arrive();
+        P = Pn;
+    }
+}
+
+template <class Pro, class Epi>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
+    inv_kernel_p(uint64_t *__restrict__ inter_base, int limb0, int B, long long p_begin, long long p_end,
+                 const double2 *__restrict__ itw, const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
+                 int big, Pro pro, Epi epi) {
+    extern __shared__ double smd[];
+    if (big) inv_persistent<true>(inter_base, limb0, B, p_begin, p_end, itw, ninv, fm, pro, epi, smd);
+    else inv_persistent<false>(inter_base, limb0, B, p_begin, p_end, itw, ninv, fm, pro, epi, smd);
+}
+
 // ---------------------------------------------------------------- functors
 struct ProPlain {  // in[P][idx]
     const uint64_t *in;
@@ -275,13 +382,65 @@ struct EpiPlain {  // out[P][idx] = v
 };
 
 // ---------------------------------------------------------------- launchers
+// persistent grid: the number of co-resident 8-CTA clusters (queried once per
+// kernel instantiation), capped by the work
+template <class K>
+inline unsigned persistent_clusters(K kernel, long long n_polys) {
+    static int cap = 0;
+    if (!cap) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 8;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(8 * 64);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 16;
+        }
+        cap = n;
+    }
+    return (unsigned)(n_polys < cap ? n_polys : cap);
+}
+// the persistent kernels run one prime class (q < 2^47 or not) per launch: a
+// launch is split into class-uniform runs of limbs (q_0 is the only large
+// prime in KAN parameters); functors still see full-launch limb indices
+inline int class_run(const hk_ctx *c, int limb0, int from, int n_limbs, bool &big) {
+    big = c->mod_h[limb0 + from] >= kSmallPrime;
+    int to = from + 1;
+    while (to < n_limbs && (c->mod_h[limb0 + to] >= kSmallPrime) == big) ++to;
+    return to;
+}
+
 template <class Pro, class Epi>
 inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
     if (n_limbs <= 0 || B <= 0) return HK_OK;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fwd_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaFuncSetAttribute(fwd_kernel_p<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         attr = true;
+    }
+    if (c->persistent_ntt) {
+        for (int from = 0; from < n_limbs;) {
+            bool big;
+            const int to = class_run(c, limb0, from, n_limbs, big);
+            const long long pb = (long long)from * B, pe = (long long)to * B;
+            const unsigned nc = persistent_clusters(fwd_kernel_p<Pro, Epi>, pe - pb);
+            fwd_kernel_p<Pro, Epi><<<8u * nc, 512, kSmem, c->stream>>>(inter, limb0, B, pb, pe,
+                                                                      (const double2 *)c->d_twf,
+                                                                      (const FpMod *)c->d_fmod, big ? 1 : 0, pro, epi);
+            ++c->launches;
+            from = to;
+        }
+        HK_LAUNCH_CHECK(c, "ntt16 fwd (persistent)");
+        return HK_OK;
     }
     const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
     fwd_kernel<Pro, Epi><<<blocks, 512, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_twf,
@@ -297,7 +456,24 @@ inline int launch_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B,
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(inv_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaFuncSetAttribute(inv_kernel_p<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         attr = true;
+    }
+    if (c->persistent_ntt) {
+        for (int from = 0; from < n_limbs;) {
+            bool big;
+            const int to = class_run(c, limb0, from, n_limbs, big);
+            const long long pb = (long long)from * B, pe = (long long)to * B;
+            const unsigned nc = persistent_clusters(inv_kernel_p<Pro, Epi>, pe - pb);
+            inv_kernel_p<Pro, Epi><<<8u * nc, 512, kSmem, c->stream>>>(inter, limb0, B, pb, pe,
+                                                                      (const double2 *)c->d_itwf,
+                                                                      (const double2 *)c->d_ninvf,
+                                                                      (const FpMod *)c->d_fmod, big ? 1 : 0, pro, epi);
+            ++c->launches;
+            from = to;
+        }
+        HK_LAUNCH_CHECK(c, "ntt16 inv (persistent)");
+        return HK_OK;
     }
     const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
     inv_kernel<Pro, Epi><<<blocks, 512, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_itwf,

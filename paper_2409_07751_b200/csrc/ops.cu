@@ -144,6 +144,14 @@ __global__ void k_tensor(const uint64_t *__restrict__ a, int la, const uint64_t 
     d[2 * pl + o] = mul_mod(a1, b1, m);
 }
 
+__global__ void k_tensor2(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb,
+                          uint64_t *__restrict__ d2, long long BN, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    (void)p;
+    const long long o = (long long)l * BN + e;
+    d2[o] = mul_mod(a[(long long)(la + 1) * BN + o], b[(long long)(lb + 1) * BN + o], mq[l]);
+}
+
 // ------------------------------------------------------------ key switching
 // Fast basis conversion: dst[t] = sum_i [src_i * inv_i]_{q_i} * hat[t][i] mod q_t.
 // The source residues of one coefficient stay in registers (NS >= n_src), the
@@ -209,7 +217,8 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
 }
 
 // acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][chain(t)] ; grid (BN/256, ne)
-__global__ void k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d, int alpha, int nd, int ne,
+__global__ void k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
+                         const uint64_t *__restrict__ dm, int alpha, int nd, int ne,
                          int l, int n_q, int nm, int log_n, const uint64_t *__restrict__ key, uint32_t g,
                          uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1, const ModQ *__restrict__ mq,
                          long long BN) {
@@ -227,7 +236,14 @@ __global__ void k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__res
     for (int j = 0; j < nd; ++j) {
         uint32_t x0, x1, y0, y1;
         const bool own = t >= j * alpha && t < (j + 1) * alpha && t <= l;  // digit's own limb: NTT form of d
-        split25(own ? d[(long long)t * BN + src_e] : ext[((long long)j * ne + t) * BN + src_e], x0, x1);
+        uint64_t x;
+        if (own) {
+            const long long od = (long long)t * BN + src_e;
+            x = dm ? mul_mod(d[od], dm[od], mm) : d[od];  // relinearisation: d = a1 (.) b1 on the fly
+        } else {
+            x = ext[((long long)j * ne + t) * BN + src_e];
+        }
+        split25(x, x0, x1);
         const uint64_t *kj = key + ((size_t)j * 2 * nm + m) * N;
         split25(kj[k], y0, y1);
         acc3_mac(a0, x0, x1, y0, y1);
@@ -429,6 +445,66 @@ __global__ void k_mdrs_finish(const uint64_t *__restrict__ acc, const uint64_t *
     const uint64_t y = add_mod(acc[o], mul_shoup(d[o], P.x, P.y, q), q);
     out[o] = mul_shoup(sub_mod(y, conv[o], q), w.x, w.y, q);
 }
+// tensor-product terms of (a, b) at limb l, element o (NTT domain):
+// d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1
+struct Tensor {
+    const uint64_t *a, *b;
+    long long pa, pb;  // offset of poly 1 in a / b
+    const ModQ *mq;
+    __device__ __forceinline__ uint64_t d(int which, int l, long long o) const {
+        const ModQ m = mq[l];
+        if (which == 0) return mul_mod(a[o], b[o], m);
+        if (which == 2) return mul_mod(a[pa + o], b[pb + o], m);
+        Acc3 acc;
+        acc3_zero(acc);
+        acc3_mac(acc, a[o], b[pb + o]);
+        acc3_mac(acc, a[pa + o], b[o]);
+        return acc3_reduce(acc, m);
+    }
+};
+// iNTT prologue for the relinearisation ModUp: d2 = a1 b1 on the fly
+struct ProD2 {
+    Tensor T;
+    long long BN;
+    int B;
+    __device__ __forceinline__ uint64_t operator()(int l, long long P, int idx) const {
+        return T.d(2, l, (long long)l * BN + (P - (long long)l * B) * ntt16::kN + idx);
+    }
+};
+// NTT epilogue, merged ModDown + rescale with d_p formed from (a, b)
+struct EpiMdRsT {
+    const uint64_t *acc;
+    Tensor T;
+    int which;
+    uint64_t *out;
+    const ulonglong2 *pmod, *mqinv;
+    const ModQ *mq;
+    int B, log_n;
+    long long BN;
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 Pm = pmod[l], w = mqinv[l];
+        const uint64_t y = add_mod(acc[o], mul_shoup(T.d(which, l, o), Pm.x, Pm.y, q), q);
+        out[o] = mul_shoup(sub_mod(y, v, q), w.x, w.y, q);
+    }
+};
+// iNTT prologue: y = acc_l + P d_l with d_l from (a, b)
+struct ProMdYT {
+    const uint64_t *acc;
+    Tensor T;
+    int which, l;
+    long long BN;
+    const ulonglong2 *pmod;
+    const ModQ *mq;
+    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
+        const long long o = (long long)l * BN + P * ntt16::kN + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 Pm = pmod[l];
+        return add_mod(acc[o], mul_shoup(T.d(which, l, o), Pm.x, Pm.y, q), q);
+    }
+};
+
 // iNTT prologue: y = acc_l + P d_l (prime l)
 struct ProMdY {
     const uint64_t *acc_l, *d_l;
@@ -604,10 +680,11 @@ static int ks_modup(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb
     return HK_OK;
 }
 
-static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, const uint64_t *key, uint32_t g) {
+static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, const uint64_t *key, uint32_t g,
+                 const uint64_t *dm = nullptr) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
     const long long BN = (long long)B * c->n;
-    k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(kb.ext, d, c->alpha, nd, ne, l, c->n_q, c->n_mod, c->log_n, key, g,
+    k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(kb.ext, d, dm, c->alpha, nd, ne, l, c->n_q, c->n_mod, c->log_n, key, g,
                                                       kb.acc, kb.acc + (size_t)ne * BN, c->d_modq, BN);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "key inner product");
@@ -670,6 +747,54 @@ static int ks_moddown_rescale(hk_ctx *c, const uint64_t *a, const uint64_t *dp, 
     k_mdrs_finish<<<egrid(BN, l, 1), 256, 0, c->stream>>>(a, dp, kb.conv, out, c->d_pmod, mqinv, c->d_modq, BN);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "moddown-rescale finish");
+    return HK_OK;
+}
+
+// ct x ct at N = 2^16: the tensor product is never materialised — d2 feeds the
+// ModUp iNTT prologue, d0 / d1 are recomputed inside the merged ModDown +
+// rescale (prologue of the q_l limb, epilogue of every output limb).
+static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, int lb, int l, int B,
+                     const KsBufs &kb, uint64_t *out) {
+    const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
+    const long long BN = (long long)B * c->n;
+    const Tensor T{a, b, (long long)(la + 1) * BN, (long long)(lb + 1) * BN, c->d_modq};
+    EpiScaleDigits esd;
+    memset(&esd, 0, sizeof esd);
+    esd.out = kb.dc;
+    esd.alpha = c->alpha;
+    esd.mq = c->d_modq;
+    if (nd > 8) return hk_fail(c, HK_E_ARG, "more than 8 key-switching digits");
+    for (int j = 0; j < nd; ++j) {
+        esd.inv[j] = c->modup[l][j].d_inv;
+        esd.inv_sh[j] = c->modup[l][j].d_inv_sh;
+    }
+    int rc = ntt16::launch_inv(c, kb.dc, 0, l + 1, B, ProD2{T, BN, B}, esd);
+    if (rc) return rc;
+    for (int j = 0; j < nd; ++j) {
+        const ConvTable &Tc = c->modup[l][j];
+        const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, l + 1);
+        uint64_t *ej = kb.ext + (size_t)j * ne * BN;
+        if ((rc = conv_launch(c, Tc, kb.dc + (size_t)d0 * BN, ej, 0, l, BN, -1, 1))) return rc;
+        if (d0 > 0 && (rc = ntt_fwd_launch(c, ej, 0, d0, B, 0))) return rc;
+        if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
+        if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
+    }
+    // own-digit limbs of d2 are formed inside the key IP from a1 (.) b1
+    if ((rc = ks_ip(c, a + (size_t)(la + 1) * BN, l, B, kb, c->d_relin, 1u, b + (size_t)(lb + 1) * BN))) return rc;
+    const ConvTable &Tm = c->mdrs[l];
+    const ulonglong2 *mqinv = c->d_mqinv + (size_t)l * c->n_q;
+    for (int p = 0; p < 2; ++p) {
+        const uint64_t *acc = kb.acc + (size_t)p * ne * BN;
+        EpiScale es{kb.sp, Tm.d_inv, Tm.d_inv_sh, c->d_modq, c->n_q};
+        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{acc + (size_t)(l + 1) * BN}, es)))
+            return rc;
+        ProMdYT py{acc, T, p, l, BN, c->d_pmod, c->d_modq};
+        EpiScale es2{kb.sp + (size_t)np * BN, Tm.d_inv + np, Tm.d_inv_sh + np, c->d_modq, l};
+        if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * BN, l, 1, B, py, es2))) return rc;
+        if ((rc = conv_launch(c, Tm, kb.sp, kb.conv, 1, l, BN, l, 1))) return rc;
+        EpiMdRsT epi{acc, T, p, out + (size_t)p * l * BN, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN};
+        if ((rc = ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv}, epi))) return rc;
+    }
     return HK_OK;
 }
 
@@ -823,6 +948,7 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
     uint64_t *d = ws;
     const KsBufs kb = ks_bufs(c, l, B, ws + 3 * pl);
+    if (c->log_n == ntt16::kLogN) return mul_fused(c, a, la, b, lb, l, B, kb, out);
     k_tensor<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");
