@@ -290,10 +290,20 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
     t = ev[0].elapsed_time(ev[1]) / reps / 1e3
     alg = 2.0 * nl * B * N * 8
     ach = alg / t / 1e9
+    traffic = None
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum of the same launch shape (ncu --set full)
+        with open(os.path.join(ROOT, "profiles", "r1_ntt_traffic.json")) as fh:
+            tr = json.load(fh)
+        if tr.get("algorithmic_bytes") == alg:
+            traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+    except Exception:
+        pass
     out["ntt"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                  "frac": round(ach / hbm, 4), "traffic": None,
-                  "kernel": f"hk_ntt_fwd (ntt16_fwd_cols + ntt16_fwd_rows), {nl} limbs x {B} polys",
-                  "algorithmic_bytes": alg, "ms": round(t * 1e3, 3)}
+                  "frac": round(ach / hbm, 4), "traffic": traffic,
+                  "kernel": f"hk_ntt_fwd -> ntt16::fwd_kernel (one 8-CTA cluster per polynomial, FP64-pipe "
+                            f"butterflies), {nl} limbs x {B} polys",
+                  "algorithmic_bytes": alg, "ms": round(t * 1e3, 3),
+                  "note": "compute/latency bound: ncu fp64 pipe 45%, issue 32% (profiles/r1_ntt_traffic.json)"}
     del buf
     # key switch via one rotation at the top level (ModUp + IP + ModDown)
     x = np.zeros((B, params.slot_count))
@@ -313,6 +323,7 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
     ach = alg / t / 1e9
     out["keyswitch"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                         "frac": round(ach / hbm, 4), "traffic": None,
+                        "note": "integer-pipe bound: ~250 limb-NTTs + ~2,400 conversion MACs per coefficient",
                         "kernel": f"hk_rotate (ModUp+KeyIP+ModDown) level {l}, {B} cts",
                         "algorithmic_bytes": alg, "ms": round(t * 1e3, 3)}
     return out
