@@ -82,7 +82,8 @@ def build_model(cfg: KanConfig, calib: np.ndarray, seed: int = 0) -> KanModel:
         S = rng.normal(0.0, cfg.w_std, (n_o, n_i, grid.n_basis))
         act = estimate_range(x, x_min=float(np.min(x)), x_max=float(np.max(x)), factor=5.0)
         poly = fit_weighted_ls(silu, act, cfg.silu_degree, w=WeightScheme.from_moments(act.mu, act.sigma))
-        layer = KanLayer(W_b=W_b, S=S, grid=grid, silu_poly=poly, act_stats=(act.mu, act.sigma))
+        layer = KanLayer(W_b=W_b, S=S, grid=grid, silu_poly=poly, act_stats=(act.mu, act.sigma),
+                         fit_range=(act.lo, act.hi))
         layers.append(layer)
         x = np.stack([layer_forward_plain(layer, row, mode="exact") for row in x])
     return KanModel(layers=layers, input_shape=cfg.input_shape)

@@ -42,7 +42,8 @@ def comparator_json():
     return cs
 
 
-def build_ref_model(dims, g, k, lo, hi, w_std, degree, calib, input_shape, seed=0, explicit_R=False):
+def build_ref_model(dims, g, k, lo, hi, w_std, degree, calib, input_shape, seed=0, explicit_R=False,
+                    ranges=None):
     """SURVEY §8(d) recipe through the reference's own classes."""
     rng = np.random.default_rng(seed)
     layers = []
@@ -55,6 +56,8 @@ def build_ref_model(dims, g, k, lo, hi, w_std, degree, calib, input_shape, seed=
         W_b = rng.normal(0.0, w_std, (n_o, n_i))
         S = rng.normal(0.0, w_std, (n_o, n_i, grid.n_basis))
         act = ra.estimate_range(x, x_min=float(np.min(x)), x_max=float(np.max(x)), factor=5.0)
+        if ranges is not None:
+            ranges.append((act.lo, act.hi))
         poly = ra.fit_weighted_ls(rm.silu, act, degree, w=ra.WeightScheme.from_moments(act.mu, act.sigma))
         layer = rm.KanLayer(W_b=W_b, S=S, grid=grid, silu_poly=poly, act_stats=(act.mu, act.sigma))
         layers.append(layer)
@@ -99,6 +102,27 @@ def main():
                         mirrored_naive=naive, plan_total=np.array(plan.total),
                         counts=np.array(json.dumps({"lazy": counts, "naive": counts_naive})),
                         **model_arrays("", model))
+    # ---- c3 [4,8,4,1] G=10 k=3 on [-2,2], deg-63 SiLU; 4096 clip(N(0,1)) inputs (first 8 kept)
+    rng = np.random.default_rng(1)
+    X3 = np.clip(rng.normal(0.0, 1.0, (4096, 4)), -2.0, 2.0)
+    rg3 = []
+    m3 = build_ref_model((4, 8, 4, 1), 10, 3, -2.0, 2.0, 0.1, 63, X3, (1, 1, 4), ranges=rg3)
+    Xs = X3[:8]
+    np.savez_compressed(os.path.join(HERE, "c3.npz"), X=Xs,
+                        mirrored=np.stack([rm.model_forward_plain(m3, x, "mirrored", cs, "lazy") for x in Xs]),
+                        exact=np.stack([rm.model_forward_plain(m3, x, "exact") for x in Xs]),
+                        ranges=np.array(rg3), plan_total=np.array(ri.plan_model(m3, ri.PipelineConfig()).total),
+                        **model_arrays("", m3))
+    # ---- c4 [784,64,10] G=5 k=3 [-1,1], explicit R; 64 x U[0,1]^784 (first 4 kept)
+    rng = np.random.default_rng(1)
+    X4 = rng.uniform(0.0, 1.0, (64, 784))
+    rg4 = []
+    m4 = build_ref_model((784, 64, 10), 5, 3, -1.0, 1.0, 0.05, 10, X4, (28, 28, 1), explicit_R=True, ranges=rg4)
+    Xs = X4[:4]
+    np.savez_compressed(os.path.join(HERE, "c4.npz"), X=Xs,
+                        mirrored=np.stack([rm.model_forward_plain(m4, x, "mirrored", cs, "lazy") for x in Xs]),
+                        exact=np.stack([rm.model_forward_plain(m4, x, "exact") for x in Xs]),
+                        ranges=np.array(rg4), plan_total=np.array(ri.plan_model(m4, ri.PipelineConfig()).total))
     # ---- small random models (reference random_model, uniform weights)
     small = {}
     for idx, (dims, g, k) in enumerate([((3, 4), 3, 2), ((4, 3, 2), 4, 3), ((2, 6, 3), 5, 1)]):

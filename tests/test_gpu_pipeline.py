@@ -91,3 +91,46 @@ def test_full_size_properties(gpu_lib):
     for _ in range(36):
         c = be.mul(c, 1.0)
     assert c.level == 0 and np.abs(c.slots - x).max() < 1e-5
+
+
+def test_c3_pipeline_bitexact_vs_oracle(gpu_lib):
+    from oracle.engine import OracleEngine
+    _, model, X = configs.workload("c3", batch=8)
+    p = make_params(9, 54)
+    bc = BackendConfig(slot_count=p.slot_count, depth_budget=54)
+    g, o = _gpu(p, 54), HeBackend(bc, p, engine=OracleEngine(p))
+    cfg = inf.PipelineConfig()
+    og, _ = inf.model_forward_he(model, inf.encrypt_input(X[:2], model, g), cfg)
+    oo, _ = inf.model_forward_he(model, inf.encrypt_input(X[:2], model, o), cfg)
+    assert np.array_equal(g.export_ct(og), o.export_ct(oo))
+
+
+def _twin(model, X):
+    from paper_2409_07751_b200 import model as mdl
+    cs = inf.PipelineConfig().comparator()
+    return np.stack([mdl.model_forward_plain(model, x, "mirrored", cs, "lazy", schedule="cheb") for x in X])
+
+
+def test_c3_full_ring_degree(gpu_lib):
+    g_ = np.load(os.path.join(GOLD, "c3.npz"))
+    _, model, X = configs.workload("c3", batch=8)
+    be = _gpu(kan_params(54), 54)
+    out, _ = inf.model_forward_he(model, inf.encrypt_input(X[:4], model, be), inf.PipelineConfig())
+    dec = be.decrypt(out)[:, :1]
+    assert np.abs(dec - _twin(model, X[:4])).max() < 1e-4
+    assert np.abs(dec - g_["mirrored"][:4]).max() < 1e-3  # reference's own float SiLU error ~2e-4 (DESIGN §5)
+
+
+def test_c4_full_ring_degree(gpu_lib):
+    """[784,64,10]: 6272-diagonal BSGS, 80 hoisted baby steps, explicit R."""
+    g_ = np.load(os.path.join(GOLD, "c4.npz"))
+    _, model, X = configs.workload("c4", batch=4)
+    be = _gpu(kan_params(36), 36)
+    out, stats = inf.model_forward_he(model, inf.encrypt_input(X[:2], model, be), inf.PipelineConfig())
+    dec = be.decrypt(out)[:, :10]
+    twin = _twin(model, X[:2])
+    err_twin = np.abs(dec - twin).max()
+    err_ref = np.abs(dec - g_["mirrored"][:2]).max()
+    print(f"c4: |dec - exact-arithmetic twin| = {err_twin:.3g}, |dec - reference mirrored| = {err_ref:.3g}")
+    assert err_twin < 1e-4
+    assert stats.to_json()["total"]["rotations"] == 287

@@ -165,3 +165,54 @@ def test_bench_compare_rows():
                                            inf.PipelineConfig(path="naive", backend=bc, label="c1")],
                              backend_factory=fac)
     assert rows[0]["rotations"] == 2 * 41 and rows[0]["speedup_vs_naive_counts"] > 1.0
+
+
+def test_c3_builder_reproduces_reference_model():
+    g = np.load(os.path.join(GOLD, "c3.npz"))
+    _, model, X = configs.workload("c3", batch=8)
+    assert np.array_equal(X, g["X"])
+    for i, layer in enumerate(model.layers):
+        assert np.array_equal(layer.W_b, g[f"L{i}_W_b"]) and np.array_equal(layer.S, g[f"L{i}_S"])
+        assert np.array_equal(np.array(layer.silu_poly.coeffs), g[f"L{i}_silu"])
+        assert tuple(layer.fit_range) == tuple(g["ranges"][i])
+    assert inf.plan_model(model, inf.PipelineConfig()).total == int(g["plan_total"]) == 54
+
+
+def test_c3_chebyshev_silu_is_the_same_polynomial():
+    """Degree-63 fits on narrow ranges (|monomial coef| up to 9e31) run in the
+    Chebyshev basis of their fit interval: exact vs rational evaluation."""
+    from fractions import Fraction as F
+    from paper_2409_07751_b200.approx import eval_silu_cheb_clear, silu_uses_cheb
+    _, model, _ = configs.workload("c3", batch=8)
+    for layer in model.layers[1:]:
+        assert silu_uses_cheb(layer)
+        lo, hi = layer.fit_range
+        xs = np.linspace(lo, hi, 9)
+        ex = np.array([float(sum(F(c) * F(float(v)) ** k for k, c in enumerate(layer.silu_poly.coeffs)))
+                       for v in xs])
+        assert np.abs(eval_silu_cheb_clear(layer, xs) - ex).max() < 1e-12
+
+
+def test_c3_encrypted_matches_reference():
+    g = np.load(os.path.join(GOLD, "c3.npz"))
+    _, model, X = configs.workload("c3", batch=8)
+    be = oracle_backend(54, log_n=9)
+    B = 2
+    out, stats = inf.model_forward_he(model, inf.encrypt_input(X[:B], model, be), inf.PipelineConfig())
+    assert out.level == 0
+    dec = be.decrypt(out)[:, :1]
+    cs = inf.PipelineConfig().comparator()
+    twin = np.stack([mdl.model_forward_plain(model, x, "mirrored", cs, "lazy", schedule="cheb") for x in X[:B]])
+    assert np.abs(dec - twin).max() < TOL
+    assert np.abs(dec - g["mirrored"][:B]).max() < TOL
+
+
+def test_c4_model_matches_reference_ranges():
+    g = np.load(os.path.join(GOLD, "c4.npz"))
+    _, model, X = configs.workload("c4", batch=4)
+    assert np.array_equal(X, g["X"])
+    for i, layer in enumerate(model.layers):
+        assert tuple(layer.fit_range) == tuple(g["ranges"][i])
+    cs = build_composite_sign()
+    mine = np.stack([mdl.model_forward_plain(model, x, "mirrored", cs, "lazy") for x in X[:1]])
+    assert np.array_equal(mine, g["mirrored"][:1])
