@@ -184,7 +184,7 @@ def test_c3_chebyshev_silu_is_the_same_polynomial():
     from fractions import Fraction as F
     from paper_2409_07751_b200.approx import eval_silu_cheb_clear, silu_uses_cheb
     _, model, _ = configs.workload("c3", batch=8)
-    for layer in model.layers[1:]:
+    for layer in model.layers:
         assert silu_uses_cheb(layer)
         lo, hi = layer.fit_range
         xs = np.linspace(lo, hi, 9)
@@ -205,6 +205,14 @@ def test_c3_encrypted_matches_reference():
     twin = np.stack([mdl.model_forward_plain(model, x, "mirrored", cs, "lazy", schedule="cheb") for x in X[:B]])
     assert np.abs(dec - twin).max() < TOL
     assert np.abs(dec - g["mirrored"][:B]).max() < TOL
+
+
+def test_silu_program_choice():
+    """c1/c4 keep the reference program (identical counts); c3 is Chebyshev."""
+    from paper_2409_07751_b200.approx import silu_uses_cheb
+    for name in ("c1", "c4"):
+        _, model, _ = configs.workload(name, batch=1)
+        assert not any(silu_uses_cheb(layer) for layer in model.layers), name
 
 
 def test_c4_model_matches_reference_ranges():
