@@ -176,6 +176,8 @@ struct hk_ctx {
     double2 *d_itwf;       // [n_mod][N] inverse twiddles, float64
     double2 *d_ninvf;      // [n_mod] {N^-1, N^-1/q}
     double2 *d_fmod;       // [n_mod] {q, 1/q}
+    double2 *d_twist;      // [n_mod][256][256] psi^(c (2 brv8(r) + 1 - 256)), float64 {w, w/q} (2^16 NTT rows)
+    double2 *d_itwist;     // [n_mod][256][256] inverse twist
     double2 *d_zeta;       // [2N]
     uint32_t *d_rot_group; // [S]
     // rescale: qinv[l][i] = q_l^-1 mod q_i (i < l), Shoup pairs
@@ -195,7 +197,6 @@ struct hk_ctx {
     std::map<uint32_t, uint64_t *> gal;
     bool have_keys;
     unsigned long long launches;    // kernels enqueued by this context (bench evidence)
-    bool persistent_ntt;            // persistent software-pipelined NTT kernels (HK_NTT_PERSISTENT=1; measured slower)
     // scratch workspace (grown on demand, stream-ordered use only)
     void *ws;
     size_t ws_bytes;

@@ -151,10 +151,6 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     c->ws = nullptr;
     c->ws_bytes = 0;
     c->launches = 0;
-    {
-        const char *e = getenv("HK_NTT_PERSISTENT");  // opt-in: slower than hardware-scheduled clusters
-        c->persistent_ntt = e && e[0] == '1';
-    }
     c->d_sk = c->d_relin = nullptr;
     const int N = c->n, nm = c->n_mod;
     std::vector<uint64_t> psi(nm);
@@ -208,6 +204,31 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
         c->d_itwf = upload(itwf);
         c->d_ninvf = upload(ninvf);
         c->d_fmod = upload(fmod);
+        // four-step twist for the 256 x 256 split (N = 2^16 only): row r, column c
+        c->d_twist = c->d_itwist = nullptr;
+        if (c->log_n == 16) {
+            std::vector<double2> tws((size_t)nm * N), itws((size_t)nm * N);
+            const uint64_t M2 = 2ull * N;
+            for (int m = 0; m < nm; ++m) {
+                const uint64_t q = c->mod_h[m];
+                const double qd = (double)q;
+                for (int r = 0; r < 256; ++r) {
+                    const int64_t e = 2 * (int64_t)h_brv((uint32_t)r, 8) + 1 - 256;  // may be negative
+                    const uint64_t ep = (uint64_t)((e % (int64_t)M2 + (int64_t)M2) % (int64_t)M2);
+                    const uint64_t base = h_powmod(psi[m], ep, q), ibase = h_inv(base, q);
+                    uint64_t t = 1, it = 1;
+                    for (int col = 0; col < 256; ++col) {
+                        const size_t o = (size_t)m * N + (size_t)r * 256 + col;
+                        tws[o] = make_double2((double)t, (double)t / qd);
+                        itws[o] = make_double2((double)it, (double)it / qd);
+                        t = h_mulmod(t, base, q);
+                        it = h_mulmod(it, ibase, q);
+                    }
+                }
+            }
+            c->d_twist = upload(tws);
+            c->d_itwist = upload(itws);
+        }
     }
     // canonical-embedding tables (same formulas as the oracle)
     const int M = 2 * N;
@@ -303,6 +324,8 @@ void hk_ctx_destroy(hk_ctx *c) {
     cudaFree(c->d_itwf);
     cudaFree(c->d_ninvf);
     cudaFree(c->d_fmod);
+    cudaFree(c->d_twist);
+    cudaFree(c->d_itwist);
     cudaFree(c->d_zeta);
     cudaFree(c->d_rot_group);
     cudaFree(c->d_rs_qinv);

@@ -29,7 +29,7 @@ namespace ntt16 {
 constexpr int kLogN = 16;
 constexpr int kN = 1 << kLogN;
 constexpr int kRowPad = 272;                 // 256 + 16: pad one element every 16
-constexpr int kSmem = 32 * kRowPad * 8;      // >= 256 * 32 * 8 for the column phase
+constexpr int kSmem = 32 * kRowPad * 8 + 256 * 16;  // data tile (>= 256*32*8) + 256-entry twiddle table
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 constexpr double kTwo52 = 4503599627370496.0;  // 2^52
 constexpr uint64_t kSmallPrime = 1ull << 47;
@@ -82,23 +82,6 @@ __device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMo
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void cluster_arrive() {
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ unsigned cluster_id_x() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned n_clusters_x() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-    return r;
-}
-
 // ---------------------------------------------------------------- forward
 template <bool kBig, class Pro>
 __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, double *inter, int tile,
@@ -130,20 +113,33 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
     for (int v = 0; v < 16; ++v) inter[(16 * k + v) * 256 + col] = kBig ? x[v] : f_center(x[v], m);
 }
 
+// Row phase (four-step form): Z[r][c] = X[r][c] * tau(r, c) with
+// tau(r, c) = psi^(c (2 brv8(r) + 1 - 256)); then the same 256-point negacyclic
+// CT as the column phase (root psi^256, shared table T[1..255] held in shared
+// memory `st`), output in bit-reversed order within the row. This is exactly
+// stages 8..15 of the full transform; the twist replaces 255 row-specific
+// twiddles per row by one coalesced table element per coefficient.
 template <bool kBig, class Epi>
 __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, const double *inter, int r,
-                                        const double2 *__restrict__ T, const FpMod &m, double *srow) {
+                                        const double2 *__restrict__ tau, const double2 *st, const FpMod &m,
+                                        double *srow) {
     const int k = threadIdx.x & 15;
     const double *rd = inter + r * 256;
+    const double2 *tr = tau + r * 256;
     double x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = __ldcg(rd + k + 16 * u);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const double2 t = __ldg(tr + k + 16 * u);
+        x[u] = f_mulmod(x[u], t.x, t.y, m.q);
+    }
 #pragma unroll
     for (int sp = 0; sp < 4; ++sp) {
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], m);
+            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = x[u];
@@ -155,8 +151,7 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
         const int d = 128 >> sp;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d))
-                ct_f<kBig>(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], m);
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], st[(1 << sp) + ((16 * k + v) >> (8 - sp))], m);
     }
     __syncwarp();
     uint64_t *su = reinterpret_cast<uint64_t *>(srow);
@@ -167,80 +162,46 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
     for (int u = 0; u < 16; ++u) epi(l, P, r * 256 + k + 16 * u, su[pad16(k + 16 * u)]);
 }
 
+// stage the shared 256-entry twiddle table of prime mi into shared memory
+__device__ __forceinline__ void stage_table(double2 *st, const double2 *__restrict__ T) {
+    if (threadIdx.x < 256) st[threadIdx.x] = T[threadIdx.x];
+}
+
 template <class Pro, class Epi>
 __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
     fwd_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ tw,
-               const FpMod *__restrict__ fm, Pro pro, Epi epi) {
+               const double2 *__restrict__ twist, const FpMod *__restrict__ fm, Pro pro, Epi epi) {
     extern __shared__ double smd[];
+    double2 *st = reinterpret_cast<double2 *>(smd + 32 * kRowPad);
     const int c = blockIdx.x & 7;
     const long long P = blockIdx.x >> 3;
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = tw + (size_t)mi * kN;
+    const double2 *tau = twist + (size_t)mi * kN;
+    stage_table(st, T);
+    __syncthreads();
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
     const int rs = threadIdx.x >> 4, r = c * 32 + rs;
     if (m.q < (double)kSmallPrime) {
-        fwd_cols<false>(pro, l, P, inter, c, T, m, smd);
+        fwd_cols<false>(pro, l, P, inter, c, st, m, smd);
         cluster_sync_all();
-        fwd_row<false>(epi, l, P, inter, r, T, m, smd + rs * kRowPad);
+        fwd_row<false>(epi, l, P, inter, r, tau, st, m, smd + rs * kRowPad);
     } else {
-        fwd_cols<true>(pro, l, P, inter, c, T, m, smd);
+        fwd_cols<true>(pro, l, P, inter, c, st, m, smd);
         cluster_sync_all();
-        fwd_row<true>(epi, l, P, inter, r, T, m, smd + rs * kRowPad);
+        fwd_row<true>(epi, l, P, inter, r, tau, st, m, smd + rs * kRowPad);
     }
-}
-
-// Persistent, software-pipelined variant: each cluster walks polynomials
-// P = cluster, cluster + n_clusters, ...; the barrier is split so the next
-// polynomial's column phase (DRAM loads + compute) overlaps the wait for the
-// current one's column phase on the other CTAs.
-template <bool kBig, class Pro, class Epi>
-__device__ __forceinline__ void fwd_persistent(uint64_t *inter_base, int limb0, int B, long long p_begin,
-                                               long long n_polys, const double2 *__restrict__ tw,
-                                               const FpMod *__restrict__ fm, const Pro &pro, const Epi &epi,
-                                               double *smd) {
-    const int c = blockIdx.x & 7;
-    const long long stride = n_clusters_x();
-    long long P = p_begin + cluster_id_x();
-    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
-    double *const ib = reinterpret_cast<double *>(inter_base);
-    {
-        const int l = (int)(P / B), mi = limb0 + l;
-        fwd_cols<kBig>(pro, l, P, ib + P * kN, c, tw + (size_t)mi * kN, fm[mi], smd);
-    }
-    cluster_arrive();
-    while (true) {
-        const long long Pn = P + stride;
-        __syncthreads();
-        if (Pn < n_polys) {
-            const int l = (int)(Pn / B), mi = limb0 + l;
-            fwd_cols<kBig>(pro, l, Pn, ib + Pn * kN, c, tw + (size_t)mi * kN, fm[mi], smd);
-        }
-        __syncthreads();
-        cluster_wait();
-        {
-            const int l = (int)(P / B), mi = limb0 + l;
-            fwd_row<kBig>(epi, l, P, ib + P * kN, r, tw + (size_t)mi * kN, fm[mi], smd + rs * kRowPad);
-        }
-        if (Pn >= n_polys) break;
-        cluster_arrive();
-        P = Pn;
-    }
-}
-
-template <class Pro, class Epi>
-__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
-    fwd_kernel_p(uint64_t *__restrict__ inter_base, int limb0, int B, long long p_begin, long long p_end,
-                 const double2 *__restrict__ tw, const FpMod *__restrict__ fm, int big, Pro pro, Epi epi) {
-    extern __shared__ double smd[];
-    if (big) fwd_persistent<true>(inter_base, limb0, B, p_begin, p_end, tw, fm, pro, epi, smd);
-    else fwd_persistent<false>(inter_base, limb0, B, p_begin, p_end, tw, fm, pro, epi, smd);
 }
 
 // ---------------------------------------------------------------- inverse
+// Row phase, inverse (four-step form): the unscaled inverse of the twisted
+// forward row phase is GS over the shared inverse table Ti[1..255] followed by
+// multiplication with tau^-1(r, c).
 template <bool kBig, class Pro>
 __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, double *inter, int r,
-                                        const double2 *__restrict__ T, const FpMod &m, double *srow) {
+                                        const double2 *__restrict__ itau, const double2 *st, const FpMod &m,
+                                        double *srow) {
     const int k = threadIdx.x & 15;
     double x[16];
 #pragma unroll
@@ -253,8 +214,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 128 >> sp;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d))
-                gs_f<kBig>(x[v], x[v + d], T[(256 << sp) + (r << sp) + ((16 * k + v) >> (8 - sp))], m);
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[(1 << sp) + ((16 * k + v) >> (8 - sp))], m);
     }
     __syncwarp();
 #pragma unroll
@@ -267,11 +227,15 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(256 << sp) + (r << sp) + (u >> (4 - sp))], m);
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m);
     }
+    const double2 *tr = itau + r * 256;
     double *rd = inter + r * 256;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) rd[k + 16 * u] = kBig ? x[u] : f_center(x[u], m);
+    for (int u = 0; u < 16; ++u) {
+        const double2 t = __ldg(tr + k + 16 * u);
+        rd[k + 16 * u] = f_center(f_mulmod(x[u], t.x, t.y, m.q), m);
+    }
 }
 
 template <bool kBig, class Epi>
@@ -307,68 +271,29 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
 template <class Pro, class Epi>
 __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
     inv_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ itw,
-               const double2 *__restrict__ ninv, const FpMod *__restrict__ fm, Pro pro, Epi epi) {
+               const double2 *__restrict__ itwist, const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
+               Pro pro, Epi epi) {
     extern __shared__ double smd[];
+    double2 *st = reinterpret_cast<double2 *>(smd + 32 * kRowPad);
     const int c = blockIdx.x & 7;
     const long long P = blockIdx.x >> 3;
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = itw + (size_t)mi * kN;
+    const double2 *itau = itwist + (size_t)mi * kN;
+    stage_table(st, T);
+    __syncthreads();
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
     const int rs = threadIdx.x >> 4, r = c * 32 + rs;
     if (m.q < (double)kSmallPrime) {
-        inv_row<false>(pro, l, P, inter, r, T, m, smd + rs * kRowPad);
+        inv_row<false>(pro, l, P, inter, r, itau, st, m, smd + rs * kRowPad);
         cluster_sync_all();
-        inv_cols<false>(epi, l, P, inter, c, T, ninv[mi], m, smd);
+        inv_cols<false>(epi, l, P, inter, c, st, ninv[mi], m, smd);
     } else {
-        inv_row<true>(pro, l, P, inter, r, T, m, smd + rs * kRowPad);
+        inv_row<true>(pro, l, P, inter, r, itau, st, m, smd + rs * kRowPad);
         cluster_sync_all();
-        inv_cols<true>(epi, l, P, inter, c, T, ninv[mi], m, smd);
+        inv_cols<true>(epi, l, P, inter, c, st, ninv[mi], m, smd);
     }
-}
-
-template <bool kBig, class Pro, class Epi>
-__device__ __forceinline__ void inv_persistent(uint64_t *inter_base, int limb0, int B, long long p_begin,
-                                               long long n_polys, const double2 *__restrict__ itw,
-                                               const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
-                                               const Pro &pro, const Epi &epi, double *smd) {
-    const int c = blockIdx.x & 7;
-    const long long stride = n_clusters_x();
-    long long P = p_begin + cluster_id_x();
-    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
-    double *const ib = reinterpret_cast<double *>(inter_base);
-    {
-        const int l = (int)(P / B), mi = limb0 + l;
-        inv_row<kBig>(pro, l, P, ib + P * kN, r, itw + (size_t)mi * kN, fm[mi], smd + rs * kRowPad);
-    }
-    cluster_arrive();
-    while (true) {
-        const long long Pn = P + stride;
-        __syncthreads();
-        if (Pn < n_polys) {
-            const int l = (int)(Pn / B), mi = limb0 + l;
-            inv_row<kBig>(pro, l, Pn, ib + Pn * kN, r, itw + (size_t)mi * kN, fm[mi], smd + rs * kRowPad);
-        }
-        __syncthreads();
-        cluster_wait();
-        {
-            const int l = (int)(P / B), mi = limb0 + l;
-            inv_cols<kBig>(epi, l, P, ib + P * kN, c, itw + (size_t)mi * kN, ninv[mi], fm[mi], smd);
-        }
-        if (Pn >= n_polys) break;
-        cluster_arrive();
-        P = Pn;
-    }
-}
-
-template <class Pro, class Epi>
-__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
-    inv_kernel_p(uint64_t *__restrict__ inter_base, int limb0, int B, long long p_begin, long long p_end,
-                 const double2 *__restrict__ itw, const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
-                 int big, Pro pro, Epi epi) {
-    extern __shared__ double smd[];
-    if (big) inv_persistent<true>(inter_base, limb0, B, p_begin, p_end, itw, ninv, fm, pro, epi, smd);
-    else inv_persistent<false>(inter_base, limb0, B, p_begin, p_end, itw, ninv, fm, pro, epi, smd);
 }
 
 // ---------------------------------------------------------------- functors
@@ -382,69 +307,18 @@ struct EpiPlain {  // out[P][idx] = v
 };
 
 // ---------------------------------------------------------------- launchers
-// persistent grid: the number of co-resident 8-CTA clusters (queried once per
-// kernel instantiation), capped by the work
-template <class K>
-inline unsigned persistent_clusters(K kernel, long long n_polys) {
-    static int cap = 0;
-    if (!cap) {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 8;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(8 * 64);
-        cfg.blockDim = dim3(512);
-        cfg.dynamicSmemBytes = kSmem;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
-            cudaGetLastError();
-            n = 16;
-        }
-        cap = n;
-    }
-    return (unsigned)(n_polys < cap ? n_polys : cap);
-}
-// the persistent kernels run one prime class (q < 2^47 or not) per launch: a
-// launch is split into class-uniform runs of limbs (q_0 is the only large
-// prime in KAN parameters); functors still see full-launch limb indices
-inline int class_run(const hk_ctx *c, int limb0, int from, int n_limbs, bool &big) {
-    big = c->mod_h[limb0 + from] >= kSmallPrime;
-    int to = from + 1;
-    while (to < n_limbs && (c->mod_h[limb0 + to] >= kSmallPrime) == big) ++to;
-    return to;
-}
-
 template <class Pro, class Epi>
 inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
     if (n_limbs <= 0 || B <= 0) return HK_OK;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fwd_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        cudaFuncSetAttribute(fwd_kernel_p<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         attr = true;
-    }
-    if (c->persistent_ntt) {
-        for (int from = 0; from < n_limbs;) {
-            bool big;
-            const int to = class_run(c, limb0, from, n_limbs, big);
-            const long long pb = (long long)from * B, pe = (long long)to * B;
-            const unsigned nc = persistent_clusters(fwd_kernel_p<Pro, Epi>, pe - pb);
-            fwd_kernel_p<Pro, Epi><<<8u * nc, 512, kSmem, c->stream>>>(inter, limb0, B, pb, pe,
-                                                                      (const double2 *)c->d_twf,
-                                                                      (const FpMod *)c->d_fmod, big ? 1 : 0, pro, epi);
-            ++c->launches;
-            from = to;
-        }
-        HK_LAUNCH_CHECK(c, "ntt16 fwd (persistent)");
-        return HK_OK;
     }
     const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
     fwd_kernel<Pro, Epi><<<blocks, 512, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_twf,
-                                                             (const FpMod *)c->d_fmod, pro, epi);
+                                                             (const double2 *)c->d_twist, (const FpMod *)c->d_fmod,
+                                                             pro, epi);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "ntt16 fwd");
     return HK_OK;
@@ -456,29 +330,12 @@ inline int launch_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B,
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(inv_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        cudaFuncSetAttribute(inv_kernel_p<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         attr = true;
-    }
-    if (c->persistent_ntt) {
-        for (int from = 0; from < n_limbs;) {
-            bool big;
-            const int to = class_run(c, limb0, from, n_limbs, big);
-            const long long pb = (long long)from * B, pe = (long long)to * B;
-            const unsigned nc = persistent_clusters(inv_kernel_p<Pro, Epi>, pe - pb);
-            inv_kernel_p<Pro, Epi><<<8u * nc, 512, kSmem, c->stream>>>(inter, limb0, B, pb, pe,
-                                                                      (const double2 *)c->d_itwf,
-                                                                      (const double2 *)c->d_ninvf,
-                                                                      (const FpMod *)c->d_fmod, big ? 1 : 0, pro, epi);
-            ++c->launches;
-            from = to;
-        }
-        HK_LAUNCH_CHECK(c, "ntt16 inv (persistent)");
-        return HK_OK;
     }
     const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
     inv_kernel<Pro, Epi><<<blocks, 512, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_itwf,
-                                                             (const double2 *)c->d_ninvf, (const FpMod *)c->d_fmod,
-                                                             pro, epi);
+                                                             (const double2 *)c->d_itwist, (const double2 *)c->d_ninvf,
+                                                             (const FpMod *)c->d_fmod, pro, epi);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "ntt16 inv");
     return HK_OK;
