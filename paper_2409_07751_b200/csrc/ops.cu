@@ -181,38 +181,46 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
     __syncthreads();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= BN) return;
-    uint32_t v0[NS], v1[NS];
+    // Karatsuba split MAC: s0 = sum x0 y0, s2 = sum x1 y1, sm = sum (x0+x1)(y0+y1),
+    // s1 = sm - s0 - s2 (once per target): three IMAD.WIDE per multiply-add.
+    uint32_t v0[NS], v1[NS], vs[NS];
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         const uint64_t x = src[(long long)i * BN + e];
         split25(prescaled ? x : mul_shoup(x, inv[i], inv_sh[i], mq[src_mod[i]].q), v0[i], v1[i]);
+        vs[i] = v0[i] + v1[i];
     }
     int d = 0;
     for (; d + 1 < n_dst; d += 2) {  // two targets in flight
         const uint2 *h0 = (const uint2 *)(sh + d * NS);
         const uint2 *h1 = (const uint2 *)(sh + (d + 1) * NS);
-        Acc3 a0, a1;
-        acc3_zero(a0);
-        acc3_zero(a1);
+        uint64_t a0 = 0, a2 = 0, am = 0, b0 = 0, b2 = 0, bm = 0;
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
             const uint2 x = h0[i], y = h1[i];
-            acc3_mac(a0, v0[i], v1[i], x.x, x.y);
-            acc3_mac(a1, v0[i], v1[i], y.x, y.y);
+            a0 = mad_wide(v0[i], x.x, a0);
+            a2 = mad_wide(v1[i], x.y, a2);
+            am = mad_wide(vs[i], x.x + x.y, am);
+            b0 = mad_wide(v0[i], y.x, b0);
+            b2 = mad_wide(v1[i], y.y, b2);
+            bm = mad_wide(vs[i], y.x + y.y, bm);
         }
-        dst[(long long)sidx[d] * BN + e] = acc3_reduce(a0, smq[d]);
-        dst[(long long)sidx[d + 1] * BN + e] = acc3_reduce(a1, smq[d + 1]);
+        const Acc3 A{a0, am - a0 - a2, a2}, Bc{b0, bm - b0 - b2, b2};
+        dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
+        dst[(long long)sidx[d + 1] * BN + e] = acc3_reduce(Bc, smq[d + 1]);
     }
     if (d < n_dst) {
         const uint2 *h0 = (const uint2 *)(sh + d * NS);
-        Acc3 a0;
-        acc3_zero(a0);
+        uint64_t a0 = 0, a2 = 0, am = 0;
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
             const uint2 x = h0[i];
-            acc3_mac(a0, v0[i], v1[i], x.x, x.y);
+            a0 = mad_wide(v0[i], x.x, a0);
+            a2 = mad_wide(v1[i], x.y, a2);
+            am = mad_wide(vs[i], x.x + x.y, am);
         }
-        dst[(long long)sidx[d] * BN + e] = acc3_reduce(a0, smq[d]);
+        const Acc3 A{a0, am - a0 - a2, a2};
+        dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
     }
 }
 
