@@ -56,7 +56,7 @@ typedef struct hk_params {
     int32_t log_n;          /* N = 2^log_n                                            */
     int32_t n_q;            /* ciphertext primes q_0..q_{n_q-1}; depth budget = n_q-1 */
     int32_t n_p;            /* special primes for hybrid key switching                */
-    int32_t dnum;           /* key-switching digits over the full q chain             */
+    int32_t dnum;           /* key-switching digits over the full q chain, 1..8       */
     const uint64_t *q;      /* [n_q]                                                  */
     const uint64_t *p;      /* [n_p]                                                  */
     const uint64_t *psi_q;  /* [n_q] primitive 2N-th roots                            */

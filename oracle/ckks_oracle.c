@@ -147,7 +147,7 @@ int hk_sync(hk_ctx *c) { (void)c; return HK_OK; }
 
 int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     (void)device;
-    if (!pr || !out || pr->log_n < 2 || pr->log_n > 17 || pr->n_q < 1 || pr->n_p < 1 || pr->dnum < 1)
+    if (!pr || !out || pr->log_n < 2 || pr->log_n > 17 || pr->n_q < 1 || pr->n_p < 1 || pr->dnum < 1 || pr->dnum > 8)
         return HK_E_ARG;
     hk_ctx *c = (hk_ctx *)calloc(1, sizeof *c);
     c->log_n = pr->log_n;

@@ -225,8 +225,9 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
 }
 
 // acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][chain(t)] ; grid (BN/256, ne)
+template <int ND>
 __global__ void k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
-                         const uint64_t *__restrict__ dm, int alpha, int nd, int ne,
+                         const uint64_t *__restrict__ dm, int alpha, int ne,
                          int l, int n_q, int nm, int log_n, const uint64_t *__restrict__ key, uint32_t g,
                          uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1, const ModQ *__restrict__ mq,
                          long long BN) {
@@ -238,24 +239,34 @@ __global__ void k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__res
     const long long src_e = g == 1u ? e : (e - k + auto_src((uint32_t)k, g, log_n));
     const int m = t <= l ? t : n_q + (t - l - 1);
     const ModQ mm = mq[m];
+    // all loads first (digit count is a template constant): memory-level parallelism
+    uint64_t x[ND], k0[ND], k1[ND];
+    const int own_j = t <= l ? t / alpha : -1;  // digit whose own limb t is: NTT form of d itself
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+        const uint64_t *kj = key + ((size_t)j * 2 * nm + m) * N;
+        k0[j] = kj[k];
+        k1[j] = kj[(size_t)nm * N + k];
+        x[j] = j == own_j ? 0 : ext[((long long)j * ne + t) * BN + src_e];
+    }
+    if (own_j >= 0) {
+        const long long od = (long long)t * BN + src_e;
+        const uint64_t v = d[od];
+        const uint64_t w = dm ? mul_mod(v, dm[od], mm) : v;  // relinearisation: d = a1 (.) b1 on the fly
+#pragma unroll
+        for (int j = 0; j < ND; ++j)
+            if (j == own_j) x[j] = w;
+    }
     Acc3 a0, a1;
     acc3_zero(a0);
     acc3_zero(a1);
-    for (int j = 0; j < nd; ++j) {
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
         uint32_t x0, x1, y0, y1;
-        const bool own = t >= j * alpha && t < (j + 1) * alpha && t <= l;  // digit's own limb: NTT form of d
-        uint64_t x;
-        if (own) {
-            const long long od = (long long)t * BN + src_e;
-            x = dm ? mul_mod(d[od], dm[od], mm) : d[od];  // relinearisation: d = a1 (.) b1 on the fly
-        } else {
-            x = ext[((long long)j * ne + t) * BN + src_e];
-        }
-        split25(x, x0, x1);
-        const uint64_t *kj = key + ((size_t)j * 2 * nm + m) * N;
-        split25(kj[k], y0, y1);
+        split25(x[j], x0, x1);
+        split25(k0[j], y0, y1);
         acc3_mac(a0, x0, x1, y0, y1);
-        split25(kj[(size_t)nm * N + k], y0, y1);
+        split25(k1[j], y0, y1);
         acc3_mac(a1, x0, x1, y0, y1);
     }
     acc0[(long long)t * BN + e] = acc3_reduce(a0, mm);
@@ -692,8 +703,22 @@ static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, c
                  const uint64_t *dm = nullptr) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
     const long long BN = (long long)B * c->n;
-    k_key_ip<<<egrid(BN, ne, 1), 256, 0, c->stream>>>(kb.ext, d, dm, c->alpha, nd, ne, l, c->n_q, c->n_mod, c->log_n, key, g,
-                                                      kb.acc, kb.acc + (size_t)ne * BN, c->d_modq, BN);
+#define HK_KEY_IP(ND)                                                                                        \
+    k_key_ip<ND><<<egrid(BN, ne, 1), 256, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, c->n_mod, \
+                                                          c->log_n, key, g, kb.acc, kb.acc + (size_t)ne * BN,  \
+                                                          c->d_modq, BN)
+    switch (nd) {
+        case 1: HK_KEY_IP(1); break;
+        case 2: HK_KEY_IP(2); break;
+        case 3: HK_KEY_IP(3); break;
+        case 4: HK_KEY_IP(4); break;
+        case 5: HK_KEY_IP(5); break;
+        case 6: HK_KEY_IP(6); break;
+        case 7: HK_KEY_IP(7); break;
+        case 8: HK_KEY_IP(8); break;
+        default: return hk_fail(c, HK_E_ARG, "key switch: more than 8 digits");
+    }
+#undef HK_KEY_IP
     ++c->launches;
     HK_LAUNCH_CHECK(c, "key inner product");
     return HK_OK;
