@@ -225,52 +225,76 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
 }
 
 // acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][chain(t)] ; grid (BN/256, ne)
+// acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j,p[t]  (p = 0, 1) on the FP64 pipe:
+// exact two-product Shoup (ntt16::f_mulmod) with w/q formed once per thread;
+// each thread owns one (coefficient k, limb t) and walks `bb` batch entries so
+// the key pair, the galois index and the address math are paid once.
+// grid (N/min(N,256) * B/bb, ne); every residue is exact, results canonical.
 template <int ND>
-__global__ void k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
-                         const uint64_t *__restrict__ dm, int alpha, int ne,
-                         int l, int n_q, int nm, int log_n, const uint64_t *__restrict__ key, uint32_t g,
-                         uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1, const ModQ *__restrict__ mq,
-                         long long BN) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= BN) return;
-    const int t = blockIdx.y;
+__global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
+                                                const uint64_t *__restrict__ dm, int alpha, int ne, int l, int n_q,
+                                                int nm, int log_n, int bb, const uint64_t *__restrict__ key,
+                                                uint32_t g, uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1,
+                                                const double2 *__restrict__ fmod, long long BN) {
+    using namespace ntt16;
     const int N = 1 << log_n;
-    const int k = (int)(e & (N - 1));
-    const long long src_e = g == 1u ? e : (e - k + auto_src((uint32_t)k, g, log_n));
+    const int kblocks = N / (int)blockDim.x;
+    const int k = (blockIdx.x % kblocks) * blockDim.x + threadIdx.x;
+    const int b0 = (blockIdx.x / kblocks) * bb;
+    const int t = blockIdx.y;
     const int m = t <= l ? t : n_q + (t - l - 1);
-    const ModQ mm = mq[m];
-    // all loads first (digit count is a template constant): memory-level parallelism
-    uint64_t x[ND], k0[ND], k1[ND];
-    const int own_j = t <= l ? t / alpha : -1;  // digit whose own limb t is: NTT form of d itself
+    const double2 fm = fmod[m];
+    const FpMod M{fm.x, fm.y};
+    const int ks = g == 1u ? k : (int)auto_src((uint32_t)k, g, log_n);
+    double w0[ND], v0[ND], w1[ND], v1[ND];
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
         const uint64_t *kj = key + ((size_t)j * 2 * nm + m) * N;
-        k0[j] = kj[k];
-        k1[j] = kj[(size_t)nm * N + k];
-        x[j] = j == own_j ? 0 : ext[((long long)j * ne + t) * BN + src_e];
+        w0[j] = u2d(kj[k]);
+        w1[j] = u2d(kj[(size_t)nm * N + k]);
+        v0[j] = __dmul_rn(w0[j], M.qinv);
+        v1[j] = __dmul_rn(w1[j], M.qinv);
     }
-    if (own_j >= 0) {
-        const long long od = (long long)t * BN + src_e;
-        const uint64_t v = d[od];
-        const uint64_t w = dm ? mul_mod(v, dm[od], mm) : v;  // relinearisation: d = a1 (.) b1 on the fly
+    const int own_j = t <= l ? t / alpha : -1;  // digit whose own limb t is: NTT form of d itself
+    const long long row = (long long)b0 * N;
+    const uint64_t *xe = ext + (long long)t * BN + row + ks;
+    const long long dstride = (long long)ne * BN;
+    const uint64_t *xd = d + (long long)t * BN + row + ks;
+    const uint64_t *xm = dm ? dm + (long long)t * BN + row + ks : nullptr;
+    uint64_t *o0 = acc0 + (long long)t * BN + row + k;
+    uint64_t *o1 = acc1 + (long long)t * BN + row + k;
+    for (int b = 0; b < bb; ++b) {
+        double x[ND];
 #pragma unroll
-        for (int j = 0; j < ND; ++j)
-            if (j == own_j) x[j] = w;
-    }
-    Acc3 a0, a1;
-    acc3_zero(a0);
-    acc3_zero(a1);
+        for (int j = 0; j < ND; ++j) x[j] = j == own_j ? 0.0 : u2d(xe[j * dstride]);
+        if (own_j >= 0) {
+            double y = u2d(*xd);
+            if (xm) {  // relinearisation: d = a1 (.) b1 on the fly
+                const double w = u2d(*xm);
+                y = f_center(f_mulmod(y, w, __dmul_rn(w, M.qinv), M.q), M);
+            }
 #pragma unroll
-    for (int j = 0; j < ND; ++j) {
-        uint32_t x0, x1, y0, y1;
-        split25(x[j], x0, x1);
-        split25(k0[j], y0, y1);
-        acc3_mac(a0, x0, x1, y0, y1);
-        split25(k1[j], y0, y1);
-        acc3_mac(a1, x0, x1, y0, y1);
+            for (int j = 0; j < ND; ++j)
+                if (j == own_j) x[j] = y;
+        }
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < ND; ++j) {  // |f_mulmod| < 2.5 q: recentre every second term
+            s0 = __dadd_rn(s0, f_mulmod(x[j], w0[j], v0[j], M.q));
+            s1 = __dadd_rn(s1, f_mulmod(x[j], w1[j], v1[j], M.q));
+            if (j & 1) {
+                s0 = f_center(s0, M);
+                s1 = f_center(s1, M);
+            }
+        }
+        *o0 = d2canon(s0, M);
+        *o1 = d2canon(s1, M);
+        xe += N;
+        xd += N;
+        if (xm) xm += N;
+        o0 += N;
+        o1 += N;
     }
-    acc0[(long long)t * BN + e] = acc3_reduce(a0, mm);
-    acc1[(long long)t * BN + e] = acc3_reduce(a1, mm);
 }
 
 // out_i = (acc_i - conv_i) * P^-1 (+ optional addend, optionally automorphed) ; grid (BN/256, l+1)
@@ -703,10 +727,12 @@ static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, c
                  const uint64_t *dm = nullptr) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
     const long long BN = (long long)B * c->n;
-#define HK_KEY_IP(ND)                                                                                        \
-    k_key_ip<ND><<<egrid(BN, ne, 1), 256, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, c->n_mod, \
-                                                          c->log_n, key, g, kb.acc, kb.acc + (size_t)ne * BN,  \
-                                                          c->d_modq, BN)
+    const int bb = B % 4 == 0 ? 4 : B % 2 == 0 ? 2 : 1;
+    const int ipt = std::min(256, c->n);
+    const dim3 ipg((unsigned)((c->n / ipt) * (B / bb)), (unsigned)ne);
+#define HK_KEY_IP(ND)                                                                                          \
+    k_key_ip<ND><<<ipg, ipt, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, c->n_mod, c->log_n, bb, key, \
+                                             g, kb.acc, kb.acc + (size_t)ne * BN, c->d_fmod, BN)
     switch (nd) {
         case 1: HK_KEY_IP(1); break;
         case 2: HK_KEY_IP(2); break;
