@@ -166,12 +166,19 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
                                               uint64_t *__restrict__ dst, int mode, int l, int n_q, long long BN,
                                               const ModQ *__restrict__ mq, int prescaled) {
     // NS == n_src exactly (one instantiation per source count): no guards
-    extern __shared__ uint64_t sh[];  // hat [n_dst][NS] as (h0 | h1 << 32), ModQ [n_dst], out index [n_dst]
-    ModQ *smq = (ModQ *)(sh + n_dst * NS);
+    // hat [n_dst][kHs] as 25-bit halves and their sum (h0, h1, h0 + h1) per source, ModQ [n_dst], out index [n_dst]
+    constexpr int kHs = (3 * NS + 3) & ~3;  // words per target, 16-byte aligned rows
+    extern __shared__ uint4 sh4[];
+    uint32_t *sh = reinterpret_cast<uint32_t *>(sh4);
+    ModQ *smq = (ModQ *)(sh + n_dst * kHs);
     int *sidx = (int *)(smq + n_dst);
     for (int i = threadIdx.x; i < n_dst * NS; i += blockDim.x) {
         const uint64_t h = hat[i];
-        sh[i] = ((uint64_t)(uint32_t)(h >> 25) << 32) | ((uint32_t)h & HK_M25);
+        const uint32_t h0 = (uint32_t)h & HK_M25, h1 = (uint32_t)(h >> 25);
+        uint32_t *w = sh + (i / NS) * kHs + 3 * (i % NS);
+        w[0] = h0;
+        w[1] = h1;
+        w[2] = h0 + h1;
     }
     for (int d = threadIdx.x; d < n_dst; d += blockDim.x) {
         const int m = dst_mod[d];
@@ -192,32 +199,30 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
     }
     int d = 0;
     for (; d + 1 < n_dst; d += 2) {  // two targets in flight
-        const uint2 *h0 = (const uint2 *)(sh + d * NS);
-        const uint2 *h1 = (const uint2 *)(sh + (d + 1) * NS);
+        const uint32_t *h0 = sh + d * kHs;
+        const uint32_t *h1 = h0 + kHs;
         uint64_t a0 = 0, a2 = 0, am = 0, b0 = 0, b2 = 0, bm = 0;
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
-            const uint2 x = h0[i], y = h1[i];
-            a0 = mad_wide(v0[i], x.x, a0);
-            a2 = mad_wide(v1[i], x.y, a2);
-            am = mad_wide(vs[i], x.x + x.y, am);
-            b0 = mad_wide(v0[i], y.x, b0);
-            b2 = mad_wide(v1[i], y.y, b2);
-            bm = mad_wide(vs[i], y.x + y.y, bm);
+            a0 = mad_wide(v0[i], h0[3 * i], a0);
+            a2 = mad_wide(v1[i], h0[3 * i + 1], a2);
+            am = mad_wide(vs[i], h0[3 * i + 2], am);
+            b0 = mad_wide(v0[i], h1[3 * i], b0);
+            b2 = mad_wide(v1[i], h1[3 * i + 1], b2);
+            bm = mad_wide(vs[i], h1[3 * i + 2], bm);
         }
         const Acc3 A{a0, am - a0 - a2, a2}, Bc{b0, bm - b0 - b2, b2};
         dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
         dst[(long long)sidx[d + 1] * BN + e] = acc3_reduce(Bc, smq[d + 1]);
     }
     if (d < n_dst) {
-        const uint2 *h0 = (const uint2 *)(sh + d * NS);
+        const uint32_t *h0 = sh + d * kHs;
         uint64_t a0 = 0, a2 = 0, am = 0;
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
-            const uint2 x = h0[i];
-            a0 = mad_wide(v0[i], x.x, a0);
-            a2 = mad_wide(v1[i], x.y, a2);
-            am = mad_wide(vs[i], x.x + x.y, am);
+            a0 = mad_wide(v0[i], h0[3 * i], a0);
+            a2 = mad_wide(v1[i], h0[3 * i + 1], a2);
+            am = mad_wide(vs[i], h0[3 * i + 2], am);
         }
         const Acc3 A{a0, am - a0 - a2, a2};
         dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
@@ -588,7 +593,8 @@ static dim3 egrid(long long BN, int limbs, int polys) {
 static int conv_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l,
                        long long BN, int n_dst = -1, int prescaled = 0) {
     if (n_dst < 0) n_dst = T.n_dst;
-    const size_t smem = sizeof(uint64_t) * (size_t)n_dst * T.n_src + sizeof(ModQ) * n_dst + sizeof(int) * n_dst;
+    const size_t smem =
+        sizeof(uint32_t) * (size_t)n_dst * ((3 * T.n_src + 3) & ~3) + sizeof(ModQ) * n_dst + sizeof(int) * n_dst;
     const dim3 grid((unsigned)((BN + 127) / 128));
 #define CONV_CASE(NSV)                                                                                        \
     case NSV:                                                                                                 \
