@@ -1,7 +1,7 @@
 // ntt16.cuh — fused N = 2^16 negacyclic NTT kernels with prologue/epilogue hooks.
 //
-// One 8-CTA thread-block cluster per polynomial (see ntt.cu for the stage
-// split). The first phase reads its inputs through a prologue functor and the
+// One 16-CTA thread-block cluster (non-portable size, 256 threads per CTA,
+// four CTAs per SM) per polynomial (see ntt.cu for the stage split). The first phase reads its inputs through a prologue functor and the
 // second phase hands canonical outputs to an epilogue functor, so element-wise
 // work that surrounds an NTT in CKKS (basis conversion, the rescale
 // remainder broadcast, plaintext products, the ModDown / rescale finish) runs
@@ -28,8 +28,11 @@ namespace ntt16 {
 
 constexpr int kLogN = 16;
 constexpr int kN = 1 << kLogN;
+constexpr int kCl = 16;                      // CTAs per cluster (non-portable size): one polynomial
+constexpr int kTh = 256;                     // threads per CTA: 16 values each
+constexpr int kTc = 256 / kCl;               // columns (column phase) / rows (row phase) per CTA
 constexpr int kRowPad = 272;                 // 256 + 16: pad one element every 16
-constexpr int kSmem = 32 * kRowPad * 8 + 256 * 16;  // data tile (>= 256*32*8) + 256-entry twiddle table
+constexpr int kSmem = kTc * kRowPad * 8 + 256 * 16;  // data tile (>= 256*kTc*8) + 256-entry twiddle table
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 constexpr double kTwo52 = 4503599627370496.0;  // 2^52
 constexpr uint64_t kSmallPrime = 1ull << 47;
@@ -86,7 +89,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 template <bool kBig, class Pro>
 __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, double *inter, int tile,
                                          const double2 *__restrict__ T, const FpMod &m, double *sm) {
-    const int c = threadIdx.x & 31, k = threadIdx.x >> 5, col = tile * 32 + c;
+    const int c = threadIdx.x % kTc, k = threadIdx.x / kTc, col = tile * kTc + c;
     double x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = u2d(pro(l, P, (k + 16 * u) * 256 + col));
@@ -98,10 +101,10 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
             if (!(u & d)) ct_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m);
     }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) sm[(k + 16 * u) * 32 + c] = x[u];
+    for (int u = 0; u < 16; ++u) sm[(k + 16 * u) * kTc + c] = x[u];
     __syncthreads();
 #pragma unroll
-    for (int v = 0; v < 16; ++v) x[v] = sm[(16 * k + v) * 32 + c];
+    for (int v = 0; v < 16; ++v) x[v] = sm[(16 * k + v) * kTc + c];
 #pragma unroll
     for (int s = 4; s < 8; ++s) {
         const int d = 128 >> s;
@@ -164,17 +167,17 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
 
 // stage the shared 256-entry twiddle table of prime mi into shared memory
 __device__ __forceinline__ void stage_table(double2 *st, const double2 *__restrict__ T) {
-    if (threadIdx.x < 256) st[threadIdx.x] = T[threadIdx.x];
+    for (int i = threadIdx.x; i < 256; i += kTh) st[i] = T[i];
 }
 
 template <class Pro, class Epi>
-__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
     fwd_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ tw,
                const double2 *__restrict__ twist, const FpMod *__restrict__ fm, Pro pro, Epi epi) {
     extern __shared__ double smd[];
-    double2 *st = reinterpret_cast<double2 *>(smd + 32 * kRowPad);
-    const int c = blockIdx.x & 7;
-    const long long P = blockIdx.x >> 3;
+    double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
+    const int c = blockIdx.x % kCl;
+    const long long P = blockIdx.x / kCl;
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = tw + (size_t)mi * kN;
@@ -182,7 +185,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
     stage_table(st, T);
     __syncthreads();
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
-    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
+    const int rs = threadIdx.x >> 4, r = c * kTc + rs;
     if (m.q < (double)kSmallPrime) {
         fwd_cols<false>(pro, l, P, inter, c, st, m, smd);
         cluster_sync_all();
@@ -241,7 +244,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
 template <bool kBig, class Epi>
 __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, const double *inter, int tile,
                                          const double2 *__restrict__ T, double2 ni, const FpMod &m, double *sm) {
-    const int c = threadIdx.x & 31, k = threadIdx.x >> 5, col = tile * 32 + c;
+    const int c = threadIdx.x % kTc, k = threadIdx.x / kTc, col = tile * kTc + c;
     double x[16];
 #pragma unroll
     for (int v = 0; v < 16; ++v) x[v] = __ldcg(inter + (16 * k + v) * 256 + col);
@@ -253,10 +256,10 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
             if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m);
     }
 #pragma unroll
-    for (int v = 0; v < 16; ++v) sm[(16 * k + v) * 32 + c] = x[v];
+    for (int v = 0; v < 16; ++v) sm[(16 * k + v) * kTc + c] = x[v];
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 16; ++u) x[u] = sm[(k + 16 * u) * 32 + c];
+    for (int u = 0; u < 16; ++u) x[u] = sm[(k + 16 * u) * kTc + c];
 #pragma unroll
     for (int s = 3; s >= 0; --s) {
         const int d = 8 >> s;
@@ -269,14 +272,14 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
 }
 
 template <class Pro, class Epi>
-__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
     inv_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ itw,
                const double2 *__restrict__ itwist, const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
                Pro pro, Epi epi) {
     extern __shared__ double smd[];
-    double2 *st = reinterpret_cast<double2 *>(smd + 32 * kRowPad);
-    const int c = blockIdx.x & 7;
-    const long long P = blockIdx.x >> 3;
+    double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
+    const int c = blockIdx.x % kCl;
+    const long long P = blockIdx.x / kCl;
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = itw + (size_t)mi * kN;
@@ -284,7 +287,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
     stage_table(st, T);
     __syncthreads();
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
-    const int rs = threadIdx.x >> 4, r = c * 32 + rs;
+    const int rs = threadIdx.x >> 4, r = c * kTc + rs;
     if (m.q < (double)kSmallPrime) {
         inv_row<false>(pro, l, P, inter, r, itau, st, m, smd + rs * kRowPad);
         cluster_sync_all();
@@ -312,11 +315,12 @@ inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B,
     if (n_limbs <= 0 || B <= 0) return HK_OK;
     static bool attr = false;
     if (!attr) {
+        cudaFuncSetAttribute(fwd_kernel<Pro, Epi>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(fwd_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         attr = true;
     }
-    const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
-    fwd_kernel<Pro, Epi><<<blocks, 512, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_twf,
+    const unsigned blocks = (unsigned)kCl * (unsigned)n_limbs * (unsigned)B;
+    fwd_kernel<Pro, Epi><<<blocks, kTh, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_twf,
                                                              (const double2 *)c->d_twist, (const FpMod *)c->d_fmod,
                                                              pro, epi);
     ++c->launches;
@@ -329,11 +333,12 @@ inline int launch_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B,
     if (n_limbs <= 0 || B <= 0) return HK_OK;
     static bool attr = false;
     if (!attr) {
+        cudaFuncSetAttribute(inv_kernel<Pro, Epi>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(inv_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         attr = true;
     }
-    const unsigned blocks = 8u * (unsigned)n_limbs * (unsigned)B;
-    inv_kernel<Pro, Epi><<<blocks, 512, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_itwf,
+    const unsigned blocks = (unsigned)kCl * (unsigned)n_limbs * (unsigned)B;
+    inv_kernel<Pro, Epi><<<blocks, kTh, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_itwf,
                                                              (const double2 *)c->d_itwist, (const double2 *)c->d_ninvf,
                                                              (const FpMod *)c->d_fmod, pro, epi);
     ++c->launches;
