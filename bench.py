@@ -297,7 +297,7 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
     t = ev[0].elapsed_time(ev[1]) / reps / 1e3
     alg = 2.0 * nl * B * N * 8
     ach = alg / t / 1e9
-    traffic = None
+    traffic, tr = None, {}
     try:  # dram__bytes_read.sum + dram__bytes_write.sum of the same launch shape (ncu --set full)
         with open(os.path.join(ROOT, "profiles", "r1_ntt_traffic.json")) as fh:
             tr = json.load(fh)
@@ -307,10 +307,11 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
         pass
     out["ntt"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                   "frac": round(ach / hbm, 4), "traffic": traffic,
-                  "kernel": f"hk_ntt_fwd -> ntt16::fwd_kernel (one 8-CTA cluster per polynomial, FP64-pipe "
+                  "kernel": f"hk_ntt_fwd -> ntt16::fwd_kernel (one 16-CTA cluster per polynomial, FP64-pipe "
                             f"butterflies), {nl} limbs x {B} polys",
                   "algorithmic_bytes": alg, "ms": round(t * 1e3, 3),
-                  "note": "compute/latency bound: ncu fp64 pipe 45%, issue 32% (profiles/r1_ntt_traffic.json)"}
+                  "note": f"FP64-issue/latency bound: ncu fp64 pipe {tr.get('fp64_pipe_pct')}%, issue "
+                          f"{tr.get('issue_active_pct')}% (profiles/r1_ntt_traffic.json)"}
     del buf
     # key switch via one rotation at the top level (ModUp + IP + ModDown)
     x = np.zeros((B, params.slot_count))
