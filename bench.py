@@ -269,6 +269,10 @@ def run_product(args):
         line["roofline"] = roof["ntt"]
         line["roofline"]["peak_kind"] = hbm_kind
         line["kernels"] = roof
+    if not args.no_c2:
+        del be, eng
+        torch.cuda.empty_cache()
+        line["c2_microbench"] = c2_microbench(local)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
     print(json.dumps(line))
@@ -334,6 +338,72 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
                         "note": "integer-pipe bound: ~250 limb-NTTs + ~2,400 conversion MACs per coefficient",
                         "kernel": f"hk_rotate (ModUp+KeyIP+ModDown) level {l}, {B} cts",
                         "algorithmic_bytes": alg, "ms": round(t * 1e3, 3)}
+    return out
+
+
+def c2_microbench(device: int, n_ct: int = 256, reps: int = 3) -> dict:
+    """BASELINE config 2: 256 ciphertexts with uniform random limbs,
+    N=2^16, 24 ~50-bit limbs, dnum=3 (alpha = 8 special primes); CUDA-event
+    times of NTT / iNTT (both polynomials), HMult+relin+rescale and rotate by
+    +-2^j (j = 0..14, 30 Galois keys), each against SURVEY's algorithmic bytes."""
+    import ctypes as C
+
+    import torch
+    from paper_2409_07751_b200.backend import galois_element
+    from paper_2409_07751_b200.engine import GpuEngine
+    from paper_2409_07751_b200.params import microbench_params
+
+    hbm, _ = _peaks()
+    p = microbench_params()
+    eng = GpuEngine(p, device=device)
+    stream = torch.cuda.current_stream(device)
+    N, n, l = p.n, len(p.q), len(p.q) - 1
+    alpha = len(p.p)
+    ct = eng.alloc_u64(2 * n * n_ct * N).view(2, n, n_ct * N)
+    for i, q in enumerate(p.q):  # uniform residues in [0, q_i)
+        ct[:, i].random_(0, int(q))
+    eng.call("hk_keygen", C.c_uint64(7))
+    steps = [s * (1 << j) for j in range(15) for s in (1, -1)]
+    gal = [galois_element(t, p.slot_count) for t in steps]
+    eng.call("hk_add_galois_keys", C.c_uint64(8), eng.u32_array(gal), len(gal))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def timed(fn, k=reps):
+        fn()
+        torch.cuda.synchronize(device)
+        ev[0].record(stream)
+        for _ in range(k):
+            fn()
+        ev[1].record(stream)
+        torch.cuda.synchronize(device)
+        return ev[0].elapsed_time(ev[1]) / k / 1e3
+
+    def entry(alg, t, what):
+        ach = alg / t / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                "ms": round(t * 1e3, 3), "algorithmic_bytes": alg, "kernel": what}
+
+    out = {"workload": f"c2: {n_ct} ciphertexts x 2 polys x {n} limbs (~50-bit), N=2^16, dnum=3, alpha={alpha}, "
+                       "uniform random limbs"}
+    base = ct.data_ptr()
+    half = n * n_ct * N * 8
+    ntt_b = 2.0 * n_ct * 2 * n * N * 8
+    t = timed(lambda: [eng.call("hk_ntt_fwd", base + q * half, 0, n, n_ct) for q in (0, 1)])
+    out["ntt"] = entry(ntt_b, t, "hk_ntt_fwd, both polynomials")
+    t = timed(lambda: [eng.call("hk_ntt_inv", base + q * half, 0, n, n_ct) for q in (0, 1)])
+    out["intt"] = entry(ntt_b, t, "hk_ntt_inv, both polynomials")
+    dst = eng.alloc_u64(2 * n * n_ct * N)
+    key_b = 2 * p.dnum * (n + alpha) * N * 8
+    t = timed(lambda: eng.call("hk_mul", base, l, base, l, eng.addr(dst), n_ct))
+    out["hmult_relin_rescale"] = entry(n_ct * (4 * n + 2 * (n - 1)) * N * 8 + key_b, t, "hk_mul (tensor, relin, rescale)")
+    del dst
+    rdst = eng.alloc_u64(2 * n * n_ct * N)
+    t = timed(lambda: [eng.call("hk_rotate", base, l, C.c_uint32(g), eng.addr(rdst), n_ct) for g in gal], k=1)
+    t /= len(gal)
+    out["rotate"] = entry(n_ct * 4 * n * N * 8 + key_b, t, "hk_rotate, mean over +-2^j, j=0..14")
+    out["gpu_launches_total"] = int(eng.lib.hk_launch_count(eng.ctx))
+    del rdst, ct, eng
+    torch.cuda.empty_cache()
     return out
 
 
@@ -526,6 +596,7 @@ def main():
     ap.add_argument("--log-n", type=int, default=16)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the config-2 primitive microbench")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
