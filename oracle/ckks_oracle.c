@@ -759,22 +759,29 @@ static void modup(const hk_ctx *c, const uint64_t *d, int l, int B, uint64_t *ex
             }
             const uint64_t qt = c->mod[m];
             uint64_t hat[64]; /* (Q_D/q_i) mod q_t */
+            uint64_t QD = 1;
             for (int i = d0; i < d1; ++i) {
                 uint64_t prod = 1;
                 for (int k = d0; k < d1; ++k)
                     if (k != i) prod = mulmod(prod, c->mod[k] % qt, qt);
                 hat[i - d0] = prod;
+                QD = mulmod(QD, c->mod[i] % qt, qt);
             }
+            const uint64_t negQD = (qt - QD) % qt;
             for (int b = 0; b < B; ++b) {
                 uint64_t *o = dst + (size_t)b * N;
                 for (int k = 0; k < N; ++k) {
                     uint64_t acc = 0;
+                    double frac = 0.0;
                     for (int ii = 0; ii < nD; ++ii) {
                         const int i = d0 + ii;
                         const uint64_t v = mulmod(dc[((size_t)i * B + b) * N + k], inv[ii], c->mod[i]);
+                        frac += (double)v * (1.0 / (double)c->mod[i]);
                         acc = addmod(acc, mulmod(v % qt, hat[ii], qt), qt);
                     }
-                    o[k] = acc;
+                    /* centred digit: the extension of [d]_{Q_D} in (-Q_D/2, Q_D/2] */
+                    const uint64_t u = (uint64_t)floor(frac + 0.5);
+                    o[k] = addmod(acc, mulmod(u % qt, negQD, qt), qt);
                 }
                 ntt_fwd_1(c, o, m);
             }
@@ -812,7 +819,12 @@ static void key_ip(const hk_ctx *c, const uint64_t *ext, int l, int B, const uin
         }
 }
 
-/* ModDown one poly: acc [ne][B][N] (NTT) -> out [l+1][B][N] = (acc - conv([acc]_P)) * P^-1 */
+/* ModDown one poly: acc [ne][B][N] (NTT) -> out [l+1][B][N] = (acc - conv([acc]_P)) * P^-1.
+ * The conversion is centred and exact: u = round(sum_k v_k / p_k) in float64 (fixed order,
+ * no contraction) removes the fast-conversion overflow, so out = round(acc / P). Plain fast
+ * conversion would leave a bias of about -(K+1)/2 per coefficient, which the c1 half
+ * multiplies by s: a random walk of s's partial sums, i.e. low-frequency noise that
+ * concentrates in a few slots. */
 static void moddown(const hk_ctx *c, const uint64_t *acc, int l, int B, uint64_t *out) {
     const int N = c->n, np = c->n_p;
     uint64_t *sp = malloc(sizeof(uint64_t) * (size_t)np * B * N);
@@ -839,16 +851,21 @@ static void moddown(const hk_ctx *c, const uint64_t *acc, int l, int B, uint64_t
             Pm = mulmod(Pm, c->mod[c->n_q + k] % q, q);
         }
         Pinv = invmod(Pm, q);
+        const uint64_t negP = (q - Pm) % q;
         uint64_t *conv = malloc(sizeof(uint64_t) * N);
         for (int b = 0; b < B; ++b) {
             for (int n = 0; n < N; ++n) {
                 uint64_t s = 0;
+                double frac = 0.0;
                 for (int k = 0; k < np; ++k) {
                     const uint64_t pk = c->mod[c->n_q + k];
                     const uint64_t v = mulmod(sp[((size_t)k * B + b) * N + n], inv[k], pk);
+                    frac += (double)v * (1.0 / (double)pk);
                     s = addmod(s, mulmod(v % q, hat[k], q), q);
                 }
-                conv[n] = s;
+                /* centred remainder: -u P with u = round(sum v_k / p_k) (exact rounding of acc / P) */
+                const uint64_t u = (uint64_t)floor(frac + 0.5);
+                conv[n] = addmod(s, mulmod(u % q, negP, q), q);
             }
             ntt_fwd_1(c, conv, i);
             const uint64_t *x = acc + ((size_t)i * B + b) * N;
@@ -899,16 +916,19 @@ static void moddown_rescale(const hk_ctx *c, const uint64_t *acc, const uint64_t
             M = mulmod(M, smod_[s] % q, q);
         }
         for (int k = 0; k < np; ++k) P = mulmod(P, smod_[k] % q, q);
-        const uint64_t Minv = invmod(M, q);
+        const uint64_t Minv = invmod(M, q), negM = (q - M) % q;
         uint64_t *conv = malloc(sizeof(uint64_t) * N);
         for (int b = 0; b < B; ++b) {
             for (int n = 0; n < N; ++n) {
                 uint64_t acc2 = 0;
+                double frac = 0.0;
                 for (int s = 0; s < ns; ++s) {
                     const uint64_t v = mulmod(src[((size_t)s * B + b) * N + n], inv[s], smod_[s]);
+                    frac += (double)v * (1.0 / (double)smod_[s]);
                     acc2 = addmod(acc2, mulmod(v % q, hat[s], q), q);
                 }
-                conv[n] = acc2;
+                const uint64_t u = (uint64_t)floor(frac + 0.5);
+                conv[n] = addmod(acc2, mulmod(u % q, negM, q), q);
             }
             ntt_fwd_1(c, conv, t);
             const size_t o = ((size_t)t * B + b) * N;

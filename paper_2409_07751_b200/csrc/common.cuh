@@ -156,6 +156,11 @@ struct ConvTable {
     uint64_t *d_hat;      // [n_dst][n_src] (Q_src/q_i) mod t
     int32_t *d_src_mod;   // [n_src]  chain index of each source prime
     int32_t *d_dst_mod;   // [n_dst]  chain index of each target prime
+    // centred (exact) conversion: u = round(sum_i v_i / m_i) in float64, target t adds
+    // u * (-M mod q_t), so the result is the centred remainder exactly (ModUp digits,
+    // ModDown, merged ModDown + rescale); nullptr = plain fast conversion
+    double *d_src_invd;   // [n_src]  1 / m_i
+    uint64_t *d_neg_m;    // [n_dst]  -M mod q_t
 };
 
 // ---------------------------------------------------------------------------
@@ -172,12 +177,15 @@ struct hk_ctx {
     ulonglong2 *d_tw;      // [n_mod][N] {psi^brv(k), shoup}
     ulonglong2 *d_itw;     // [n_mod][N] {psi^-brv(k), shoup}
     ulonglong2 *d_ninv;    // [n_mod] {N^-1, shoup}
-    double2 *d_twf;        // [n_mod][N] {psi^brv(k), psi^brv(k)/q} as float64 (fused 2^16 NTT)
-    double2 *d_itwf;       // [n_mod][N] inverse twiddles, float64
-    double2 *d_ninvf;      // [n_mod] {N^-1, N^-1/q}
-    double2 *d_fmod;       // [n_mod] {q, 1/q}
-    double2 *d_twist;      // [n_mod][256][256] psi^(c (2 brv8(r) + 1 - 256)), float64 {w, w/q} (2^16 NTT rows)
+    // fused 2^16 kernels (ntt16.cuh), N = 2^16 (root psi) or 2^17 (root psi^2 per half); stride 2^16
+    double2 *d_twf;        // [n_mod][2^16] {w^brv(k), w^brv(k)/q} as float64
+    double2 *d_itwf;       // [n_mod][2^16] inverse twiddles, float64
+    double2 *d_ninvf;      // [n_mod] {2^-16, 2^-16/q}
+    double2 *d_fmod;       // [n_mod] {q, 1/q} (every N)
+    double2 *d_twist;      // [n_mod][256][256] w^(c (2 brv8(r) + 1 - 256)), float64 {w, w/q} (rows)
     double2 *d_itwist;     // [n_mod][256][256] inverse twist
+    ulonglong2 *d_n17;     // N = 2^17: [n_mod][4][2^16] radix-2 pre/post twists (ntt.cu)
+    ulonglong2 *d_n17w;    // N = 2^17: [n_mod][2] {psi^(2^16), inverse}
     double2 *d_zeta;       // [2N]
     uint32_t *d_rot_group; // [S]
     // rescale: qinv[l][i] = q_l^-1 mod q_i (i < l), Shoup pairs

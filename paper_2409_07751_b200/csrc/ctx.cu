@@ -76,7 +76,7 @@ static T *upload(const std::vector<T> &v) {
 
 // fast basis conversion table: sources -> targets (chain indices)
 static ConvTable make_conv(const std::vector<uint64_t> &mod, const std::vector<int> &src,
-                           const std::vector<int> &dst) {
+                           const std::vector<int> &dst, bool exact = false) {
     ConvTable t;
     t.n_src = (int)src.size();
     t.n_dst = (int)dst.size();
@@ -103,6 +103,21 @@ static ConvTable make_conv(const std::vector<uint64_t> &mod, const std::vector<i
     t.d_hat = upload(hat);
     t.d_src_mod = upload(std::vector<int32_t>(src.begin(), src.end()));
     t.d_dst_mod = upload(std::vector<int32_t>(dst.begin(), dst.end()));
+    t.d_src_invd = nullptr;
+    t.d_neg_m = nullptr;
+    if (exact) {  // centred conversion: 1/m_i as float64, -M mod q_t (M = product of the sources)
+        std::vector<double> invd(src.size());
+        for (size_t i = 0; i < src.size(); ++i) invd[i] = 1.0 / (double)mod[src[i]];
+        std::vector<uint64_t> negm(dst.size());
+        for (size_t d = 0; d < dst.size(); ++d) {
+            const uint64_t qt = mod[dst[d]];
+            uint64_t M = 1;
+            for (size_t k = 0; k < src.size(); ++k) M = h_mulmod(M, mod[src[k]] % qt, qt);
+            negm[d] = (qt - M) % qt;
+        }
+        t.d_src_invd = upload(invd);
+        t.d_neg_m = upload(negm);
+    }
     return t;
 }
 
@@ -112,6 +127,8 @@ static void free_conv(ConvTable &t) {
     cudaFree(t.d_hat);
     cudaFree(t.d_src_mod);
     cudaFree(t.d_dst_mod);
+    cudaFree(t.d_src_invd);
+    cudaFree(t.d_neg_m);
 }
 
 extern "C" {
@@ -189,45 +206,78 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     c->d_itw = upload(itw);
     c->d_ninv = upload(ninv);
     {
-        std::vector<double2> twf((size_t)nm * N), itwf((size_t)nm * N), ninvf(nm), fmod(nm);
+        std::vector<double2> fmod(nm);
+        for (int m = 0; m < nm; ++m) fmod[m] = make_double2((double)c->mod_h[m], 1.0 / (double)c->mod_h[m]);
+        c->d_fmod = upload(fmod);
+    }
+    // Tables of the fused 2^16 kernels (ntt16.cuh), float64 {w, w/q}, stride 2^16 per prime:
+    // N = 2^16 uses root psi; N = 2^17 runs each half through the 2^16 kernel with root
+    // psi^2 after one radix-2 stage and a pre-twist by psi^-+i (ntt.cu, ntt17_*).
+    c->d_twf = c->d_itwf = c->d_ninvf = c->d_twist = c->d_itwist = nullptr;
+    c->d_n17 = nullptr;
+    c->d_n17w = nullptr;
+    if (c->log_n == 16 || c->log_n == 17) {
+        const int H = 1 << 16;
+        std::vector<double2> twf((size_t)nm * H), itwf((size_t)nm * H), ninvf(nm);
+        std::vector<double2> tws((size_t)nm * H), itws((size_t)nm * H);
+        const uint64_t M2 = 2ull * H;
         for (int m = 0; m < nm; ++m) {
-            const double qd = (double)c->mod_h[m];
-            for (int k = 0; k < N; ++k) {
-                const size_t o = (size_t)m * N + k;
-                twf[o] = make_double2((double)tw[o].x, (double)tw[o].x / qd);
-                itwf[o] = make_double2((double)itw[o].x, (double)itw[o].x / qd);
+            const uint64_t q = c->mod_h[m];
+            const double qd = (double)q;
+            const uint64_t w = c->log_n == 16 ? psi[m] : h_mulmod(psi[m], psi[m], q), iw = h_inv(w, q);
+            uint64_t pw = 1, ipw = 1;
+            for (int k = 0; k < H; ++k) {
+                const size_t o = (size_t)m * H + h_brv((uint32_t)k, 16);
+                twf[o] = make_double2((double)pw, (double)pw / qd);
+                itwf[o] = make_double2((double)ipw, (double)ipw / qd);
+                pw = h_mulmod(pw, w, q);
+                ipw = h_mulmod(ipw, iw, q);
             }
-            ninvf[m] = make_double2((double)ninv[m].x, (double)ninv[m].x / qd);
-            fmod[m] = make_double2(qd, 1.0 / qd);
+            const uint64_t ni = h_inv((uint64_t)H % q, q);
+            ninvf[m] = make_double2((double)ni, (double)ni / qd);
+            // four-step twist for the 256 x 256 split: row r, column c
+            for (int r = 0; r < 256; ++r) {
+                const int64_t e = 2 * (int64_t)h_brv((uint32_t)r, 8) + 1 - 256;  // may be negative
+                const uint64_t ep = (uint64_t)((e % (int64_t)M2 + (int64_t)M2) % (int64_t)M2);
+                const uint64_t base = h_powmod(w, ep, q), ibase = h_inv(base, q);
+                uint64_t t = 1, it = 1;
+                for (int col = 0; col < 256; ++col) {
+                    const size_t o = (size_t)m * H + (size_t)r * 256 + col;
+                    tws[o] = make_double2((double)t, (double)t / qd);
+                    itws[o] = make_double2((double)it, (double)it / qd);
+                    t = h_mulmod(t, base, q);
+                    it = h_mulmod(it, ibase, q);
+                }
+            }
         }
         c->d_twf = upload(twf);
         c->d_itwf = upload(itwf);
         c->d_ninvf = upload(ninvf);
-        c->d_fmod = upload(fmod);
-        // four-step twist for the 256 x 256 split (N = 2^16 only): row r, column c
-        c->d_twist = c->d_itwist = nullptr;
-        if (c->log_n == 16) {
-            std::vector<double2> tws((size_t)nm * N), itws((size_t)nm * N);
-            const uint64_t M2 = 2ull * N;
+        c->d_twist = upload(tws);
+        c->d_itwist = upload(itws);
+        if (c->log_n == 17) {
+            // [m][4][2^16] Shoup pairs: psi^-i, psi^i (forward pre-twist of halves 0 / 1),
+            // psi^i / 2, psi^-i / 2 (inverse post-twist); [m][2]: w = psi^(2^16), w^-1
+            std::vector<ulonglong2> t17((size_t)nm * 4 * H), w17((size_t)nm * 2);
             for (int m = 0; m < nm; ++m) {
-                const uint64_t q = c->mod_h[m];
-                const double qd = (double)q;
-                for (int r = 0; r < 256; ++r) {
-                    const int64_t e = 2 * (int64_t)h_brv((uint32_t)r, 8) + 1 - 256;  // may be negative
-                    const uint64_t ep = (uint64_t)((e % (int64_t)M2 + (int64_t)M2) % (int64_t)M2);
-                    const uint64_t base = h_powmod(psi[m], ep, q), ibase = h_inv(base, q);
-                    uint64_t t = 1, it = 1;
-                    for (int col = 0; col < 256; ++col) {
-                        const size_t o = (size_t)m * N + (size_t)r * 256 + col;
-                        tws[o] = make_double2((double)t, (double)t / qd);
-                        itws[o] = make_double2((double)it, (double)it / qd);
-                        t = h_mulmod(t, base, q);
-                        it = h_mulmod(it, ibase, q);
-                    }
+                const uint64_t q = c->mod_h[m], ip = h_inv(psi[m], q), half = h_inv(2, q);
+                uint64_t fw = 1, bw = 1;
+                for (int i = 0; i < H; ++i) {
+                    ulonglong2 *row = t17.data() + (size_t)m * 4 * H;
+                    row[i] = make_ulonglong2(bw, h_shoup(bw, q));
+                    row[H + i] = make_ulonglong2(fw, h_shoup(fw, q));
+                    const uint64_t fh = h_mulmod(fw, half, q), bh = h_mulmod(bw, half, q);
+                    row[2 * H + i] = make_ulonglong2(fh, h_shoup(fh, q));
+                    row[3 * H + i] = make_ulonglong2(bh, h_shoup(bh, q));
+                    fw = h_mulmod(fw, psi[m], q);
+                    bw = h_mulmod(bw, ip, q);
                 }
+                const uint64_t w = h_powmod(psi[m], (uint64_t)H, q), wi = h_inv(w, q);
+                w17[2 * m] = make_ulonglong2(w, h_shoup(w, q));
+                w17[2 * m + 1] = make_ulonglong2(wi, h_shoup(wi, q));
             }
-            c->d_twist = upload(tws);
-            c->d_itwist = upload(itws);
+            c->d_n17 = upload(t17);
+            c->d_n17w = upload(w17);
         }
     }
     // canonical-embedding tables (same formulas as the oracle)
@@ -261,7 +311,7 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
             for (int t = 0; t <= l; ++t)
                 if (t < d0 || t >= d1) dst.push_back(t);
             for (int k = 0; k < c->n_p; ++k) dst.push_back(c->n_q + k);
-            c->modup[l].push_back(make_conv(c->mod_h, src, dst));
+            c->modup[l].push_back(make_conv(c->mod_h, src, dst, true));
         }
     }
     // ModDown: specials -> all q primes (a level uses the first l+1 targets)
@@ -269,7 +319,7 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
         std::vector<int> src, dst;
         for (int k = 0; k < c->n_p; ++k) src.push_back(c->n_q + k);
         for (int i = 0; i < c->n_q; ++i) dst.push_back(i);
-        c->moddown = make_conv(c->mod_h, src, dst);
+        c->moddown = make_conv(c->mod_h, src, dst, true);
         std::vector<ulonglong2> pinv(c->n_q);
         for (int i = 0; i < c->n_q; ++i) {
             const uint64_t q = c->mod_h[i];
@@ -293,7 +343,7 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
             for (int k = 0; k < c->n_p; ++k) s2.push_back(c->n_q + k);
             s2.push_back(l);
             for (int t = 0; t < l; ++t) d2.push_back(t);
-            c->mdrs[l] = make_conv(c->mod_h, s2, d2);
+            c->mdrs[l] = make_conv(c->mod_h, s2, d2, true);
             for (int t = 0; t < l; ++t) {
                 const uint64_t q = c->mod_h[t];
                 const uint64_t v = h_inv(h_mulmod(pmod[t].x, c->mod_h[l] % q, q), q);
@@ -326,6 +376,8 @@ void hk_ctx_destroy(hk_ctx *c) {
     cudaFree(c->d_fmod);
     cudaFree(c->d_twist);
     cudaFree(c->d_itwist);
+    cudaFree(c->d_n17);
+    cudaFree(c->d_n17w);
     cudaFree(c->d_zeta);
     cudaFree(c->d_rot_group);
     cudaFree(c->d_rs_qinv);

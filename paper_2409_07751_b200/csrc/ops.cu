@@ -164,7 +164,9 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
                                               const uint64_t *__restrict__ hat, const int32_t *__restrict__ src_mod,
                                               const int32_t *__restrict__ dst_mod, int n_dst,
                                               uint64_t *__restrict__ dst, int mode, int l, int n_q, long long BN,
-                                              const ModQ *__restrict__ mq, int prescaled) {
+                                              const ModQ *__restrict__ mq, int prescaled,
+                                              const double *__restrict__ src_invd,
+                                              const uint64_t *__restrict__ neg_m) {
     // NS == n_src exactly (one instantiation per source count): no guards
     // hat [n_dst][kHs] as 25-bit halves and their sum (h0, h1, h0 + h1) per source, ModQ [n_dst], out index [n_dst]
     constexpr int kHs = (3 * NS + 3) & ~3;  // words per target, 16-byte aligned rows
@@ -191,12 +193,17 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
     // Karatsuba split MAC: s0 = sum x0 y0, s2 = sum x1 y1, sm = sum (x0+x1)(y0+y1),
     // s1 = sm - s0 - s2 (once per target): three IMAD.WIDE per multiply-add.
     uint32_t v0[NS], v1[NS], vs[NS];
+    double frac = 0.0;  // sum_i v_i / m_i (exact mode), fixed order, no contraction
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         const uint64_t x = src[(long long)i * BN + e];
-        split25(prescaled ? x : mul_shoup(x, inv[i], inv_sh[i], mq[src_mod[i]].q), v0[i], v1[i]);
+        const uint64_t v = prescaled ? x : mul_shoup(x, inv[i], inv_sh[i], mq[src_mod[i]].q);
+        if (neg_m) frac = __dadd_rn(frac, __dmul_rn(ntt16::u2d(v), src_invd[i]));
+        split25(v, v0[i], v1[i]);
         vs[i] = v0[i] + v1[i];
     }
+    // centred remainder: subtract u * M with u = round(frac) (u <= NS)
+    const uint64_t u = neg_m ? (uint64_t)floor(__dadd_rn(frac, 0.5)) : 0;
     int d = 0;
     for (; d + 1 < n_dst; d += 2) {  // two targets in flight
         const uint32_t *h0 = sh + d * kHs;
@@ -211,7 +218,11 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
             b2 = mad_wide(v1[i], h1[3 * i + 1], b2);
             bm = mad_wide(vs[i], h1[3 * i + 2], bm);
         }
-        const Acc3 A{a0, am - a0 - a2, a2}, Bc{b0, bm - b0 - b2, b2};
+        Acc3 A{a0, am - a0 - a2, a2}, Bc{b0, bm - b0 - b2, b2};
+        if (neg_m) {
+            A.s0 += u * __ldg(neg_m + d);
+            Bc.s0 += u * __ldg(neg_m + d + 1);
+        }
         dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
         dst[(long long)sidx[d + 1] * BN + e] = acc3_reduce(Bc, smq[d + 1]);
     }
@@ -224,7 +235,8 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
             a2 = mad_wide(v1[i], h0[3 * i + 1], a2);
             am = mad_wide(vs[i], h0[3 * i + 2], am);
         }
-        const Acc3 A{a0, am - a0 - a2, a2};
+        Acc3 A{a0, am - a0 - a2, a2};
+        if (neg_m) A.s0 += u * __ldg(neg_m + d);
         dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
     }
 }
@@ -602,7 +614,7 @@ static int conv_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint6
             cudaFuncSetAttribute(k_conv<NSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
         k_conv<NSV><<<grid, 128, smem, c->stream>>>(src, T.n_src, T.d_inv, T.d_inv_sh, T.d_hat, T.d_src_mod, \
                                                      T.d_dst_mod, n_dst, dst, mode, l, c->n_q, BN, c->d_modq, \
-                                                     prescaled);                                              \
+                                                     prescaled, T.d_src_invd, T.d_neg_m);                     \
         ++c->launches;                                                                                        \
         HK_LAUNCH_CHECK(c, "basis conversion");                                                              \
         return HK_OK;

@@ -15,7 +15,7 @@ from paper_2409_07751_b200.params import make_params, microbench_params
 
 pytestmark = pytest.mark.gpu
 
-CASES = [(5, 6), (10, 4), (13, 3), (16, 3)]
+CASES = [(5, 6), (10, 4), (13, 3), (16, 3), (17, 2)]
 
 
 def _pair(log_n, depth, seed=0, dnum=3):
