@@ -75,9 +75,17 @@ int hk_sync(hk_ctx *ctx);
  * the counter-based stream seeded by `seed` (identical in oracle and GPU). */
 int hk_keygen(hk_ctx *ctx, uint64_t seed);
 int hk_add_galois_keys(hk_ctx *ctx, uint64_t seed, const uint32_t *galois_elts, int32_t n);
+/* Galois keys usable up to ciphertext `level` only: digits 0..level/alpha and the
+ * rows of q_0..q_level plus the special primes (the same values as the full key's
+ * rows, so results are identical). A key already present at a lower level is
+ * regenerated at `level`; one at a higher level is kept. The oracle keeps full keys. */
+int hk_add_galois_keys_level(hk_ctx *ctx, uint64_t seed, const uint32_t *galois_elts, int32_t n,
+                             int32_t level);
+/* 0 if absent, else 1 + the highest ciphertext level the key serves. */
 int hk_has_galois_key(const hk_ctx *ctx, uint32_t galois_elt);
 /* copy key material out (parity tests): which = 0 secret [n_q+n_p][N];
- * 1 relin [n_digits][2][n_q+n_p][N]; 2 galois key for `galois_elt`. */
+ * 1 relin [n_digits][2][n_q+n_p][N]; 2 galois key for `galois_elt` (full-level
+ * keys only, same layout as relin). */
 int hk_export_key(hk_ctx *ctx, int32_t which, uint32_t galois_elt, uint64_t *out);
 uint64_t hk_key_words(const hk_ctx *ctx, int32_t which);
 

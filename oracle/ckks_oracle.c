@@ -492,9 +492,10 @@ int hk_keygen(hk_ctx *c, uint64_t seed) {
     return HK_OK;
 }
 
+/* 0 if absent, else 1 + the highest level the key serves (oracle keys are full) */
 int hk_has_galois_key(const hk_ctx *c, uint32_t g) {
     for (int i = 0; i < c->n_gal; ++i)
-        if (c->gal[i].g == g) return 1;
+        if (c->gal[i].g == g) return c->n_q;
     return 0;
 }
 
@@ -523,6 +524,14 @@ int hk_add_galois_keys(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n) 
         c->n_gal++;
     }
     return HK_OK;
+}
+
+/* Level-truncated keys on the GPU hold a subset of the full key's rows; the
+ * oracle keeps full keys, so key-switching results are identical. */
+int hk_add_galois_keys_level(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n, int32_t level) {
+    if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
+    if (level < 0 || level >= c->n_q) return fail(c, HK_E_ARG, "galois key level %d out of range", level);
+    return hk_add_galois_keys(c, seed, gs, n);
 }
 
 int hk_export_key(hk_ctx *c, int32_t which, uint32_t g, uint64_t *out) {

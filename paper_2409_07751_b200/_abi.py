@@ -32,6 +32,7 @@ SIGNATURES = {
     "hk_sync": (C.c_int, [vp]),
     "hk_keygen": (C.c_int, [vp, u64]),
     "hk_add_galois_keys": (C.c_int, [vp, u64, vp, i32]),
+    "hk_add_galois_keys_level": (C.c_int, [vp, u64, vp, i32, i32]),
     "hk_has_galois_key": (C.c_int, [vp, u32]),
     "hk_export_key": (C.c_int, [vp, i32, u32, vp]),
     "hk_key_words": (C.c_uint64, [vp, i32]),

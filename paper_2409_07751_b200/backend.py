@@ -385,7 +385,7 @@ class HeBackend:
             return a
         self.counter.rotations += 1
         g = galois_element(t, self.config.slot_count)
-        self.ensure_galois_keys([g])
+        self.ensure_galois_keys([g], a.level)
         eng = self.engine
         out = eng.alloc_u64(2 * (a.level + 1) * a.batch * self.n)
         eng.call("hk_rotate", eng.addr(a.data), a.level, C.c_uint32(g), eng.addr(out), a.batch)
@@ -404,7 +404,7 @@ class HeBackend:
         outs = {}
         if todo:
             gs = [galois_element(t, self.config.slot_count) for t in todo]
-            self.ensure_galois_keys(gs)
+            self.ensure_galois_keys(gs, a.level)
             eng = self.engine
             bufs = [eng.alloc_u64(2 * (a.level + 1) * a.batch * self.n) for _ in todo]
             eng.call("hk_rotate_hoisted", eng.addr(a.data), a.level, eng.u32_array(gs), len(gs),
@@ -440,17 +440,23 @@ class HeBackend:
         self.counter.adds += n_terms - 1
         return self._wrap(out, level - 1, B, a0.batched)
 
-    def ensure_galois_keys(self, galois_elts) -> None:
-        missing = [int(g) for g in galois_elts
-                   if not self.engine.lib.hk_has_galois_key(self.engine.ctx, C.c_uint32(int(g)))]
+    def ensure_galois_keys(self, galois_elts, level: int | None = None) -> None:
+        """Galois keys serving ciphertexts up to `level` (default: the top level).
+        The GPU stores a key truncated to the highest level it has been asked
+        for (digits and limbs above it are never read) and regrows it on demand;
+        the key values do not depend on the level, so results are identical."""
+        top = self.config.depth_budget
+        level = top if level is None else min(int(level), top)
+        lib, ctx = self.engine.lib, self.engine.ctx
+        missing = [int(g) for g in galois_elts if lib.hk_has_galois_key(ctx, C.c_uint32(int(g))) < level + 1]
         if missing:
             missing = sorted(set(missing))
-            self.engine.call("hk_add_galois_keys", C.c_uint64(self._seed("galois")),
-                             self.engine.u32_array(missing), len(missing))
+            self.engine.call("hk_add_galois_keys_level", C.c_uint64(self._seed("galois")),
+                             self.engine.u32_array(missing), len(missing), level)
 
-    def ensure_rotation_keys(self, steps) -> None:
+    def ensure_rotation_keys(self, steps, level: int | None = None) -> None:
         self.ensure_galois_keys([galois_element(t, self.config.slot_count)
-                                 for t in steps if t % self.config.slot_count])
+                                 for t in steps if t % self.config.slot_count], level)
 
     # ------------------------------------------------------------------
     # internals

@@ -163,6 +163,14 @@ struct ConvTable {
     uint64_t *d_neg_m;    // [n_dst]  -M mod q_t
 };
 
+// A key-switching key truncated to `level`: digits 0..level/alpha, rows
+// {q_0..q_level, p_0..p_{K-1}} ([digits][2][rows][N]); rows equal the full key's.
+struct GalKey {
+    uint64_t *p;
+    int level;
+    int rows;  // level + 1 + K
+};
+
 // ---------------------------------------------------------------------------
 // context
 // ---------------------------------------------------------------------------
@@ -202,7 +210,7 @@ struct hk_ctx {
     // keys
     uint64_t *d_sk;                 // [n_mod][N]
     uint64_t *d_relin;              // [n_digits][2][n_mod][N]
-    std::map<uint32_t, uint64_t *> gal;
+    std::map<uint32_t, GalKey> gal;
     bool have_keys;
     unsigned long long launches;    // kernels enqueued by this context (bench evidence)
     // scratch workspace (grown on demand, stream-ordered use only)

@@ -47,27 +47,33 @@ __global__ void automorph_polys(const uint64_t *__restrict__ in, uint64_t *__res
 }
 
 // key digit j: a (uniform, NTT domain) and e (coefficient domain, reduced)
+// key rows r < rows: modulus m = r <= top ? r : n_q + (r - top - 1) (top = key level)
+__device__ __forceinline__ int key_row_mod(int r, int top, int n_q) { return r <= top ? r : n_q + (r - top - 1); }
+
 __global__ void ks_sample(uint64_t *__restrict__ b, uint64_t *__restrict__ a, uint64_t seed, uint64_t stream_a,
-                          uint64_t stream_e, int log_n, int nm, const ModQ *__restrict__ mq) {
+                          uint64_t stream_e, int log_n, int rows, int top, int n_q, const ModQ *__restrict__ mq) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int N = 1 << log_n;
-    if (gid >= (long long)nm * N) return;
-    const int m = (int)(gid >> log_n), k = (int)(gid & (N - 1));
+    if (gid >= (long long)rows * N) return;
+    const int r = (int)(gid >> log_n), k = (int)(gid & (N - 1));
+    const int m = key_row_mod(r, top, n_q);
     const uint64_t q = mq[m].q;
     a[gid] = hk_rng64(seed, stream_a, (uint64_t)m * N + k) % q;
     b[gid] = smod_dev(cbd21(hk_rng64(seed, stream_e, (uint64_t)k)), q);
 }
 
-// b = e_ntt - a*s (+ P*s' on digit limbs)
+// b = e_ntt - a*s (+ P*s' on digit limbs); s, sp are full [n_mod][N]
 __global__ void ks_finish(uint64_t *__restrict__ b, const uint64_t *__restrict__ a, const uint64_t *__restrict__ s,
                           const uint64_t *__restrict__ sp, const uint64_t *__restrict__ pmod, int d0, int d1,
-                          int log_n, int nm, const ModQ *__restrict__ mq) {
+                          int log_n, int rows, int top, int n_q, const ModQ *__restrict__ mq) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= ((long long)nm << log_n)) return;
-    const int m = (int)(gid >> log_n);
+    if (gid >= ((long long)rows << log_n)) return;
+    const int r = (int)(gid >> log_n), k = (int)(gid & ((1 << log_n) - 1));
+    const int m = key_row_mod(r, top, n_q);
     const ModQ mm = mq[m];
-    uint64_t v = sub_mod(b[gid], mul_mod(a[gid], s[gid], mm), mm.q);
-    if (m >= d0 && m < d1) v = add_mod(v, mul_mod(pmod[m], sp[gid], mm), mm.q);
+    const long long o = ((long long)m << log_n) + k;
+    uint64_t v = sub_mod(b[gid], mul_mod(a[gid], s[o], mm), mm.q);
+    if (m >= d0 && m < d1) v = add_mod(v, mul_mod(pmod[m], sp[o], mm), mm.q);
     b[gid] = v;
 }
 
@@ -156,8 +162,8 @@ uint64_t h_inv(uint64_t a, uint64_t q) {
 }
 
 // key-switching key for target s' (device [nm][N], NTT) into key [n_digits][2][nm][N]
-int make_ks_key(hk_ctx *c, uint64_t seed, uint64_t tag, const uint64_t *sprime, uint64_t *key) {
-    const int N = c->n, nm = c->n_mod;
+int make_ks_key(hk_ctx *c, uint64_t seed, uint64_t tag, const uint64_t *sprime, uint64_t *key, int top) {
+    const int N = c->n, nm = c->n_mod, rows = top + 1 + c->n_p, nd = top / c->alpha + 1;
     std::vector<uint64_t> pmod(nm, 0);
     for (int i = 0; i < c->n_q; ++i) {
         uint64_t acc = 1;
@@ -167,17 +173,19 @@ int make_ks_key(hk_ctx *c, uint64_t seed, uint64_t tag, const uint64_t *sprime, 
     uint64_t *d_pmod = nullptr;
     HK_CUDA(c, cudaMalloc(&d_pmod, sizeof(uint64_t) * nm));
     HK_CUDA(c, cudaMemcpyAsync(d_pmod, pmod.data(), sizeof(uint64_t) * nm, cudaMemcpyHostToDevice, c->stream));
-    const long long tot = (long long)nm * N;
-    for (int j = 0; j < c->n_digits; ++j) {
+    const long long tot = (long long)rows * N;
+    for (int j = 0; j < nd; ++j) {
         const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, c->n_q);
-        uint64_t *bj = key + ((size_t)j * 2 + 0) * nm * N;
-        uint64_t *aj = key + ((size_t)j * 2 + 1) * nm * N;
+        uint64_t *bj = key + ((size_t)j * 2 + 0) * rows * N;
+        uint64_t *aj = key + ((size_t)j * 2 + 1) * rows * N;
         ks_sample<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bj, aj, seed, ST_KEY_A + tag * 64 + j,
-                                                              ST_KEY_E + tag * 64 + j, c->log_n, nm, c->d_modq); ++c->launches;
-        int rc = ntt_fwd_launch(c, bj, 0, nm, 1, 0);
+                                                              ST_KEY_E + tag * 64 + j, c->log_n, rows, top, c->n_q,
+                                                              c->d_modq); ++c->launches;
+        int rc = ntt_fwd_launch(c, bj, 0, top + 1, 1, 0);
+        if (!rc) rc = ntt_fwd_launch(c, bj + (size_t)(top + 1) * N, c->n_q, c->n_p, 1, 0);
         if (rc) return rc;
         ks_finish<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bj, aj, c->d_sk, sprime, d_pmod, d0, d1, c->log_n,
-                                                              nm, c->d_modq); ++c->launches;
+                                                              rows, top, c->n_q, c->d_modq); ++c->launches;
     }
     HK_LAUNCH_CHECK(c, "make_ks_key");
     HK_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -206,7 +214,7 @@ int hk_keygen(hk_ctx *c, uint64_t seed) {
     const int N = c->n, nm = c->n_mod;
     cudaFree(c->d_sk);
     cudaFree(c->d_relin);
-    for (auto &kv : c->gal) cudaFree(kv.second);
+    for (auto &kv : c->gal) cudaFree(kv.second.p);
     c->gal.clear();
     c->d_sk = c->d_relin = nullptr;
     HK_CUDA(c, cudaMalloc(&c->d_sk, sizeof(uint64_t) * nm * N));
@@ -218,36 +226,47 @@ int hk_keygen(hk_ctx *c, uint64_t seed) {
     uint64_t *s2 = nullptr;
     HK_CUDA(c, cudaMalloc(&s2, sizeof(uint64_t) * nm * N));
     square_mod<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c->d_sk, s2, c->log_n, nm, c->d_modq); ++c->launches;
-    rc = make_ks_key(c, seed, 0, s2, c->d_relin);
+    rc = make_ks_key(c, seed, 0, s2, c->d_relin, c->n_q - 1);
     cudaFree(s2);
     if (rc) return rc;
     c->have_keys = true;
     return HK_OK;
 }
 
-int hk_has_galois_key(const hk_ctx *c, uint32_t g) { return c->gal.count(g) ? 1 : 0; }
+int hk_has_galois_key(const hk_ctx *c, uint32_t g) {
+    auto it = c->gal.find(g);
+    return it == c->gal.end() ? 0 : it->second.level + 1;
+}
 
-int hk_add_galois_keys(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n) {
+int hk_add_galois_keys_level(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n, int32_t level) {
     if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (level < 0 || level >= c->n_q) return hk_fail(c, HK_E_ARG, "galois key level %d out of range", level);
     const int N = c->n, nm = c->n_mod;
     const uint32_t M = 2u * (uint32_t)N;
     for (int i = 0; i < n; ++i) {
         const uint32_t g = gs[i];
         if ((g & 1u) == 0 || g >= M) return hk_fail(c, HK_E_ARG, "galois element %u invalid", g);
-        if (c->gal.count(g)) continue;
+        auto it = c->gal.find(g);
+        if (it != c->gal.end() && it->second.level >= level) continue;
+        const int rows = level + 1 + c->n_p, nd = level / c->alpha + 1;
         uint64_t *sg = nullptr, *key = nullptr;
         HK_CUDA(c, cudaMalloc(&sg, sizeof(uint64_t) * nm * N));
-        HK_CUDA(c, cudaMalloc(&key, sizeof(uint64_t) * hk_key_words(c, 1)));
+        HK_CUDA(c, cudaMalloc(&key, sizeof(uint64_t) * (size_t)nd * 2 * rows * N));
         int rc = automorph_launch(c, c->d_sk, sg, g, nm);
-        if (!rc) rc = make_ks_key(c, seed, 1 + (uint64_t)g, sg, key);
+        if (!rc) rc = make_ks_key(c, seed, 1 + (uint64_t)g, sg, key, level);
         cudaFree(sg);
         if (rc) {
             cudaFree(key);
             return rc;
         }
-        c->gal[g] = key;
+        if (it != c->gal.end()) cudaFree(it->second.p);  // grown to a higher level
+        c->gal[g] = GalKey{key, level, rows};
     }
     return HK_OK;
+}
+
+int hk_add_galois_keys(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n) {
+    return hk_add_galois_keys_level(c, seed, gs, n, c->n_q - 1);
 }
 
 int hk_export_key(hk_ctx *c, int32_t which, uint32_t g, uint64_t *out) {
@@ -255,7 +274,10 @@ int hk_export_key(hk_ctx *c, int32_t which, uint32_t g, uint64_t *out) {
     const uint64_t *src = nullptr;
     if (which == 0) src = c->d_sk;
     else if (which == 1) src = c->d_relin;
-    else if (c->gal.count(g)) src = c->gal[g];
+    else if (c->gal.count(g)) {
+        if (c->gal[g].level != c->n_q - 1) return hk_fail(c, HK_E_ARG, "galois key %u is level-truncated", g);
+        src = c->gal[g].p;
+    }
     if (!src) return hk_fail(c, HK_E_NOKEY, "no galois key for %u", g);
     HK_CUDA(c, cudaMemcpyAsync(out, src, sizeof(uint64_t) * hk_key_words(c, which == 0 ? 0 : 1),
                                cudaMemcpyDeviceToDevice, c->stream));

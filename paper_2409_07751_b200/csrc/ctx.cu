@@ -390,7 +390,7 @@ void hk_ctx_destroy(hk_ctx *c) {
     cudaFree(c->d_mqinv);
     cudaFree(c->d_sk);
     cudaFree(c->d_relin);
-    for (auto &kv : c->gal) cudaFree(kv.second);
+    for (auto &kv : c->gal) cudaFree(kv.second.p);
     cudaFree(c->ws);
     delete c;
 }

@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
 template <int ND>
 __global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
                                                 const uint64_t *__restrict__ dm, int alpha, int ne, int l, int n_q,
-                                                int nm, int log_n, int bb, const uint64_t *__restrict__ key,
+                                                int nm, int ksp0, int log_n, int bb, const uint64_t *__restrict__ key,
                                                 uint32_t g, uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1,
                                                 const double2 *__restrict__ fmod, long long BN) {
     using namespace ntt16;
@@ -260,13 +260,14 @@ __global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext
     const int b0 = (blockIdx.x / kblocks) * bb;
     const int t = blockIdx.y;
     const int m = t <= l ? t : n_q + (t - l - 1);
+    const int kr = t <= l ? t : ksp0 + (t - l - 1);  // key row: nm rows, specials from ksp0
     const double2 fm = fmod[m];
     const FpMod M{fm.x, fm.y};
     const int ks = g == 1u ? k : (int)auto_src((uint32_t)k, g, log_n);
     double w0[ND], v0[ND], w1[ND], v1[ND];
 #pragma unroll
     for (int j = 0; j < ND; ++j) {
-        const uint64_t *kj = key + ((size_t)j * 2 * nm + m) * N;
+        const uint64_t *kj = key + ((size_t)j * 2 * nm + kr) * N;
         w0[j] = u2d(kj[k]);
         w1[j] = u2d(kj[(size_t)nm * N + k]);
         v0[j] = __dmul_rn(w0[j], M.qinv);
@@ -741,16 +742,24 @@ static int ks_modup(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb
     return HK_OK;
 }
 
-static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, const uint64_t *key, uint32_t g,
+// key layout: rows = key level + 1 + K, specials from row (key level + 1)
+struct KeyRef {
+    const uint64_t *p;
+    int level;
+};
+
+static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, KeyRef key, uint32_t g,
                  const uint64_t *dm = nullptr) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    if (key.level < l) return hk_fail(c, HK_E_NOKEY, "key for element %u serves level %d < %d", g, key.level, l);
+    const int krows = key.level + 1 + c->n_p;
     const long long BN = (long long)B * c->n;
     const int bb = B % 4 == 0 ? 4 : B % 2 == 0 ? 2 : 1;
     const int ipt = std::min(256, c->n);
     const dim3 ipg((unsigned)((c->n / ipt) * (B / bb)), (unsigned)ne);
 #define HK_KEY_IP(ND)                                                                                          \
-    k_key_ip<ND><<<ipg, ipt, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, c->n_mod, c->log_n, bb, key, \
-                                             g, kb.acc, kb.acc + (size_t)ne * BN, c->d_fmod, BN)
+    k_key_ip<ND><<<ipg, ipt, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, krows, key.level + 1,     \
+                                             c->log_n, bb, key.p, g, kb.acc, kb.acc + (size_t)ne * BN, c->d_fmod, BN)
     switch (nd) {
         case 1: HK_KEY_IP(1); break;
         case 2: HK_KEY_IP(2); break;
@@ -857,7 +866,9 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
         if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
     }
     // own-digit limbs of d2 are formed inside the key IP from a1 (.) b1
-    if ((rc = ks_ip(c, a + (size_t)(la + 1) * BN, l, B, kb, c->d_relin, 1u, b + (size_t)(lb + 1) * BN))) return rc;
+    if ((rc = ks_ip(c, a + (size_t)(la + 1) * BN, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u,
+                    b + (size_t)(lb + 1) * BN)))
+        return rc;
     const ConvTable &Tm = c->mdrs[l];
     const ulonglong2 *mqinv = c->d_mqinv + (size_t)l * c->n_q;
     for (int p = 0; p < 2; ++p) {
@@ -877,7 +888,7 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
 
 // Key switch d under n keys (hoisted ModUp); for key r writes
 //   out0[r] = ks0 (+ sigma_g(add0) if add0) and out1[r] = ks1, each [l+1][B][N].
-static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const uint64_t *const *keys,
+static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const KeyRef *keys,
                      const uint32_t *gal, uint64_t *const *out0, uint64_t *const *out1, const uint64_t *add0,
                      uint64_t *scratch) {
     const KsBufs kb = ks_bufs(c, l, B, scratch);
@@ -1030,7 +1041,7 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");
     int rc = ks_modup(c, d + 2 * pl, l, B, kb);
-    if (!rc) rc = ks_ip(c, d + 2 * pl, l, B, kb, c->d_relin, 1u);
+    if (!rc) rc = ks_ip(c, d + 2 * pl, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u);
     const int ne = l + 1 + c->n_p;
     if (!rc) rc = ks_moddown_rescale(c, kb.acc, d, l, B, kb, out);
     if (!rc) rc = ks_moddown_rescale(c, kb.acc + (size_t)ne * BN, d + pl, l, B, kb, out + (size_t)l * BN);
@@ -1042,13 +1053,15 @@ int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *
     if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
     if (la < 0 || la >= c->n_q) return hk_fail(c, HK_E_ARG, "rotate: level");
     if (n < 1) return HK_OK;
-    std::vector<const uint64_t *> keys(n);
+    std::vector<KeyRef> keys(n);
     std::vector<uint64_t *> o0(n), o1(n);
     const long long pl = (long long)(la + 1) * B * c->n;
     for (int i = 0; i < n; ++i) {
         auto it = c->gal.find(gs[i]);
         if (it == c->gal.end()) return hk_fail(c, HK_E_NOKEY, "no galois key for element %u", gs[i]);
-        keys[i] = it->second;
+        if (it->second.level < la)
+            return hk_fail(c, HK_E_NOKEY, "galois key %u serves level %d < %d", gs[i], it->second.level, la);
+        keys[i] = KeyRef{it->second.p, it->second.level};
         o0[i] = outs[i];
         o1[i] = outs[i] + pl;
     }

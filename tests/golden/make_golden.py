@@ -7,10 +7,14 @@ Outputs
   tests/golden/c1.npz      c1 model (built with the reference's classes from the
                            same seeded draws), inputs, reference mirrored and
                            exact outputs, per-layer logical op counts
+  tests/golden/c3.npz, c4.npz  first samples of c3 / c4 with reference outputs
+  tests/golden/c5.npz      c5 [3072,128,10] first 2 samples; the reference's HE
+                           program needs 33792 packed slots, so its counts are
+                           taken at slot_count 65536 (N = 2^17)
   tests/golden/small.npz   small multi-layer random models + inputs + outputs
   tests/golden/backend.json known-answer vectors of the backend contract
 
-Run:  python tests/golden/make_golden.py
+Run:  python tests/golden/make_golden.py [c5]
 """
 
 import json
@@ -86,8 +90,37 @@ def model_arrays(prefix, model):
     return d
 
 
+def c5_fixture(cs):
+    """c5 [3072,128,10] G=5 k=3 [-1,1], explicit R; 32 x per-channel-standardised
+    U[0,1]^(32x32x3) in HWC raster; first 2 samples kept."""
+    rng = np.random.default_rng(1)
+    x = rng.uniform(0.0, 1.0, (32, 32, 32, 3))
+    mu = x.mean(axis=(0, 1, 2), keepdims=True)
+    sd = x.std(axis=(0, 1, 2), keepdims=True)
+    X5 = ((x - mu) / sd).reshape(32, 3072)
+    rg5 = []
+    m5 = build_ref_model((3072, 128, 10), 5, 3, -1.0, 1.0, 0.02, 10, X5, (32, 32, 3), explicit_R=True,
+                         ranges=rg5)
+    Xs = X5[:2]
+    plan = ri.plan_model(m5, ri.PipelineConfig())
+    be = CleartextBackend(BackendConfig(slot_count=65536, depth_budget=plan.total))
+    out, stats = ri.model_forward_he(m5, ri.encrypt_input(Xs[0], m5, be), ri.PipelineConfig())
+    counts = [{"rotations": st.rotations, "ct_mults": st.ct_mults, "pt_mults": st.pt_mults,
+               "adds": st.adds, "depth_consumed": st.depth_consumed} for st in stats.per_layer]
+    np.savez_compressed(os.path.join(HERE, "c5.npz"), X=Xs,
+                        mirrored=np.stack([rm.model_forward_plain(m5, x, "mirrored", cs, "lazy") for x in Xs]),
+                        exact=np.stack([rm.model_forward_plain(m5, x, "exact") for x in Xs]),
+                        he_cleartext_s65536=np.asarray(out.slots[:10]),
+                        ranges=np.array(rg5), plan_total=np.array(plan.total),
+                        counts=np.array(json.dumps(counts)))
+    print("c5 plan depth", plan.total, "counts", counts)
+
+
 def main():
     cs = comparator_json()
+    if sys.argv[1:] == ["c5"]:
+        c5_fixture(cs)
+        return
     # ---- c1
     rng = np.random.default_rng(1)
     X = rng.uniform(-1.0, 1.0, (128, 2))
@@ -151,6 +184,7 @@ def main():
                           "degrees": [s.degree for s in cs.stages]}}
     with open(os.path.join(HERE, "backend.json"), "w") as fh:
         json.dump(kat, fh, indent=1)
+    c5_fixture(cs)
     print("wrote fixtures; c1 plan depth", plan.total, "counts", counts)
 
 

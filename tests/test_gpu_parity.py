@@ -119,3 +119,24 @@ def test_microbench_params_bitexact(gpu_lib):
     ga, oa = g.encrypt(x), o.encrypt(x)
     _same(g, o, g.mul(ga, ga), o.mul(oa, oa), "mul")
     _same(g, o, g.rotate(ga, 1 << 14), o.rotate(oa, 1 << 14), "rotate")
+
+
+@pytest.mark.parametrize("log_n,depth", [(13, 5), (16, 4)])
+def test_level_truncated_galois_keys(gpu_lib, log_n, depth):
+    """Galois keys are stored truncated to the highest level asked for and
+    regrown on demand (hk_add_galois_keys_level); the oracle keeps full keys.
+    Rotations at a low level (truncated key), then at a higher level (regrown
+    key), then hoisted, must stay bit-exact."""
+    g, o, p = _pair(log_n, depth)
+    S = p.slot_count
+    x = np.random.default_rng(11).uniform(-1, 1, (2, S))
+    ga, oa = g.encrypt(x), o.encrypt(x)
+    gl, ol = g.mul(g.mul(ga, 0.5), 2.0), o.mul(o.mul(oa, 0.5), 2.0)  # level depth - 2
+    _same(g, o, g.rotate(gl, 5), o.rotate(ol, 5), "rotate at low level")
+    elt = galois_element(5, S)
+    assert g.engine.lib.hk_has_galois_key(g.engine.ctx, elt) == gl.level + 1
+    _same(g, o, g.rotate(ga, 5), o.rotate(oa, 5), "rotate at top level (regrown key)")
+    assert g.engine.lib.hk_has_galois_key(g.engine.ctx, elt) == depth + 1
+    for cg, co in zip(g.rotate_many(gl, [5, 7, -2]), o.rotate_many(ol, [5, 7, -2])):
+        _same(g, o, cg, co, "hoisted, mixed key levels")
+    np.testing.assert_allclose(g.decrypt(g.rotate(gl, 5)), np.roll(x, -5, axis=1), atol=1e-6)
