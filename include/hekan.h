@@ -98,6 +98,15 @@ int hk_ntt_inv(hk_ctx *ctx, uint64_t *buf, int32_t limb0, int32_t n_limbs, int32
  * slots: f64 [batch][S] (real payloads). pt: u64 [level+1][batch][N], NTT. */
 int hk_encode(hk_ctx *ctx, const double *slots, int32_t batch, int32_t level,
               double scale, uint64_t *pt);
+/* BSGS diagonals of one giant-step block, generated and encoded in one call
+ * (inference.py:166-176, the diagonal gather + np.roll + encode per diagonal):
+ * diagonal v in [0, count) has slot s = W~[r][(r + base + v) mod m], r = (s - base)
+ * mod S, zero for r >= m, with W~ the n_o x n_in row-major matrix `W` zero-padded
+ * to m x m (requires base + count <= m <= S). W lives where the engine's buffers
+ * live (device for the GPU, host for the oracle). pt: u64 [level+1][count][N],
+ * identical to hk_encode of the same slot vectors. */
+int hk_encode_diagonals(hk_ctx *ctx, const double *W, int32_t n_o, int32_t n_in, int32_t m, int32_t base,
+                        int32_t count, int32_t level, double scale, uint64_t *pt);
 /* Constant c at scale: per-limb residues of round(c*scale) for limbs 0..level. */
 int hk_encode_const(hk_ctx *ctx, double c, int32_t level, double scale, uint64_t *res);
 
@@ -146,10 +155,12 @@ int hk_rotate_hoisted(hk_ctx *ctx, const uint64_t *a, int32_t la,
 
 /* ---- fused BSGS giant-step block (inference.py:166-178): for one giant step
  * out = sum_i pt_i (*) babies_i, accumulated lazily, then ONE rescale.
- * babies[i]: ct at level la; pts[i]: plaintext at level >= la (pt_batch 1).
+ * babies[i]: ct at level la; pts[i]: plaintext at level >= la (pt_batch 1) whose
+ * limb l starts at pts[i] + l * pt_stride * N (1 for a plain [lp+1][1][N]
+ * plaintext; `count` for diagonal v of hk_encode_diagonals, pts[v] = pt + v * N).
  * Logically this is n mul_pt + (n-1) add; out is at level la-1. */
 int hk_mac_plain(hk_ctx *ctx, const uint64_t *const *babies, const uint64_t *const *pts,
-                 int32_t n, int32_t la, int32_t lp, uint64_t *out, int32_t batch);
+                 int32_t n, int32_t la, int32_t lp, int32_t pt_stride, uint64_t *out, int32_t batch);
 
 /* ---- introspection */
 int32_t hk_version(void);

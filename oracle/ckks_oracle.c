@@ -373,6 +373,31 @@ int hk_encode(hk_ctx *c, const double *slots, int32_t B, int32_t level, double s
     return hk_ntt_fwd(c, pt, 0, nl, B);
 }
 
+/* BSGS diagonals of one giant-step block (inference.py:166-176): slot s of diagonal v
+ * is W~[r][(r + base + v) mod m] with r = (s - base) mod S (zero for r >= m), W~ the
+ * row-major n_o x n_in matrix zero-padded to m x m; encoded like hk_encode. */
+int hk_encode_diagonals(hk_ctx *c, const double *W, int32_t n_o, int32_t n_in, int32_t m, int32_t base,
+                        int32_t count, int32_t level, double scale, uint64_t *pt) {
+    if (level < 0 || level >= c->n_q || count < 0) return fail(c, HK_E_ARG, "encode_diagonals: level/count");
+    if (n_o < 1 || n_in < 1 || m < n_o || m < n_in || m > c->slots || base < 0 || base + count > m)
+        return fail(c, HK_E_ARG, "encode_diagonals: shape (%d x %d, m %d, base %d, count %d)", n_o, n_in, m, base,
+                    count);
+    if (count == 0) return HK_OK;
+    const int S = c->slots;
+    double *slots = calloc((size_t)count * S, sizeof(double));
+    for (int v = 0; v < count; ++v)
+        for (int s = 0; s < S; ++s) {
+            const int r = ((s - base) % S + S) % S;
+            if (r < m && r < n_o) {
+                const int col = (int)(((long long)r + base + v) % m);
+                if (col < n_in) slots[(size_t)v * S + s] = W[(size_t)r * n_in + col];
+            }
+        }
+    const int rc = hk_encode(c, slots, count, level, scale, pt);
+    free(slots);
+    return rc;
+}
+
 int hk_encode_const(hk_ctx *c, double v, int32_t level, double scale, uint64_t *res) {
     if (level < 0 || level >= c->n_q) return fail(c, HK_E_ARG, "encode_const: level out of range");
     const double x = v * scale;
@@ -1020,8 +1045,8 @@ int hk_rotate(hk_ctx *c, const uint64_t *a, int32_t la, uint32_t g, uint64_t *ou
 }
 
 int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const *pts, int32_t n,
-                 int32_t la, int32_t lp, uint64_t *out, int32_t B) {
-    if (la < 0 || la >= c->n_q || lp < la || n < 1) return fail(c, HK_E_ARG, "mac_plain: args");
+                 int32_t la, int32_t lp, int32_t pt_stride, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q || lp < la || n < 1 || pt_stride < 1) return fail(c, HK_E_ARG, "mac_plain: args");
     if (la < 1) return fail(c, HK_E_DEPTH, "multiplication at level %d", la);
     const int N = c->n;
     const size_t poly = (size_t)(la + 1) * B * N;
@@ -1033,7 +1058,7 @@ int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const
                 uint64_t *z = t + p * poly + ((size_t)l * B + b) * N;
                 for (int i = 0; i < n; ++i) {
                     const uint64_t *x = babies[i] + p * poly + ((size_t)l * B + b) * N;
-                    const uint64_t *y = pts[i] + (size_t)l * N;
+                    const uint64_t *y = pts[i] + (size_t)l * pt_stride * N;
                     for (int k = 0; k < N; ++k) z[k] = addmod(z[k], mulmod(x[k], y[k], q), q);
                 }
             }

@@ -204,6 +204,7 @@ class HeBackend:
         self.n = params.n
         self._enc_counter = itertools.count()
         self._pt_cache: dict = {}
+        self._mat_cache: dict = {}
         self._pt_cache_bytes = 0
         self.pt_cache_limit = 8 << 30
         self.engine.call("hk_keygen", C.c_uint64(self._seed("keys")))
@@ -435,7 +436,52 @@ class HeBackend:
             raise ValueError("mac_plain operands must share one level")
         out = eng.alloc_u64(2 * level * B * self.n)
         eng.call("hk_mac_plain", eng.addr_array([x.data for x in babies]), eng.addr_array(pts),
-                 n_terms, level, level, eng.addr(out), B)
+                 n_terms, level, level, 1, eng.addr(out), B)
+        self.counter.pt_mults += n_terms
+        self.counter.adds += n_terms - 1
+        return self._wrap(out, level - 1, B, a0.batched)
+
+    # ------------------------------------------------------------------
+    # BSGS diagonals on the device
+    # ------------------------------------------------------------------
+
+    def device_matrix(self, W: np.ndarray):
+        """Engine-resident copy of a BSGS weight matrix (row-major f64), cached
+        per content; the diagonals are generated from it on the device."""
+        W = np.ascontiguousarray(W, dtype=np.float64)
+        key = (hashlib.blake2b(W.view(np.uint8), digest_size=16).digest(), W.shape)
+        hit = self._mat_cache.get(key)
+        if hit is None:
+            if len(self._mat_cache) > 64:
+                self._mat_cache.clear()
+            hit = self._mat_cache[key] = self.engine.put_f64(W)
+        return hit
+
+    def bsgs_block(self, babies, Wdev, shape, m: int, base: int) -> CipherText:
+        """One giant-step block of bsgs_matvec: diagonals base..base+len(babies)-1
+        of the m x m zero-padded matrix, rolled by `base`, generated and encoded
+        on the device at the babies' level, then the fused MAC with one rescale.
+        Counts exactly like mac_plain (len(babies) pt_mults, len-1 adds)."""
+        n_terms = len(babies)
+        if n_terms == 0:
+            raise LengthMismatch("bsgs_block needs babies")
+        a0 = babies[0]
+        for x in babies:
+            self._check_ours(x)
+            if x.batch != a0.batch or x.level != a0.level:
+                raise LengthMismatch("bsgs_block operands must share batch and level")
+        level = a0.level
+        if level < 1:
+            raise DepthExhausted(f"multiplication at level {level}")
+        eng, B, n = self.engine, a0.batch, self.n
+        pt = eng.alloc_u64((level + 1) * n_terms * n)
+        eng.call("hk_encode_diagonals", eng.addr(Wdev), int(shape[0]), int(shape[1]), int(m), int(base),
+                 n_terms, level, self.params.pt_mult_scale(level), eng.addr(pt))
+        p0 = eng.addr(pt)
+        ptrs = (C.c_void_p * n_terms)(*[p0 + v * n * 8 for v in range(n_terms)])
+        out = eng.alloc_u64(2 * level * B * n)
+        eng.call("hk_mac_plain", eng.addr_array([x.data for x in babies]), ptrs, n_terms, level, level,
+                 n_terms, eng.addr(out), B)
         self.counter.pt_mults += n_terms
         self.counter.adds += n_terms - 1
         return self._wrap(out, level - 1, B, a0.batched)

@@ -87,7 +87,42 @@ __global__ void round_to_limbs(const double2 *__restrict__ w, int S, int log_n, 
     }
 }
 
+// BSGS diagonal v of one giant-step block, rolled by `base` (inference.py:172-176):
+// slot s holds d_v[(s - base) mod S], d_v[r] = W~[r][(r + base + v) mod m] for r < m,
+// W~ = W (n_o x n_in, row-major) zero-padded to m x m
+__global__ void gen_diagonals(const double *__restrict__ W, int n_o, int n_in, int m, int base, int S,
+                              double2 *__restrict__ a, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;
+    const long long v = gid / S;
+    const int s = (int)(gid - v * S);
+    int r = s - base % S;
+    if (r < 0) r += S;
+    double val = 0.0;
+    if (r < m && r < n_o) {
+        const int col = (int)(((long long)r + base + v) % m);
+        if (col < n_in) val = W[(long long)r * n_in + col];
+    }
+    a[gid] = make_double2(val, 0.0);
+}
+
 }  // namespace
+
+// slots already in a (B x S complex, real parts) -> pt [level+1][B][N], NTT domain
+static int encode_loaded(hk_ctx *c, double2 *a, int B, int level, double scale, uint64_t *pt) {
+    const int S = c->slots, M = 2 * c->n, bits = c->log_n - 1;
+    const long long all = (long long)B * S, half = (long long)B * (S / 2);
+    double2 *b2 = a + all;
+    for (int len = S; len >= 2; len >>= 1) {
+        fft_inv_stage<<<hk_grid(half, 256), 256, 0, c->stream>>>(a, S, len, M, c->d_zeta, c->d_rot_group, half);
+        ++c->launches;
+    }
+    bitrev_copy<<<hk_grid(all, 256), 256, 0, c->stream>>>(a, b2, S, bits, all); ++c->launches;
+    round_to_limbs<<<hk_grid(all, 256), 256, 0, c->stream>>>(b2, S, c->log_n, 1.0 / (double)S, scale, level + 1,
+                                                             B, c->d_modq, pt, all); ++c->launches;
+    HK_LAUNCH_CHECK(c, "encode");
+    return ntt_fwd_launch(c, pt, 0, level + 1, B, 0);
+}
 
 // shared with crypt.cu: coefficient-domain values (as doubles / scale) -> slots
 int hk_decode_launch(hk_ctx *c, double2 *w, double2 *tmp, int B, double *slots);
@@ -114,21 +149,25 @@ int hk_decode_launch(hk_ctx *c, double2 *w, double2 *tmp, int B, double *slots) 
 extern "C" int hk_encode(hk_ctx *c, const double *slots, int32_t B, int32_t level, double scale, uint64_t *pt) {
     if (level < 0 || level >= c->n_q || B < 0) return hk_fail(c, HK_E_ARG, "encode: level %d out of range", level);
     if (B == 0) return HK_OK;
-    const int S = c->slots, M = 2 * c->n, bits = c->log_n - 1;
-    const long long all = (long long)B * S, half = (long long)B * (S / 2);
+    const long long all = (long long)B * c->slots;
     double2 *a = (double2 *)hk_workspace(c, sizeof(double2) * 2 * all);
     if (!a) return hk_fail(c, HK_E_NOMEM, "encode workspace");
-    double2 *b2 = a + all;
     load_slots<<<hk_grid(all, 256), 256, 0, c->stream>>>(slots, a, all); ++c->launches;
-    for (int len = S; len >= 2; len >>= 1) {
-        fft_inv_stage<<<hk_grid(half, 256), 256, 0, c->stream>>>(a, S, len, M, c->d_zeta, c->d_rot_group, half);
-        ++c->launches;
-    }
-    bitrev_copy<<<hk_grid(all, 256), 256, 0, c->stream>>>(a, b2, S, bits, all); ++c->launches;
-    round_to_limbs<<<hk_grid(all, 256), 256, 0, c->stream>>>(b2, S, c->log_n, 1.0 / (double)S, scale, level + 1,
-                                                             B, c->d_modq, pt, all); ++c->launches;
-    HK_LAUNCH_CHECK(c, "encode");
-    return ntt_fwd_launch(c, pt, 0, level + 1, B, 0);
+    return encode_loaded(c, a, B, level, scale, pt);
+}
+
+extern "C" int hk_encode_diagonals(hk_ctx *c, const double *W, int32_t n_o, int32_t n_in, int32_t m, int32_t base,
+                                   int32_t count, int32_t level, double scale, uint64_t *pt) {
+    if (level < 0 || level >= c->n_q || count < 0) return hk_fail(c, HK_E_ARG, "encode_diagonals: level/count");
+    if (n_o < 1 || n_in < 1 || m < n_o || m < n_in || m > c->slots || base < 0 || base + count > m)
+        return hk_fail(c, HK_E_ARG, "encode_diagonals: shape (%d x %d, m %d, base %d, count %d)", n_o, n_in, m, base,
+                       count);
+    if (count == 0) return HK_OK;
+    const long long all = (long long)count * c->slots;
+    double2 *a = (double2 *)hk_workspace(c, sizeof(double2) * 2 * all);
+    if (!a) return hk_fail(c, HK_E_NOMEM, "encode_diagonals workspace");
+    gen_diagonals<<<hk_grid(all, 256), 256, 0, c->stream>>>(W, n_o, n_in, m, base, c->slots, a, all); ++c->launches;
+    return encode_loaded(c, a, count, level, scale, pt);
 }
 
 extern "C" int hk_encode_const(hk_ctx *c, double v, int32_t level, double scale, uint64_t *res) {

@@ -16,7 +16,7 @@ int automorph_launch(hk_ctx *c, const uint64_t *in, uint64_t *out, uint32_t g, l
 
 namespace {
 
-constexpr int kMacMax = 64;     // operands per mac_plain launch
+constexpr int kMacMax = 192;    // operands per mac_plain launch (BSGS block: c4 80, c5 157)
 
 struct Residues { uint64_t v[HK_MAX_MOD]; };
 struct PtrList { const uint64_t *p[kMacMax]; };
@@ -86,12 +86,12 @@ __global__ void k_mul_const(const uint64_t *__restrict__ a, int la, Residues r, 
 }
 
 // out = sum_i babies[i] (.) pts[i], both polys; `init` adds the previous out
-__global__ void k_mac(PtrList babies, PtrList pts, int n, int la, uint64_t *__restrict__ out, long long BN,
+__global__ void k_mac(PtrList babies, PtrList pts, int n, int la, int ps, uint64_t *__restrict__ out, long long BN,
                       int log_n, int init, const ModQ *__restrict__ mq) {
     ELEM_INDEX
     const int N = 1 << log_n;
     const long long o = ((long long)p * (la + 1) + l) * BN + e;
-    const long long pe = (long long)l * N + (e & (N - 1));
+    const long long pe = (long long)l * ps * N + (e & (N - 1));
     Acc3 acc;
     acc3_zero(acc);
     if (init) acc.s0 = out[o];
@@ -352,6 +352,7 @@ struct RsSrc {
     const uint64_t *a2;
     const uint64_t *pt;
     int la, pb, n, log_n;
+    int ps;  // plaintext limb stride in units of N (SRC_MAC)
     long long BN;
     const ModQ *mq;
     const double2 *fmod;  // {q, 1/q} per prime
@@ -372,7 +373,7 @@ struct RsSrc {
         }
         Acc3 acc;
         acc3_zero(acc);
-        const long long pe = ((long long)l << log_n) + idx;
+        const long long pe = (((long long)l * ps) << log_n) + idx;
         for (int i = 0; i < n; ++i) acc3_mac(acc, babies.p[i][o], pts.p[i][pe]);
         return acc3_reduce(acc, mq[l]);
     }
@@ -678,6 +679,7 @@ static RsSrc<KIND> make_src(hk_ctx *c, const uint64_t *a, int la, int B) {
     s.BN = (long long)B * c->n;
     s.mq = c->d_modq;
     s.fmod = c->d_fmod;
+    s.ps = 1;
     return s;
 }
 
@@ -996,8 +998,8 @@ int hk_mul_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
 }
 
 int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const *pts, int32_t n, int32_t la,
-                 int32_t lp, uint64_t *out, int32_t B) {
-    if (la < 0 || la >= c->n_q || lp < la || n < 1) return hk_fail(c, HK_E_ARG, "mac_plain: args");
+                 int32_t lp, int32_t pt_stride, uint64_t *out, int32_t B) {
+    if (la < 0 || la >= c->n_q || lp < la || n < 1 || pt_stride < 1) return hk_fail(c, HK_E_ARG, "mac_plain: args");
     if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
     if (c->log_n == ntt16::kLogN && n <= kMacMax) {
@@ -1005,6 +1007,7 @@ int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const
         if (!ws) return hk_fail(c, HK_E_NOMEM, "mac_plain workspace");
         RsSrc<SRC_MAC> src = make_src<SRC_MAC>(c, babies[0], la, B);
         src.n = n;
+        src.ps = pt_stride;
         for (int i = 0; i < n; ++i) {
             src.babies.p[i] = babies[i];
             src.pts.p[i] = pts[i];
@@ -1020,7 +1023,9 @@ int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const
             bl.p[i] = babies[s + i];
             pl.p[i] = pts[s + i];
         }
-        k_mac<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(bl, pl, cnt, la, ws, BN, c->log_n, s > 0, c->d_modq); ++c->launches;
+        k_mac<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(bl, pl, cnt, la, pt_stride, ws, BN, c->log_n, s > 0,
+                                                           c->d_modq);
+        ++c->launches;
     }
     HK_LAUNCH_CHECK(c, "mac_plain");
     return rescale_launch(c, ws, la, B, out, ws + tot);
