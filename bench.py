@@ -2,7 +2,7 @@
 """Encrypted-KAN throughput on B200 (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference]
-                  [--config c1] [--batch B] [--log-n 16]
+                  [--config c1|c3|c4|c5] [--batch B] [--chunk C] [--log-n 16]
 
 A step = one encrypted forward pass (`model_forward_he`) of the config's KAN
 over one batch of B ciphertexts (one sample per ciphertext, as
@@ -176,7 +176,7 @@ def run_product(args):
     del outs
     err = None
     gpath = os.path.join(ROOT, "tests", "golden", f"{args.config}.npz")
-    if os.path.exists(gpath) and args.log_n == 16:
+    if os.path.exists(gpath) and args.log_n == (17 if args.config == "c5" else 16):
         gold = np.load(gpath)["mirrored"]
         n = min(B, gold.shape[0])
         err = float(np.max(np.abs(dec[:n] - gold[:n])))
@@ -256,7 +256,8 @@ def run_product(args):
                                f"{B} ciphertexts/GPU in chunks of {chunk}, RNS-CKKS N=2^{args.log_n} L={depth} "
                                f"dnum={params.dnum} alpha={params.alpha}",
                    "global_batch": total_inf, "parallelism": f"dp{world} (ciphertext sharding)",
-                   "l2": "inputs 4.7 GB/GPU >> 126 MB L2 (no flush needed)"},
+                   "l2": f"inputs {B * 2 * (depth + 1) * params.n * 8 / 1e9:.1f} GB/GPU >> 126 MB L2 "
+                         "(no flush needed)"},
         "e2e": {"value": round(total_inf / (e2e_ms / 1e3), 4), "unit": "inferences/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "encrypt_input + model_forward_he + decrypt, host slots in/out"},
@@ -274,7 +275,11 @@ def run_product(args):
         torch.cuda.empty_cache()
         line["c2_microbench"] = c2_microbench(local)
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
+        if args.log_n > 16:
+            line["cpu_baseline"] = {"skipped": "oracle setup at N=2^17 generates every Galois key on the "
+                                               "CPU (hundreds of keys, many minutes); run c1 for the baseline"}
+        else:
+            line["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
     print(json.dumps(line))
 
 
@@ -592,12 +597,18 @@ def main():
     ap.add_argument("--impl", choices=("product", "reference"), default="product")
     ap.add_argument("--config", default="c1")
     ap.add_argument("--batch", type=int, default=0)
-    ap.add_argument("--chunk", type=int, default=32, help="ciphertexts per batched launch")
-    ap.add_argument("--log-n", type=int, default=16)
+    ap.add_argument("--chunk", type=int, default=None,
+                    help="ciphertexts per batched launch (default 32; 8 for c5 at N=2^17)")
+    ap.add_argument("--log-n", type=int, default=None,
+                    help="ring degree (default 16; 17 for c5, whose 33792 packed slots need S=2^16)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the config-2 primitive microbench")
     args = ap.parse_args()
+    if args.log_n is None:
+        args.log_n = 17 if args.config == "c5" else 16
+    if args.chunk is None:
+        args.chunk = 8 if args.log_n > 16 else 32
     if args.impl == "reference":
         run_reference(args)
     else:

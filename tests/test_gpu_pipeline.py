@@ -134,3 +134,29 @@ def test_c4_full_ring_degree(gpu_lib):
     print(f"c4: |dec - exact-arithmetic twin| = {err_twin:.3g}, |dec - reference mirrored| = {err_ref:.3g}")
     assert err_twin < 1e-4
     assert stats.to_json()["total"]["rotations"] == 287
+
+
+def test_c5_ring_2e17(gpu_lib):
+    """c5 [3072,128,10]: 33792 repeat-packed slots need S = 2^16, i.e. N = 2^17
+    (the reference itself raises PackingOverflow at its 2^15 slots; its program
+    runs at slot_count 65536, tests/golden/make_golden.py). Decrypted outputs vs
+    the reference's mirrored forward and the exact-arithmetic twin, and the
+    reference's per-layer op counts (Chebyshev basis: +32 adds per layer)."""
+    g_ = np.load(os.path.join(GOLD, "c5.npz"))
+    _, model, X = configs.workload("c5", batch=2)
+    depth = int(g_["plan_total"])
+    assert inf.plan_model(model, inf.PipelineConfig()).total == depth
+    be = _gpu(kan_params(depth, log_n=17), depth)
+    out, stats = inf.model_forward_he(model, inf.encrypt_input(X[:2], model, be), inf.PipelineConfig())
+    dec = be.decrypt(out)[:, :10]
+    err_twin = np.abs(dec - _twin(model, X[:2])).max()
+    err_ref = np.abs(dec - g_["mirrored"][:2]).max()
+    print(f"c5: |dec - twin| = {err_twin:.3g}, |dec - reference mirrored| = {err_ref:.3g}")
+    assert err_twin < 1e-4 and err_ref < 1e-4
+    ref = json.loads(str(g_["counts"]))
+    for ours, theirs in zip(stats.per_layer, ref):
+        assert ours.rotations == theirs["rotations"]
+        assert ours.ct_mults == theirs["ct_mults"]
+        assert ours.pt_mults == theirs["pt_mults"]
+        assert ours.adds == theirs["adds"] + 32
+        assert ours.depth_consumed == theirs["depth_consumed"]

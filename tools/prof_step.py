@@ -1,6 +1,8 @@
 """One c1 forward pass over B ciphertexts (after a warm pass that builds keys
 and plaintext caches) — for ncu launch lists of the real step mix."""
 import argparse
+
+import numpy as np
 import os
 import sys
 
@@ -12,10 +14,14 @@ from paper_2409_07751_b200.params import kan_params  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=32)
 ap.add_argument("--passes", type=int, default=2)
+ap.add_argument("--config", default="c1")
+ap.add_argument("--log-n", type=int, default=16)
 args = ap.parse_args()
-_, model, X = configs.workload("c1", batch=args.batch)
-p = kan_params(36)
-be = make_backend(BackendConfig(slot_count=p.slot_count, depth_budget=36), params=p)
+_, model, X = configs.workload(args.config, batch=args.batch)
+X = X[:args.batch] if X.shape[0] >= args.batch else np.resize(X, (args.batch, X.shape[1]))
+depth = inf.plan_model(model, inf.PipelineConfig()).total
+p = kan_params(depth, log_n=args.log_n)
+be = make_backend(BackendConfig(slot_count=p.slot_count, depth_budget=depth), params=p)
 ct = inf.encrypt_input(X, model, be)
 for _ in range(args.passes):
     out, _ = inf.model_forward_he(model, ct, inf.PipelineConfig())
