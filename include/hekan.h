@@ -98,15 +98,16 @@ int hk_ntt_inv(hk_ctx *ctx, uint64_t *buf, int32_t limb0, int32_t n_limbs, int32
  * slots: f64 [batch][S] (real payloads). pt: u64 [level+1][batch][N], NTT. */
 int hk_encode(hk_ctx *ctx, const double *slots, int32_t batch, int32_t level,
               double scale, uint64_t *pt);
-/* BSGS diagonals of one giant-step block, generated and encoded in one call
- * (inference.py:166-176, the diagonal gather + np.roll + encode per diagonal):
- * diagonal v in [0, count) has slot s = W~[r][(r + base + v) mod m], r = (s - base)
- * mod S, zero for r >= m, with W~ the n_o x n_in row-major matrix `W` zero-padded
- * to m x m (requires base + count <= m <= S). W lives where the engine's buffers
- * live (device for the GPU, host for the oracle). pt: u64 [level+1][count][N],
- * identical to hk_encode of the same slot vectors. */
+/* BSGS diagonals of consecutive giant-step blocks of nb diagonals, generated and
+ * encoded in one call (inference.py:166-176, the diagonal gather + np.roll + encode
+ * per diagonal): diagonal v in [0, count) has slot s = W~[r][(r + base + v) mod m],
+ * r = (s - rb) mod S with rb = base + (v / nb) * nb (its block's roll), zero for
+ * r >= m, W~ the n_o x n_in row-major matrix `W` zero-padded to m x m (requires
+ * base + count <= m <= S). W lives where the engine's buffers live (device for the
+ * GPU, host for the oracle). pt: u64 [level+1][count][N], identical to hk_encode
+ * of the same slot vectors. */
 int hk_encode_diagonals(hk_ctx *ctx, const double *W, int32_t n_o, int32_t n_in, int32_t m, int32_t base,
-                        int32_t count, int32_t level, double scale, uint64_t *pt);
+                        int32_t count, int32_t nb, int32_t level, double scale, uint64_t *pt);
 /* Constant c at scale: per-limb residues of round(c*scale) for limbs 0..level. */
 int hk_encode_const(hk_ctx *ctx, double c, int32_t level, double scale, uint64_t *res);
 
@@ -161,6 +162,14 @@ int hk_rotate_hoisted(hk_ctx *ctx, const uint64_t *a, int32_t la,
  * Logically this is n mul_pt + (n-1) add; out is at level la-1. */
 int hk_mac_plain(hk_ctx *ctx, const uint64_t *const *babies, const uint64_t *const *pts,
                  int32_t n, int32_t la, int32_t lp, int32_t pt_stride, uint64_t *out, int32_t batch);
+
+/* G <= 8 consecutive giant-step blocks sharing one set of n <= 192 babies, each
+ * block exactly hk_mac_plain(babies[0..counts[g]), diagonals g*nb .. g*nb+counts[g]-1
+ * of `pt` ([la+1][pt_count][N], hk_encode_diagonals), pt_stride = pt_count) into
+ * outs[g] at level la-1. Every baby is read once for the group (c4/c5 BSGS). */
+int hk_mac_plain_blocks(hk_ctx *ctx, const uint64_t *const *babies, int32_t n, int32_t la, const uint64_t *pt,
+                        int32_t pt_count, int32_t nb, int32_t G, const int32_t *counts, uint64_t *const *outs,
+                        int32_t batch);
 
 /* ---- introspection */
 int32_t hk_version(void);

@@ -373,13 +373,14 @@ int hk_encode(hk_ctx *c, const double *slots, int32_t B, int32_t level, double s
     return hk_ntt_fwd(c, pt, 0, nl, B);
 }
 
-/* BSGS diagonals of one giant-step block (inference.py:166-176): slot s of diagonal v
- * is W~[r][(r + base + v) mod m] with r = (s - base) mod S (zero for r >= m), W~ the
- * row-major n_o x n_in matrix zero-padded to m x m; encoded like hk_encode. */
+/* BSGS diagonals of consecutive giant-step blocks (inference.py:166-176): slot s of
+ * diagonal v is W~[r][(r + base + v) mod m] with r = (s - rb) mod S (zero for r >= m),
+ * rb = base + (v / nb) * nb the block's roll, W~ the row-major n_o x n_in matrix
+ * zero-padded to m x m; encoded like hk_encode. */
 int hk_encode_diagonals(hk_ctx *c, const double *W, int32_t n_o, int32_t n_in, int32_t m, int32_t base,
-                        int32_t count, int32_t level, double scale, uint64_t *pt) {
+                        int32_t count, int32_t nb, int32_t level, double scale, uint64_t *pt) {
     if (level < 0 || level >= c->n_q || count < 0) return fail(c, HK_E_ARG, "encode_diagonals: level/count");
-    if (n_o < 1 || n_in < 1 || m < n_o || m < n_in || m > c->slots || base < 0 || base + count > m)
+    if (n_o < 1 || n_in < 1 || m < n_o || m < n_in || m > c->slots || base < 0 || base + count > m || nb < 1)
         return fail(c, HK_E_ARG, "encode_diagonals: shape (%d x %d, m %d, base %d, count %d)", n_o, n_in, m, base,
                     count);
     if (count == 0) return HK_OK;
@@ -387,7 +388,8 @@ int hk_encode_diagonals(hk_ctx *c, const double *W, int32_t n_o, int32_t n_in, i
     double *slots = calloc((size_t)count * S, sizeof(double));
     for (int v = 0; v < count; ++v)
         for (int s = 0; s < S; ++s) {
-            const int r = ((s - base) % S + S) % S;
+            const int rb = base + (v / nb) * nb;
+            const int r = ((s - rb) % S + S) % S;
             if (r < m && r < n_o) {
                 const int col = (int)(((long long)r + base + v) % m);
                 if (col < n_in) slots[(size_t)v * S + s] = W[(size_t)r * n_in + col];
@@ -975,6 +977,29 @@ static void moddown_rescale(const hk_ctx *c, const uint64_t *acc, const uint64_t
         free(conv);
     }
     free(src);
+}
+
+/* G consecutive BSGS giant-step blocks sharing one set of babies: block g is
+ * hk_mac_plain over babies[0..counts[g]) and plaintexts v = g*nb + i of the
+ * [la+1][pt_count][N] diagonal buffer (pt_stride = pt_count), into outs[g]. */
+int hk_mac_plain_blocks(hk_ctx *c, const uint64_t *const *babies, int32_t n, int32_t la, const uint64_t *pt,
+                        int32_t pt_count, int32_t nb, int32_t G, const int32_t *counts, uint64_t *const *outs,
+                        int32_t B) {
+    if (la < 0 || la >= c->n_q || n < 1 || n > 192 || G < 1 || G > 8 || nb < 1 || B < 1)
+        return fail(c, HK_E_ARG, "mac_plain_blocks: args");
+    if (la < 1) return fail(c, HK_E_DEPTH, "multiplication at level %d", la);
+    for (int g = 0; g < G; ++g) {
+        if (counts[g] < 1 || counts[g] > n || counts[g] > nb) return fail(c, HK_E_ARG, "mac_plain_blocks: count");
+        if (g * nb + counts[g] > pt_count) return fail(c, HK_E_ARG, "mac_plain_blocks: plaintext count");
+    }
+    const uint64_t **pts = malloc(sizeof(uint64_t *) * n);
+    int rc = HK_OK;
+    for (int g = 0; g < G && rc == HK_OK; ++g) {
+        for (int i = 0; i < counts[g]; ++i) pts[i] = pt + (size_t)(g * nb + i) * c->n;
+        rc = hk_mac_plain(c, babies, pts, counts[g], la, la, pt_count, outs[g], B);
+    }
+    free(pts);
+    return rc;
 }
 
 int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {

@@ -39,7 +39,7 @@ SIGNATURES = {
     "hk_ntt_fwd": (C.c_int, [vp, vp, i32, i32, i32]),
     "hk_ntt_inv": (C.c_int, [vp, vp, i32, i32, i32]),
     "hk_encode": (C.c_int, [vp, vp, i32, i32, dbl, vp]),
-    "hk_encode_diagonals": (C.c_int, [vp, vp, i32, i32, i32, i32, i32, i32, dbl, vp]),
+    "hk_encode_diagonals": (C.c_int, [vp, vp, i32, i32, i32, i32, i32, i32, i32, dbl, vp]),
     "hk_encode_const": (C.c_int, [vp, dbl, i32, dbl, vp]),
     "hk_encrypt": (C.c_int, [vp, vp, i32, i32, u64, vp]),
     "hk_decrypt": (C.c_int, [vp, vp, i32, i32, dbl, vp]),
@@ -54,6 +54,7 @@ SIGNATURES = {
     "hk_rotate": (C.c_int, [vp, vp, i32, u32, vp, i32]),
     "hk_rotate_hoisted": (C.c_int, [vp, vp, i32, vp, i32, vp, i32]),
     "hk_mac_plain": (C.c_int, [vp, vp, vp, i32, i32, i32, i32, vp, i32]),
+    "hk_mac_plain_blocks": (C.c_int, [vp, vp, i32, i32, vp, i32, i32, i32, vp, vp, i32]),
     "hk_version": (C.c_int32, []),
     "hk_launch_count": (C.c_uint64, [vp]),
 }

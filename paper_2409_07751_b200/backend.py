@@ -457,34 +457,44 @@ class HeBackend:
             hit = self._mat_cache[key] = self.engine.put_f64(W)
         return hit
 
-    def bsgs_block(self, babies, Wdev, shape, m: int, base: int) -> CipherText:
-        """One giant-step block of bsgs_matvec: diagonals base..base+len(babies)-1
-        of the m x m zero-padded matrix, rolled by `base`, generated and encoded
-        on the device at the babies' level, then the fused MAC with one rescale.
-        Counts exactly like mac_plain (len(babies) pt_mults, len-1 adds)."""
-        n_terms = len(babies)
-        if n_terms == 0:
-            raise LengthMismatch("bsgs_block needs babies")
+    def bsgs_blocks(self, babies, Wdev, shape, m: int, base: int, nb: int, counts) -> list:
+        """len(counts) <= 8 consecutive giant-step blocks of bsgs_matvec starting at
+        diagonal `base` (block g covers diagonals base + g*nb .. + counts[g] - 1 of
+        the m x m zero-padded matrix, rolled by its own base): the group's diagonals
+        are generated and encoded on the device in one call, every baby is read once
+        for the whole group, then each block is rescaled. Counts per block exactly
+        like mac_plain (counts[g] pt_mults, counts[g] - 1 adds)."""
+        G = len(counts)
+        if not 1 <= G <= 8 or not babies:
+            raise LengthMismatch("bsgs_blocks needs 1..8 blocks and babies")
         a0 = babies[0]
         for x in babies:
             self._check_ours(x)
             if x.batch != a0.batch or x.level != a0.level:
-                raise LengthMismatch("bsgs_block operands must share batch and level")
+                raise LengthMismatch("bsgs_blocks operands must share batch and level")
         level = a0.level
         if level < 1:
             raise DepthExhausted(f"multiplication at level {level}")
         eng, B, n = self.engine, a0.batch, self.n
-        pt = eng.alloc_u64((level + 1) * n_terms * n)
+        total = (G - 1) * nb + counts[-1]
+        pt = eng.alloc_u64((level + 1) * total * n)
         eng.call("hk_encode_diagonals", eng.addr(Wdev), int(shape[0]), int(shape[1]), int(m), int(base),
-                 n_terms, level, self.params.pt_mult_scale(level), eng.addr(pt))
-        p0 = eng.addr(pt)
-        ptrs = (C.c_void_p * n_terms)(*[p0 + v * n * 8 for v in range(n_terms)])
-        out = eng.alloc_u64(2 * level * B * n)
-        eng.call("hk_mac_plain", eng.addr_array([x.data for x in babies]), ptrs, n_terms, level, level,
-                 n_terms, eng.addr(out), B)
-        self.counter.pt_mults += n_terms
-        self.counter.adds += n_terms - 1
-        return self._wrap(out, level - 1, B, a0.batched)
+                 total, int(nb), level, self.params.pt_mult_scale(level), eng.addr(pt))
+        outs = [eng.alloc_u64(2 * level * B * n) for _ in range(G)]
+        if 2 * B >= 16:  # the grouped kernel's (poly, sample) lanes are full
+            cnt = (C.c_int32 * G)(*[int(x) for x in counts])
+            eng.call("hk_mac_plain_blocks", eng.addr_array([x.data for x in babies]), len(babies), level,
+                     eng.addr(pt), total, nb, G, cnt, eng.addr_array(outs), B)
+        else:  # small batches: per-block fused MAC + rescale on the same diagonals
+            p0 = eng.addr(pt)
+            for g, c_ in enumerate(counts):
+                ptrs = (C.c_void_p * c_)(*[p0 + (g * nb + i) * n * 8 for i in range(c_)])
+                eng.call("hk_mac_plain", eng.addr_array([x.data for x in babies[:c_]]), ptrs, int(c_), level,
+                         level, total, eng.addr(outs[g]), B)
+        for c_ in counts:
+            self.counter.pt_mults += int(c_)
+            self.counter.adds += int(c_) - 1
+        return [self._wrap(o, level - 1, B, a0.batched) for o in outs]
 
     def ensure_galois_keys(self, galois_elts, level: int | None = None) -> None:
         """Galois keys serving ciphertexts up to `level` (default: the top level).

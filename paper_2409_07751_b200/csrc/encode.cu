@@ -87,16 +87,18 @@ __global__ void round_to_limbs(const double2 *__restrict__ w, int S, int log_n, 
     }
 }
 
-// BSGS diagonal v of one giant-step block, rolled by `base` (inference.py:172-176):
-// slot s holds d_v[(s - base) mod S], d_v[r] = W~[r][(r + base + v) mod m] for r < m,
-// W~ = W (n_o x n_in, row-major) zero-padded to m x m
-__global__ void gen_diagonals(const double *__restrict__ W, int n_o, int n_in, int m, int base, int S,
+// BSGS diagonal base + v, rolled by its giant-step block's base (inference.py:172-176):
+// slot s holds d[(s - rb) mod S] with rb = base + (v / nb) * nb and
+// d[r] = W~[r][(r + base + v) mod m] for r < m, W~ = W (n_o x n_in, row-major)
+// zero-padded to m x m
+__global__ void gen_diagonals(const double *__restrict__ W, int n_o, int n_in, int m, int base, int nb, int S,
                               double2 *__restrict__ a, long long total) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= total) return;
     const long long v = gid / S;
     const int s = (int)(gid - v * S);
-    int r = s - base % S;
+    const int rb = base + (int)(v / nb) * nb;
+    int r = s - rb % S;
     if (r < 0) r += S;
     double val = 0.0;
     if (r < m && r < n_o) {
@@ -157,16 +159,17 @@ extern "C" int hk_encode(hk_ctx *c, const double *slots, int32_t B, int32_t leve
 }
 
 extern "C" int hk_encode_diagonals(hk_ctx *c, const double *W, int32_t n_o, int32_t n_in, int32_t m, int32_t base,
-                                   int32_t count, int32_t level, double scale, uint64_t *pt) {
+                                   int32_t count, int32_t nb, int32_t level, double scale, uint64_t *pt) {
     if (level < 0 || level >= c->n_q || count < 0) return hk_fail(c, HK_E_ARG, "encode_diagonals: level/count");
-    if (n_o < 1 || n_in < 1 || m < n_o || m < n_in || m > c->slots || base < 0 || base + count > m)
+    if (n_o < 1 || n_in < 1 || m < n_o || m < n_in || m > c->slots || base < 0 || base + count > m || nb < 1)
         return hk_fail(c, HK_E_ARG, "encode_diagonals: shape (%d x %d, m %d, base %d, count %d)", n_o, n_in, m, base,
                        count);
     if (count == 0) return HK_OK;
     const long long all = (long long)count * c->slots;
     double2 *a = (double2 *)hk_workspace(c, sizeof(double2) * 2 * all);
     if (!a) return hk_fail(c, HK_E_NOMEM, "encode_diagonals workspace");
-    gen_diagonals<<<hk_grid(all, 256), 256, 0, c->stream>>>(W, n_o, n_in, m, base, c->slots, a, all); ++c->launches;
+    gen_diagonals<<<hk_grid(all, 256), 256, 0, c->stream>>>(W, n_o, n_in, m, base, nb, c->slots, a, all);
+    ++c->launches;
     return encode_loaded(c, a, count, level, scale, pt);
 }
 

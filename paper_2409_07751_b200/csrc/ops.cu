@@ -99,6 +99,61 @@ __global__ void k_mac(PtrList babies, PtrList pts, int n, int la, int ps, uint64
     out[o] = acc3_reduce(acc, mq[l]);
 }
 
+// G consecutive BSGS giant-step blocks at once (hk_mac_plain_blocks): every baby
+// value is read ONCE for the group instead of once per block.
+//   acc_g[p][l][b][k] = sum_{i < cnt_g} babies[i][p][l][b][k] * pt[l][g*nb + i][k]   (mod q_l)
+// CTA = 16 coefficients x 16 (poly, sample) lanes of one limb; the group's plaintext
+// tile [G][n][16] is staged in shared memory as 25-bit halves; Karatsuba split MACs
+// into 3-word accumulators, one Barrett reduction per output.
+constexpr int kBlkK = 16;
+template <int G>
+__global__ void __launch_bounds__(256) k_mac_blocks(PtrList babies, int n, int nb, int4 cnt_lo, int4 cnt_hi,
+                                                   const uint64_t *__restrict__ pt, int pt_count, int la,
+                                                   uint64_t *__restrict__ acc, long long BN, int B, int log_n,
+                                                   const ModQ *__restrict__ mq) {
+    extern __shared__ uint2 shp[];  // [G][n][kBlkK] (y0, y1)
+    const int N = 1 << log_n, l = blockIdx.y;
+    const int k0 = blockIdx.x * kBlkK;
+    const int cnt[8] = {cnt_lo.x, cnt_lo.y, cnt_lo.z, cnt_lo.w, cnt_hi.x, cnt_hi.y, cnt_hi.z, cnt_hi.w};
+    for (int t = threadIdx.x; t < G * n * kBlkK; t += blockDim.x) {
+        const int kk = t % kBlkK, gi = t / kBlkK, g = gi / n, i = gi - g * n;
+        uint2 v = make_uint2(0, 0);
+        if (i < cnt[g]) {
+            const uint64_t y = pt[((long long)l * pt_count + g * nb + i) * N + k0 + kk];
+            v = make_uint2((uint32_t)y & HK_M25, (uint32_t)(y >> 25));
+        }
+        shp[t] = v;
+    }
+    __syncthreads();
+    const int kk = threadIdx.x % kBlkK, lane = threadIdx.x / kBlkK;
+    const ModQ m = mq[l];
+    const size_t gstride = (size_t)2 * (la + 1) * BN;
+    for (int pb = lane; pb < 2 * B; pb += 256 / kBlkK) {
+        const int p = pb >= B ? 1 : 0, b = pb - p * B;
+        const long long o = ((long long)p * (la + 1) + l) * BN + (long long)b * N + k0 + kk;
+        uint64_t a0[G], a2[G], am[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) a0[g] = a2[g] = am[g] = 0;
+        for (int i = 0; i < n; ++i) {
+            uint32_t x0, x1;
+            split25(babies.p[i][o], x0, x1);
+            const uint32_t xs = x0 + x1;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const uint2 y = shp[(g * n + i) * kBlkK + kk];
+                a0[g] = mad_wide(x0, y.x, a0[g]);
+                a2[g] = mad_wide(x1, y.y, a2[g]);
+                am[g] = mad_wide(xs, y.x + y.y, am[g]);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const Acc3 A{a0[g], am[g] - a0[g] - a2[g], a2[g]};
+            acc[g * gstride + o] = acc3_reduce(A, m);
+        }
+    }
+}
+
 // ------------------------------------------------------------ rescale
 // R[i][pb][k] = centered(L[pb][k] mod q_l) mod q_i, i < l ; grid (BN2 / 256, l)
 __global__ void k_rs_center(const uint64_t *__restrict__ L, uint64_t *__restrict__ R, int l, long long BN2,
@@ -1029,6 +1084,54 @@ int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const
     }
     HK_LAUNCH_CHECK(c, "mac_plain");
     return rescale_launch(c, ws, la, B, out, ws + tot);
+}
+
+int hk_mac_plain_blocks(hk_ctx *c, const uint64_t *const *babies, int32_t n, int32_t la, const uint64_t *pt,
+                        int32_t pt_count, int32_t nb, int32_t G, const int32_t *counts, uint64_t *const *outs,
+                        int32_t B) {
+    if (la < 0 || la >= c->n_q || n < 1 || n > kMacMax || G < 1 || G > 8 || nb < 1 || B < 1)
+        return hk_fail(c, HK_E_ARG, "mac_plain_blocks: args");
+    if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
+    int need = 0;
+    for (int g = 0; g < G; ++g) {
+        if (counts[g] < 1 || counts[g] > n || counts[g] > nb) return hk_fail(c, HK_E_ARG, "mac_plain_blocks: count");
+        need = std::max(need, g * nb + counts[g]);
+    }
+    if (need > pt_count) return hk_fail(c, HK_E_ARG, "mac_plain_blocks: plaintext count %d < %d", pt_count, need);
+    if (c->n < kBlkK) return hk_fail(c, HK_E_ARG, "mac_plain_blocks: ring too small");
+    const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * ((size_t)G * tot + rs_scratch_words(c, la, B)));
+    if (!ws) return hk_fail(c, HK_E_NOMEM, "mac_plain_blocks workspace");
+    PtrList bl;
+    for (int i = 0; i < n; ++i) bl.p[i] = babies[i];
+    int cz[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+    for (int g = 0; g < G; ++g) cz[g] = counts[g];
+    const int4 lo = make_int4(cz[0], cz[1], cz[2], cz[3]), hi = make_int4(cz[4], cz[5], cz[6], cz[7]);
+    const size_t smem = sizeof(uint2) * (size_t)G * n * kBlkK;
+    const dim3 grid((unsigned)(c->n / kBlkK), (unsigned)(la + 1));
+#define HK_MACB(GV)                                                                                             \
+    case GV:                                                                                                    \
+        cudaFuncSetAttribute(k_mac_blocks<GV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+        k_mac_blocks<GV><<<grid, 256, smem, c->stream>>>(bl, n, nb, lo, hi, pt, pt_count, la, ws, BN, B,        \
+                                                         c->log_n, c->d_modq);                                  \
+        break;
+    switch (G) {
+        HK_MACB(1) HK_MACB(2) HK_MACB(3) HK_MACB(4) HK_MACB(5) HK_MACB(6) HK_MACB(7) HK_MACB(8)
+        default: break;
+    }
+#undef HK_MACB
+    ++c->launches;
+    HK_LAUNCH_CHECK(c, "mac_plain_blocks");
+    uint64_t *rs = ws + (size_t)G * tot;
+    for (int g = 0; g < G; ++g) {
+        int rc;
+        if (c->log_n == ntt16::kLogN)
+            rc = rescale_fused(c, make_src<SRC_PLAIN>(c, ws + (size_t)g * tot, la, B), la, B, outs[g], rs);
+        else
+            rc = rescale_launch(c, ws + (size_t)g * tot, la, B, outs[g], rs);
+        if (rc) return rc;
+    }
+    return HK_OK;
 }
 
 int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {
