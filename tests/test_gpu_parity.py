@@ -140,3 +140,22 @@ def test_level_truncated_galois_keys(gpu_lib, log_n, depth):
     for cg, co in zip(g.rotate_many(gl, [5, 7, -2]), o.rotate_many(ol, [5, 7, -2])):
         _same(g, o, cg, co, "hoisted, mixed key levels")
     np.testing.assert_allclose(g.decrypt(g.rotate(gl, 5)), np.roll(x, -5, axis=1), atol=1e-6)
+
+
+@pytest.mark.parametrize("B,n_o,n_in,split", [(8, 24, 64, (8, 8)), (8, 64, 40, (7, 10)), (2, 24, 64, (8, 8))])
+def test_bsgs_device_diagonals_bitexact(gpu_lib, B, n_o, n_in, split):
+    """bsgs_matvec through hk_encode_diagonals + hk_mac_plain_blocks (grouped
+    giant-step MAC, B >= 8) or the per-block fused MAC (B < 8): bit-exact with the
+    oracle and equal to W x in cleartext."""
+    from paper_2409_07751_b200 import inference as inf
+    g, o, p = _pair(13, 3)
+    S = p.slot_count
+    rng = np.random.default_rng(5)
+    W = rng.uniform(-0.5, 0.5, (n_o, n_in))
+    x = np.zeros((B, S))
+    x[:, :n_in] = rng.uniform(-1, 1, (B, n_in))
+    cg = inf.bsgs_matvec(W, g.encrypt(x), split=split)
+    co = inf.bsgs_matvec(W, o.encrypt(x), split=split)
+    _same(g, o, cg, co, "bsgs")
+    assert g.counter.pt_mults == o.counter.pt_mults == max(n_o, n_in)
+    np.testing.assert_allclose(g.decrypt(cg)[:, :n_o], x[:, :n_in] @ W.T, atol=1e-6)
