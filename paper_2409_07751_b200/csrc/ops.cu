@@ -115,14 +115,24 @@ __global__ void __launch_bounds__(256) k_mac_blocks(PtrList babies, int n, int n
     const int N = 1 << log_n, l = blockIdx.y;
     const int k0 = blockIdx.x * kBlkK;
     const int cnt[8] = {cnt_lo.x, cnt_lo.y, cnt_lo.z, cnt_lo.w, cnt_hi.x, cnt_hi.y, cnt_hi.z, cnt_hi.w};
-    for (int t = threadIdx.x; t < G * n * kBlkK; t += blockDim.x) {
-        const int kk = t % kBlkK, gi = t / kBlkK, g = gi / n, i = gi - g * n;
-        uint2 v = make_uint2(0, 0);
-        if (i < cnt[g]) {
-            const uint64_t y = pt[((long long)l * pt_count + g * nb + i) * N + k0 + kk];
-            v = make_uint2((uint32_t)y & HK_M25, (uint32_t)(y >> 25));
+    // stage the tile with 8 independent loads in flight per thread
+    const int tile = G * n * kBlkK;
+    for (int t0 = threadIdx.x; t0 < tile; t0 += 8 * blockDim.x) {
+        uint64_t y[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = t0 + u * blockDim.x;
+            y[u] = 0;
+            if (t < tile) {
+                const int kk = t % kBlkK, gi = t / kBlkK, g = gi / n, i = gi - g * n;
+                if (i < cnt[g]) y[u] = __ldg(pt + ((long long)l * pt_count + g * nb + i) * N + k0 + kk);
+            }
         }
-        shp[t] = v;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = t0 + u * blockDim.x;
+            if (t < tile) shp[t] = make_uint2((uint32_t)y[u] & HK_M25, (uint32_t)(y[u] >> 25));
+        }
     }
     __syncthreads();
     const int kk = threadIdx.x % kBlkK, lane = threadIdx.x / kBlkK;
@@ -134,7 +144,26 @@ __global__ void __launch_bounds__(256) k_mac_blocks(PtrList babies, int n, int n
         uint64_t a0[G], a2[G], am[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) a0[g] = a2[g] = am[g] = 0;
-        for (int i = 0; i < n; ++i) {
+        int i = 0;
+        for (; i + 8 <= n; i += 8) {  // eight babies' loads in flight
+            uint64_t xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) xv[u] = babies.p[i + u][o];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                uint32_t x0, x1;
+                split25(xv[u], x0, x1);
+                const uint32_t xs = x0 + x1;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint2 y = shp[(g * n + i + u) * kBlkK + kk];
+                    a0[g] = mad_wide(x0, y.x, a0[g]);
+                    a2[g] = mad_wide(x1, y.y, a2[g]);
+                    am[g] = mad_wide(xs, y.x + y.y, am[g]);
+                }
+            }
+        }
+        for (; i < n; ++i) {
             uint32_t x0, x1;
             split25(babies.p[i][o], x0, x1);
             const uint32_t xs = x0 + x1;
