@@ -338,9 +338,18 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
     nd = l // alpha + 1
     alg = B * 4 * (l + 1) * N * 8 + 2 * nd * (l + 1 + n_p) * N * 8
     ach = alg / t / 1e9
+    ks_traffic = None
+    try:  # summed dram bytes of one rotation's launches at this shape (tools/prof_rot.py)
+        with open(os.path.join(ROOT, "profiles", "r1_rotate_traffic.json")) as fh:
+            rt = json.load(fh)
+        if rt.get("algorithmic_bytes") == alg:
+            ks_traffic = rt["dram_read_bytes"] + rt["dram_write_bytes"]
+    except Exception:
+        pass
     out["keyswitch"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                        "frac": round(ach / hbm, 4), "traffic": None,
-                        "note": "integer-pipe bound: ~250 limb-NTTs + ~2,400 conversion MACs per coefficient",
+                        "frac": round(ach / hbm, 4), "traffic": ks_traffic,
+                        "note": "compute bound: ~250 limb-NTTs + ~2,400 conversion MACs per coefficient; "
+                                "traffic counts the extended-basis intermediates (profiles/r1_rotate_traffic.json)",
                         "kernel": f"hk_rotate (ModUp+KeyIP+ModDown) level {l}, {B} cts",
                         "algorithmic_bytes": alg, "ms": round(t * 1e3, 3)}
     return out
