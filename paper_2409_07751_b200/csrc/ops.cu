@@ -144,13 +144,14 @@ __global__ void __launch_bounds__(256) k_mac_blocks(PtrList babies, int n, int n
         uint64_t a0[G], a2[G], am[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) a0[g] = a2[g] = am[g] = 0;
+        constexpr int U = G <= 4 ? 16 : 8;  // babies' loads in flight (registers permitting)
         int i = 0;
-        for (; i + 8 <= n; i += 8) {  // eight babies' loads in flight
-            uint64_t xv[8];
+        for (; i + U <= n; i += U) {
+            uint64_t xv[U];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) xv[u] = babies.p[i + u][o];
+            for (int u = 0; u < U; ++u) xv[u] = babies.p[i + u][o];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < U; ++u) {
                 uint32_t x0, x1;
                 split25(xv[u], x0, x1);
                 const uint32_t xs = x0 + x1;

@@ -16,6 +16,8 @@
 
 using namespace ntt16;
 
+constexpr int kSmem32 = 32 * kRowPad * 8 + 256 * 16;  // 8-CTA variants (512 threads, 32 columns)
+
 template <int V>
 __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 2)
     lab_fwd(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
@@ -399,6 +401,90 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 4)
     }
 }
 
+
+// V9: V8 (16-CTA clusters) with the CTA-uniform twiddles T[1..15] of stages 0-3 of
+// both phases read from constant memory (DFMA operands, no LDS)
+__constant__ double2 cT[64][16];
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 4)
+    lab_fwd9(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
+             const double2 *__restrict__ tw, const double2 *__restrict__ twist, FpMod m, int mi) {
+    extern __shared__ double smd[];
+    double2 *st = reinterpret_cast<double2 *>(smd + 16 * kRowPad);
+    const int cb = blockIdx.x & 15;
+    const long long P = blockIdx.x >> 4;
+    st[threadIdx.x] = tw[threadIdx.x];
+    __syncthreads();
+    double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
+    {
+        const int c = threadIdx.x & 15, k = threadIdx.x >> 4, col = cb * 16 + c;
+        double x[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x[u] = u2d(in[P * kN + (k + 16 * u) * 256 + col]);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int d = 8 >> s;
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (!(u & d)) ct_f<false>(x[u], x[u + d], cT[mi][(1 << s) + (u >> (4 - s))], m);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) smd[(k + 16 * u) * 16 + c] = x[u];
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < 16; ++v) x[v] = smd[(16 * k + v) * 16 + c];
+#pragma unroll
+        for (int s = 4; s < 8; ++s) {
+            const int d = 128 >> s;
+#pragma unroll
+            for (int v = 0; v < 16; ++v)
+                if (!(v & d)) ct_f<false>(x[v], x[v + d], st[(1 << s) + ((16 * k + v) >> (8 - s))], m);
+        }
+#pragma unroll
+        for (int v = 0; v < 16; ++v) inter[(16 * k + v) * 256 + col] = f_center(x[v], m);
+    }
+    cluster_sync_all();
+    {
+        const int rs = threadIdx.x >> 4, r = cb * 16 + rs;
+        const int k = threadIdx.x & 15;
+        double *srow = smd + rs * kRowPad;
+        double x[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x[u] = __ldcg(inter + r * 256 + k + 16 * u);
+        const double2 *tr = twist + r * 256;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const double2 t = __ldg(tr + k + 16 * u);
+            x[u] = f_mulmod(x[u], t.x, t.y, m.q);
+        }
+#pragma unroll
+        for (int sp = 0; sp < 4; ++sp) {
+            const int d = 8 >> sp;
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (!(u & d)) ct_f<false>(x[u], x[u + d], cT[mi][(1 << sp) + (u >> (4 - sp))], m);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = x[u];
+        __syncwarp();
+#pragma unroll
+        for (int v = 0; v < 16; ++v) x[v] = srow[pad16(16 * k + v)];
+#pragma unroll
+        for (int sp = 4; sp < 8; ++sp) {
+            const int d = 128 >> sp;
+#pragma unroll
+            for (int v = 0; v < 16; ++v)
+                if (!(v & d)) ct_f<false>(x[v], x[v + d], st[(1 << sp) + ((16 * k + v) >> (8 - sp))], m);
+        }
+        __syncwarp();
+        uint64_t *su = reinterpret_cast<uint64_t *>(srow);
+#pragma unroll
+        for (int v = 0; v < 16; ++v) su[pad16(16 * k + v)] = d2canon(x[v], m);
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) out[P * kN + r * 256 + k + 16 * u] = su[pad16(k + 16 * u)];
+    }
+}
+
 #define CK(x)                                                                    \
     do {                                                                         \
         cudaError_t e_ = (x);                                                    \
@@ -411,15 +497,15 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 4)
 template <int V>
 float run(int polys, const uint64_t *in, uint64_t *inter, uint64_t *out, const double2 *tw, const double2 *twist,
           FpMod m, int reps) {
-    CK(cudaFuncSetAttribute(lab_fwd<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    CK(cudaFuncSetAttribute(lab_fwd<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem32));
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    lab_fwd<V><<<8 * polys, 512, kSmem>>>(in, inter, out, tw, twist, m);
+    lab_fwd<V><<<8 * polys, 512, kSmem32>>>(in, inter, out, tw, twist, m);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     cudaEventRecord(a);
-    for (int i = 0; i < reps; ++i) lab_fwd<V><<<8 * polys, 512, kSmem>>>(in, inter, out, tw, twist, m);
+    for (int i = 0; i < reps; ++i) lab_fwd<V><<<8 * polys, 512, kSmem32>>>(in, inter, out, tw, twist, m);
     cudaEventRecord(b);
     CK(cudaEventSynchronize(b));
     float ms;
@@ -458,14 +544,14 @@ int main(int argc, char **argv) {
     t[3] = run<3>(polys, in, inter, out, tw, twist, m, reps);
     t[4] = run<4>(polys, in, inter, out, tw, twist, m, reps);
     {
-        CK(cudaFuncSetAttribute(lab_fwd5, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        CK(cudaFuncSetAttribute(lab_fwd5, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem32));
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
-        lab_fwd5<<<8 * polys, 512, kSmem>>>(in, out, tw, twist, m);
+        lab_fwd5<<<8 * polys, 512, kSmem32>>>(in, out, tw, twist, m);
         CK(cudaDeviceSynchronize());
         cudaEventRecord(a);
-        for (int i = 0; i < reps; ++i) lab_fwd5<<<8 * polys, 512, kSmem>>>(in, out, tw, twist, m);
+        for (int i = 0; i < reps; ++i) lab_fwd5<<<8 * polys, 512, kSmem32>>>(in, out, tw, twist, m);
         cudaEventRecord(b);
         CK(cudaEventSynchronize(b));
         float ms;
@@ -473,14 +559,14 @@ int main(int argc, char **argv) {
         printf("%-22s %8.3f ms  %6.3f us/limb-poly\n", "V5 DSMEM exchange", ms / reps, 1e3 * ms / reps / polys);
     }
     {
-        CK(cudaFuncSetAttribute(lab_fwd6, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        CK(cudaFuncSetAttribute(lab_fwd6, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem32));
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
-        lab_fwd6<<<8 * polys, 512, kSmem>>>(in, out, tw, twist, m);
+        lab_fwd6<<<8 * polys, 512, kSmem32>>>(in, out, tw, twist, m);
         CK(cudaDeviceSynchronize());
         cudaEventRecord(a);
-        for (int i = 0; i < reps; ++i) lab_fwd6<<<8 * polys, 512, kSmem>>>(in, out, tw, twist, m);
+        for (int i = 0; i < reps; ++i) lab_fwd6<<<8 * polys, 512, kSmem32>>>(in, out, tw, twist, m);
         cudaEventRecord(b);
         CK(cudaEventSynchronize(b));
         float ms;
@@ -504,6 +590,27 @@ int main(int argc, char **argv) {
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         printf("%-22s %8.3f ms  %6.3f us/limb-poly\n", "V8 cluster16 x 256", ms / reps, 1e3 * ms / reps / polys);
+    }
+    {
+        std::vector<double2> ct(64 * 16);
+        for (int j = 0; j < 64; ++j)
+            for (int i = 0; i < 16; ++i) ct[j * 16 + i] = h[i];
+        CK(cudaMemcpyToSymbol(cT, ct.data(), sizeof(double2) * 64 * 16));
+        CK(cudaFuncSetAttribute(lab_fwd9, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(lab_fwd9, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem8));
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        lab_fwd9<<<16 * polys, 256, kSmem8>>>(in, inter, out, tw, twist, m, 3);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(a);
+        for (int i = 0; i < reps; ++i) lab_fwd9<<<16 * polys, 256, kSmem8>>>(in, inter, out, tw, twist, m, 3);
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("%-22s %8.3f ms  %6.3f us/limb-poly\n", "V9 const twiddles", ms / reps, 1e3 * ms / reps / polys);
     }
     for (int i = 0; i < 5; ++i)
         printf("%-22s %8.3f ms  %6.3f us/limb-poly\n", names[i], t[i], 1e3 * t[i] / polys);
