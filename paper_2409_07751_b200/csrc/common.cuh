@@ -188,7 +188,7 @@ struct hk_ctx {
     // fused 2^16 kernels (ntt16.cuh), N = 2^16 (root psi) or 2^17 (root psi^2 per half); stride 2^16
     double2 *d_twf;        // [n_mod][2^16] {w^brv(k), w^brv(k)/q} as float64
     double2 *d_itwf;       // [n_mod][2^16] inverse twiddles, float64
-    double2 *d_ninvf;      // [n_mod] {2^-16, 2^-16/q}
+    double2 *d_ninvf;      // [n_mod][2] {2^-16, 2^-16/q}, {2^-16 Ti[1], .../q} (inverse stage 0 fused)
     double2 *d_fmod;       // [n_mod] {q, 1/q} (every N)
     double2 *d_twist;      // [n_mod][256][256] w^(c (2 brv8(r) + 1 - 256)), float64 {w, w/q} (rows)
     double2 *d_itwist;     // [n_mod][256][256] inverse twist

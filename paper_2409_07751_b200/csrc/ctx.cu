@@ -218,7 +218,7 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     c->d_n17w = nullptr;
     if (c->log_n == 16 || c->log_n == 17) {
         const int H = 1 << 16;
-        std::vector<double2> twf((size_t)nm * H), itwf((size_t)nm * H), ninvf(nm);
+        std::vector<double2> twf((size_t)nm * H), itwf((size_t)nm * H), ninvf(2 * (size_t)nm);
         std::vector<double2> tws((size_t)nm * H), itws((size_t)nm * H);
         const uint64_t M2 = 2ull * H;
         for (int m = 0; m < nm; ++m) {
@@ -233,8 +233,12 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
                 pw = h_mulmod(pw, w, q);
                 ipw = h_mulmod(ipw, iw, q);
             }
-            const uint64_t ni = h_inv((uint64_t)H % q, q);
-            ninvf[m] = make_double2((double)ni, (double)ni / qd);
+            // T[1] = w^(2^15) (stage 0 of the 256-point sub-transforms) and its inverse, folded
+            // into the twist tables (c >= 128) and the inverse scaling (ntt16.cuh)
+            const uint64_t t1 = h_powmod(w, 1ull << 15, q), ti1 = h_inv(t1, q);
+            const uint64_t ni = h_inv((uint64_t)H % q, q), niw = h_mulmod(ni, ti1, q);
+            ninvf[2 * m] = make_double2((double)ni, (double)ni / qd);
+            ninvf[2 * m + 1] = make_double2((double)niw, (double)niw / qd);
             // four-step twist for the 256 x 256 split: row r, column c
             for (int r = 0; r < 256; ++r) {
                 const int64_t e = 2 * (int64_t)h_brv((uint32_t)r, 8) + 1 - 256;  // may be negative
@@ -243,8 +247,10 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
                 uint64_t t = 1, it = 1;
                 for (int col = 0; col < 256; ++col) {
                     const size_t o = (size_t)m * H + (size_t)r * 256 + col;
-                    tws[o] = make_double2((double)t, (double)t / qd);
-                    itws[o] = make_double2((double)it, (double)it / qd);
+                    const uint64_t tv = col < 128 ? t : h_mulmod(t, t1, q);
+                    const uint64_t itv = col < 128 ? it : h_mulmod(it, ti1, q);
+                    tws[o] = make_double2((double)tv, (double)tv / qd);
+                    itws[o] = make_double2((double)itv, (double)itv / qd);
                     t = h_mulmod(t, base, q);
                     it = h_mulmod(it, ibase, q);
                 }

@@ -132,13 +132,21 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
     double x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = __ldcg(rd + k + 16 * u);
+    // twist fused with stage 0 (pairs c, c+128, twiddle T[1]): the table holds
+    // tau(r, c) for c < 128 and tau(r, c) * T[1] for c >= 128
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-        const double2 t = __ldg(tr + k + 16 * u);
-        x[u] = f_mulmod(x[u], t.x, t.y, m.q);
+    for (int u = 0; u < 8; ++u) {
+        const double2 ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
+        const double a = f_mulmod(x[u], ta.x, ta.y, m.q), b = f_mulmod(x[u + 8], tb.x, tb.y, m.q);
+        x[u] = __dadd_rn(a, b);
+        x[u + 8] = __dsub_rn(a, b);
+        if (kBig) {
+            x[u] = f_center(x[u], m);
+            x[u + 8] = f_center(x[u + 8], m);
+        }
     }
 #pragma unroll
-    for (int sp = 0; sp < 4; ++sp) {
+    for (int sp = 1; sp < 4; ++sp) {
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
@@ -226,24 +234,29 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = srow[pad16(k + 16 * u)];
 #pragma unroll
-    for (int sp = 3; sp >= 0; --sp) {
+    for (int sp = 3; sp >= 1; --sp) {
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
             if (!(u & d)) gs_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m);
     }
+    // stage 0 (pairs c, c+128, twiddle Ti[1]) fused with the untwist: the table holds
+    // tau^-1(r, c) for c < 128 and tau^-1(r, c) * Ti[1] for c >= 128
     const double2 *tr = itau + r * 256;
     double *rd = inter + r * 256;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-        const double2 t = __ldg(tr + k + 16 * u);
-        rd[k + 16 * u] = f_center(f_mulmod(x[u], t.x, t.y, m.q), m);
+    for (int u = 0; u < 8; ++u) {
+        const double2 ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
+        const double U = x[u], V = x[u + 8];
+        rd[k + 16 * u] = f_center(f_mulmod(__dadd_rn(U, V), ta.x, ta.y, m.q), m);
+        rd[k + 16 * (u + 8)] = f_center(f_mulmod(__dsub_rn(U, V), tb.x, tb.y, m.q), m);
     }
 }
 
 template <bool kBig, class Epi>
 __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, const double *inter, int tile,
-                                         const double2 *__restrict__ T, double2 ni, const FpMod &m, double *sm) {
+                                         const double2 *__restrict__ T, double2 ni, double2 niw, const FpMod &m,
+                                         double *sm) {
     const int c = threadIdx.x % kTc, k = threadIdx.x / kTc, col = tile * kTc + c;
     double x[16];
 #pragma unroll
@@ -261,14 +274,21 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = sm[(k + 16 * u) * kTc + c];
 #pragma unroll
-    for (int s = 3; s >= 0; --s) {
+    for (int s = 3; s >= 1; --s) {
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
             if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m);
     }
+    // stage 0 (twiddle Ti[1]) fused with the N^-1 scaling: niw = N^-1 * Ti[1]
 #pragma unroll
-    for (int u = 0; u < 16; ++u) epi(l, P, (k + 16 * u) * 256 + col, d2canon(f_mulmod(x[u], ni.x, ni.y, m.q), m));
+    for (int u = 0; u < 8; ++u) {
+        const double U = x[u], V = x[u + 8];
+        x[u] = f_mulmod(__dadd_rn(U, V), ni.x, ni.y, m.q);
+        x[u + 8] = f_mulmod(__dsub_rn(U, V), niw.x, niw.y, m.q);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) epi(l, P, (k + 16 * u) * 256 + col, d2canon(x[u], m));
 }
 
 template <class Pro, class Epi>
@@ -291,11 +311,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
     if (m.q < (double)kSmallPrime) {
         inv_row<false>(pro, l, P, inter, r, itau, st, m, smd + rs * kRowPad);
         cluster_sync_all();
-        inv_cols<false>(epi, l, P, inter, c, st, ninv[mi], m, smd);
+        inv_cols<false>(epi, l, P, inter, c, st, ninv[2 * mi], ninv[2 * mi + 1], m, smd);
     } else {
         inv_row<true>(pro, l, P, inter, r, itau, st, m, smd + rs * kRowPad);
         cluster_sync_all();
-        inv_cols<true>(epi, l, P, inter, c, st, ninv[mi], m, smd);
+        inv_cols<true>(epi, l, P, inter, c, st, ninv[2 * mi], ninv[2 * mi + 1], m, smd);
     }
 }
 
