@@ -153,6 +153,12 @@ int hk_rotate(hk_ctx *ctx, const uint64_t *a, int32_t la, uint32_t galois_elt,
 int hk_rotate_hoisted(hk_ctx *ctx, const uint64_t *a, int32_t la,
                       const uint32_t *galois_elts, int32_t n, uint64_t *const *outs,
                       int32_t batch);
+/* sum_i sigma_{g_i}(ct_i) for n ciphertexts at level la (g_i = 1: identity, no key
+ * switch): the BSGS giant-step accumulation of inference.py:177-180 with the key
+ * inner products summed in the extended basis and ONE ModDown (lazy ModDown).
+ * Logically n rotations (non-identity) + (n-1) adds; out [2][la+1][B][N]. */
+int hk_rotate_sum(hk_ctx *ctx, const uint64_t *const *cts, int32_t la, const uint32_t *galois_elts, int32_t n,
+                  uint64_t *out, int32_t batch);
 
 /* ---- fused BSGS giant-step block (inference.py:166-178): for one giant step
  * out = sum_i pt_i (*) babies_i, accumulated lazily, then ONE rescale.

@@ -1032,6 +1032,61 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     return HK_OK;
 }
 
+/* sum_i sigma_{g_i}(ct_i) with one ModDown: key inner products accumulate over the
+ * terms in the extended basis, then ModDown, then + sum_i sigma_{g_i}(c0_i) and the
+ * c1 of identity terms (g_i = 1). */
+int hk_rotate_sum(hk_ctx *c, const uint64_t *const *cts, int32_t la, const uint32_t *gs, int32_t n, uint64_t *out,
+                  int32_t B) {
+    if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || la >= c->n_q || n < 1 || B < 1) return fail(c, HK_E_ARG, "rotate_sum: args");
+    for (int i = 0; i < n; ++i) {
+        if ((gs[i] & 1u) == 0 || gs[i] >= 2u * (uint32_t)c->n) return fail(c, HK_E_ARG, "galois element %u invalid", gs[i]);
+        if (gs[i] != 1u && !find_gal(c, gs[i])) return fail(c, HK_E_NOKEY, "no galois key for element %u", gs[i]);
+    }
+    const int l = la, N = c->n, ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
+    const size_t pl = (size_t)(l + 1) * B * N, el = (size_t)ne * B * N;
+    uint64_t *ext = malloc(sizeof(uint64_t) * (size_t)nd * el);
+    uint64_t *acc = malloc(sizeof(uint64_t) * 2 * el), *tot = calloc(2 * el, sizeof(uint64_t));
+    uint64_t *add = calloc(2 * pl, sizeof(uint64_t)), *tmp = malloc(sizeof(uint64_t) * N);
+    int n_ks = 0;
+    for (int r = 0; r < n; ++r) {
+        const uint32_t g = gs[r];
+        for (int p = 0; p < 2; ++p) {  /* p = 0: sigma_g(c0); p = 1: c1 of identity terms */
+            if (p == 1 && g != 1u) continue;
+            for (int i = 0; i <= l; ++i)
+                for (int b = 0; b < B; ++b) {
+                    const size_t off = ((size_t)i * B + b) * N;
+                    automorph_ntt(c, cts[r] + p * pl + off, tmp, g);
+                    for (int k = 0; k < N; ++k) add[p * pl + off + k] = addmod(add[p * pl + off + k], tmp[k], c->mod[i]);
+                }
+        }
+        if (g == 1u) continue;
+        modup(c, cts[r] + pl, l, B, ext);
+        key_ip(c, ext, l, B, find_gal(c, g), g, acc);
+        for (int p = 0; p < 2; ++p)
+            for (int t = 0; t < ne; ++t) {
+                const uint64_t q = c->mod[ext_mod(c, l, t)];
+                const size_t off = (size_t)p * el + (size_t)t * B * N;
+                for (size_t k = 0; k < (size_t)B * N; ++k) tot[off + k] = addmod(tot[off + k], acc[off + k], q);
+            }
+        ++n_ks;
+    }
+    if (n_ks) {
+        moddown(c, tot, l, B, out);
+        moddown(c, tot + el, l, B, out + pl);
+    } else {
+        memset(out, 0, sizeof(uint64_t) * 2 * pl);
+    }
+    for (int p = 0; p < 2; ++p)
+        for (int i = 0; i <= l; ++i)
+            for (size_t k = 0; k < (size_t)B * N; ++k) {
+                const size_t off = p * pl + (size_t)i * B * N + k;
+                out[off] = addmod(out[off], add[off], c->mod[i]);
+            }
+    free(ext); free(acc); free(tot); free(add); free(tmp);
+    return HK_OK;
+}
+
 int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *gs, int32_t n,
                       uint64_t *const *outs, int32_t B) {
     if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");

@@ -55,6 +55,7 @@ SIGNATURES = {
     "hk_rotate_hoisted": (C.c_int, [vp, vp, i32, vp, i32, vp, i32]),
     "hk_mac_plain": (C.c_int, [vp, vp, vp, i32, i32, i32, i32, vp, i32]),
     "hk_mac_plain_blocks": (C.c_int, [vp, vp, i32, i32, vp, i32, i32, i32, vp, vp, i32]),
+    "hk_rotate_sum": (C.c_int, [vp, vp, i32, vp, i32, vp, i32]),
     "hk_version": (C.c_int32, []),
     "hk_launch_count": (C.c_uint64, [vp]),
 }

@@ -415,6 +415,32 @@ class HeBackend:
                 outs[t] = self._wrap(buf, a.level, a.batch, a.batched)
         return [a if t == 0 else outs[t] for t in steps]
 
+    def rotate_sum(self, cts, steps) -> CipherText:
+        """sum_i rotate(cts[i], steps[i]) with the key switches' inner products
+        accumulated in the extended basis and one ModDown (BSGS giant steps,
+        inference.py:177-180). Counts like rotate()-then-add: one rotation per
+        nonzero step, len - 1 adds."""
+        if not cts or len(cts) != len(steps):
+            raise LengthMismatch("rotate_sum needs matching non-empty lists")
+        a0 = cts[0]
+        for x in cts:
+            self._check_ours(x)
+            if x.batch != a0.batch or x.level != a0.level:
+                raise LengthMismatch("rotate_sum operands must share batch and level")
+        steps = [int(t) for t in steps]
+        for t in steps:
+            if abs(t) >= self.config.slot_count:
+                raise ValueError(f"|t| = {abs(t)} must be < slot_count {self.config.slot_count}")
+        gs = [galois_element(t, self.config.slot_count) if t else 1 for t in steps]
+        self.ensure_galois_keys([g for g in gs if g != 1], a0.level)
+        eng = self.engine
+        out = eng.alloc_u64(2 * (a0.level + 1) * a0.batch * self.n)
+        eng.call("hk_rotate_sum", eng.addr_array([x.data for x in cts]), a0.level, eng.u32_array(gs), len(cts),
+                 eng.addr(out), a0.batch)
+        self.counter.rotations += sum(1 for t in steps if t)
+        self.counter.adds += len(cts) - 1
+        return self._wrap(out, a0.level, a0.batch, a0.batched)
+
     def mac_plain(self, babies, plains) -> CipherText:
         """sum_i babies[i] * plains[i] with ONE rescale (fused BSGS block,
         inference.py:171-178). Counts len(babies) pt_mults and len-1 adds."""

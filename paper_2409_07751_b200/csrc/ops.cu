@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext
                                                 const uint64_t *__restrict__ dm, int alpha, int ne, int l, int n_q,
                                                 int nm, int ksp0, int log_n, int bb, const uint64_t *__restrict__ key,
                                                 uint32_t g, uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1,
-                                                const double2 *__restrict__ fmod, long long BN) {
+                                                const double2 *__restrict__ fmod, long long BN, int accum) {
     using namespace ntt16;
     const int N = 1 << log_n;
     const int kblocks = N / (int)blockDim.x;
@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext
             for (int j = 0; j < ND; ++j)
                 if (j == own_j) x[j] = y;
         }
-        double s0 = 0.0, s1 = 0.0;
+        // accum: add onto the running sum of earlier key switches (hk_rotate_sum)
+        double s0 = accum ? u2d(*o0) : 0.0, s1 = accum ? u2d(*o1) : 0.0;
 #pragma unroll
         for (int j = 0; j < ND; ++j) {  // |f_mulmod| < 2.5 q: recentre every second term
             s0 = __dadd_rn(s0, f_mulmod(x[j], w0[j], v0[j], M.q));
@@ -398,6 +399,21 @@ __global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext
         o0 += N;
         o1 += N;
     }
+}
+
+// out (+)= sigma_g(in) over [l+1][B][N] ; grid (BN/256, l+1)
+__global__ void k_auto_acc(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, uint32_t g, int log_n,
+                           long long BN, int init, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    (void)p;
+    const long long o = (long long)l * BN + e;
+    long long src = o;
+    if (g != 1u) {
+        const int k = (int)(e & ((1 << log_n) - 1));
+        src = o - k + auto_src((uint32_t)k, g, log_n);
+    }
+    const uint64_t v = in[src];
+    out[o] = init ? v : add_mod(out[o], v, mq[l].q);
 }
 
 // out_i = (acc_i - conv_i) * P^-1 (+ optional addend, optionally automorphed) ; grid (BN/256, l+1)
@@ -836,7 +852,7 @@ struct KeyRef {
 };
 
 static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, KeyRef key, uint32_t g,
-                 const uint64_t *dm = nullptr) {
+                 const uint64_t *dm = nullptr, int accum = 0) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
     if (key.level < l) return hk_fail(c, HK_E_NOKEY, "key for element %u serves level %d < %d", g, key.level, l);
     const int krows = key.level + 1 + c->n_p;
@@ -846,7 +862,8 @@ static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, K
     const dim3 ipg((unsigned)((c->n / ipt) * (B / bb)), (unsigned)ne);
 #define HK_KEY_IP(ND)                                                                                          \
     k_key_ip<ND><<<ipg, ipt, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, krows, key.level + 1,     \
-                                             c->log_n, bb, key.p, g, kb.acc, kb.acc + (size_t)ne * BN, c->d_fmod, BN)
+                                             c->log_n, bb, key.p, g, kb.acc, kb.acc + (size_t)ne * BN, c->d_fmod, BN, \
+                                             accum)
     switch (nd) {
         case 1: HK_KEY_IP(1); break;
         case 2: HK_KEY_IP(2); break;
@@ -1206,6 +1223,58 @@ int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * ks_words(c, la, B));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "rotate workspace");
     return keyswitch(c, a + pl, la, B, n, keys.data(), gs, o0.data(), o1.data(), a, ws);
+}
+
+// sum_i sigma_{g_i}(ct_i) with ONE ModDown (lazy BSGS giant steps): the key inner
+// products of every term accumulate in the extended basis; sum_i sigma_{g_i}(c0_i)
+// (and the c1 of identity terms, g_i = 1) join in the ModDown epilogues.
+int hk_rotate_sum(hk_ctx *c, const uint64_t *const *cts, int32_t la, const uint32_t *gs, int32_t n, uint64_t *out,
+                  int32_t B) {
+    if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || la >= c->n_q || n < 1 || B < 1) return hk_fail(c, HK_E_ARG, "rotate_sum: args");
+    const uint32_t M = 2u * (uint32_t)c->n;
+    std::vector<KeyRef> keys(n);
+    for (int i = 0; i < n; ++i) {
+        if ((gs[i] & 1u) == 0 || gs[i] >= M) return hk_fail(c, HK_E_ARG, "galois element %u invalid", gs[i]);
+        if (gs[i] == 1u) continue;
+        auto it = c->gal.find(gs[i]);
+        if (it == c->gal.end()) return hk_fail(c, HK_E_NOKEY, "no galois key for element %u", gs[i]);
+        if (it->second.level < la)
+            return hk_fail(c, HK_E_NOKEY, "galois key %u serves level %d < %d", gs[i], it->second.level, la);
+        keys[i] = KeyRef{it->second.p, it->second.level};
+    }
+    const long long BN = (long long)B * c->n, pl = (long long)(la + 1) * BN;
+    uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (ks_words(c, la, B) + 2 * pl));
+    if (!ws) return hk_fail(c, HK_E_NOMEM, "rotate_sum workspace");
+    uint64_t *c0sum = ws, *c1id = ws + pl;
+    const KsBufs kb = ks_bufs(c, la, B, ws + 2 * pl);
+    int n_id = 0, n_ks = 0, rc = HK_OK;
+    for (int i = 0; i < n; ++i) {
+        k_auto_acc<<<egrid(BN, la + 1, 1), 256, 0, c->stream>>>(cts[i], c0sum, gs[i], c->log_n, BN, i == 0,
+                                                                c->d_modq);
+        ++c->launches;
+        if (gs[i] == 1u) {
+            k_auto_acc<<<egrid(BN, la + 1, 1), 256, 0, c->stream>>>(cts[i] + pl, c1id, 1u, c->log_n, BN, n_id == 0,
+                                                                    c->d_modq);
+            ++c->launches;
+            ++n_id;
+        }
+    }
+    HK_LAUNCH_CHECK(c, "rotate_sum: automorphism sums");
+    for (int i = 0; i < n && !rc; ++i) {
+        if (gs[i] == 1u) continue;
+        rc = ks_modup(c, cts[i] + pl, la, B, kb);
+        if (!rc) rc = ks_ip(c, cts[i] + pl, la, B, kb, keys[i], gs[i], nullptr, n_ks > 0);
+        ++n_ks;
+    }
+    if (rc) return rc;
+    if (n_ks == 0) {
+        HK_CUDA(c, cudaMemcpyAsync(out, c0sum, sizeof(uint64_t) * 2 * pl, cudaMemcpyDeviceToDevice, c->stream));
+        return HK_OK;
+    }
+    const int ne = la + 1 + c->n_p;
+    if ((rc = ks_moddown(c, kb.acc, la, B, kb, out, c0sum, 1u))) return rc;
+    return ks_moddown(c, kb.acc + (size_t)ne * BN, la, B, kb, out + pl, n_id ? c1id : nullptr, 1u);
 }
 
 int hk_rotate(hk_ctx *c, const uint64_t *a, int32_t la, uint32_t g, uint64_t *out, int32_t B) {

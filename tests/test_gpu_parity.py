@@ -159,3 +159,19 @@ def test_bsgs_device_diagonals_bitexact(gpu_lib, B, n_o, n_in, split):
     _same(g, o, cg, co, "bsgs")
     assert g.counter.pt_mults == o.counter.pt_mults == max(n_o, n_in)
     np.testing.assert_allclose(g.decrypt(cg)[:, :n_o], x[:, :n_in] @ W.T, atol=1e-6)
+
+
+@pytest.mark.parametrize("log_n,depth", [(13, 4), (16, 3)])
+def test_rotate_sum_bitexact(gpu_lib, log_n, depth):
+    """hk_rotate_sum (lazy ModDown over BSGS giant steps, identity terms included):
+    bit-exact with the oracle and equal to the sum of rotations in value."""
+    g, o, p = _pair(log_n, depth)
+    S = p.slot_count
+    rng = np.random.default_rng(9)
+    xs = [rng.uniform(-1, 1, (2, S)) for _ in range(4)]
+    steps = [0, 3, -7, 3]
+    gc, oc = [g.encrypt(x) for x in xs], [o.encrypt(x) for x in xs]
+    _same(g, o, g.rotate_sum(gc, steps), o.rotate_sum(oc, steps), "rotate_sum")
+    _same(g, o, g.rotate_sum(gc[:1], [0]), o.rotate_sum(oc[:1], [0]), "rotate_sum identity only")
+    ref = sum(np.roll(x, -t, axis=1) for x, t in zip(xs, steps))
+    np.testing.assert_allclose(g.decrypt(g.rotate_sum(gc, steps)), ref, atol=1e-6)
