@@ -18,8 +18,9 @@
  * HeBackend op (backend.py:192-245) decrypts to the CleartextBackend result
  * within CKKS error, and the reference pipeline's golden outputs
  * (tests/golden/, generated from /root/reference by tests/golden/make_golden.py)
- * are reproduced within 1e-4. At the RNS level parity is "self-pinned"
- * (NTT vs schoolbook, encode vs direct DFT, decrypt(encrypt) round trips).
+ * are reproduced within 1e-4. At the RNS level: PARITY UNPINNED (no reference
+ * RNS arithmetic exists to compare against); the restatement is self-checked
+ * instead (NTT vs schoolbook, encode vs direct DFT, decrypt(encrypt) round trips).
  *
  * Semantics of each entry point: include/hekan.h. All buffers HOST pointers.
  */
