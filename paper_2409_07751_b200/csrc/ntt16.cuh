@@ -74,10 +74,14 @@ __device__ __forceinline__ void ct_f(double &x, double &y, double2 w, const FpMo
         y = f_center(y, m);
     }
 }
+// Gentleman-Sande butterfly. The sum is recentred only when `center` (small primes
+// recentre at stages 6, 4 and 2 only: |x| stays below 6q < 2^50, inside the exact
+// range of f_mulmod and f_center); the large prime recentres every stage.
 template <bool kBig>
-__device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMod &m) {
+__device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMod &m, bool center = true) {
     const double U = x, V = y;
-    x = f_center(__dadd_rn(U, V), m);
+    const double sum = __dadd_rn(U, V);
+    x = (kBig || center) ? f_center(sum, m) : sum;
     y = f_mulmod(__dsub_rn(U, V), w.x, w.y, m.q);
     if (kBig) y = f_center(y, m);
 }
@@ -113,7 +117,9 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
             if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m);
     }
 #pragma unroll
-    for (int v = 0; v < 16; ++v) inter[(16 * k + v) * 256 + col] = kBig ? x[v] : f_center(x[v], m);
+    // no recentre for small primes: |x| < 13 q < 2^51 and the row phase starts with the
+    // twist multiply (f_mulmod, exact for |x| < 2^51); the large prime is centred already
+    for (int v = 0; v < 16; ++v) inter[(16 * k + v) * 256 + col] = x[v];
 }
 
 // Row phase (four-step form): Z[r][c] = X[r][c] * tau(r, c) with
@@ -225,7 +231,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 128 >> sp;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[(1 << sp) + ((16 * k + v) >> (8 - sp))], m);
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[(1 << sp) + ((16 * k + v) >> (8 - sp))], m, !(sp & 1));
     }
     __syncwarp();
 #pragma unroll
@@ -238,7 +244,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m);
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m, !(sp & 1));
     }
     // stage 0 (pairs c, c+128, twiddle Ti[1]) fused with the untwist: the table holds
     // tau^-1(r, c) for c < 128 and tau^-1(r, c) * Ti[1] for c >= 128
@@ -248,8 +254,12 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
     for (int u = 0; u < 8; ++u) {
         const double2 ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
         const double U = x[u], V = x[u + 8];
-        rd[k + 16 * u] = f_center(f_mulmod(__dadd_rn(U, V), ta.x, ta.y, m.q), m);
-        rd[k + 16 * (u + 8)] = f_center(f_mulmod(__dsub_rn(U, V), tb.x, tb.y, m.q), m);
+        // |f_mulmod| < 1.5 q: small primes skip the recentre (the column phase's first GS
+        // stages keep |x| < 6 q); the large prime needs it for the next f_mulmod's range
+        const double a = f_mulmod(__dadd_rn(U, V), ta.x, ta.y, m.q);
+        const double b = f_mulmod(__dsub_rn(U, V), tb.x, tb.y, m.q);
+        rd[k + 16 * u] = kBig ? f_center(a, m) : a;
+        rd[k + 16 * (u + 8)] = kBig ? f_center(b, m) : b;
     }
 }
 
@@ -266,7 +276,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m);
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m, !(s & 1));
     }
 #pragma unroll
     for (int v = 0; v < 16; ++v) sm[(16 * k + v) * kTc + c] = x[v];
@@ -278,7 +288,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m);
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m, !(s & 1));
     }
     // stage 0 (twiddle Ti[1]) fused with the N^-1 scaling: niw = N^-1 * Ti[1]
 #pragma unroll
