@@ -56,6 +56,12 @@ __device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo, const Mo
 __device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const ModQ &m) {
     return reduce128(__umul64hi(a, b), a * b, m);
 }
+// any signed 64-bit value mod q (Barrett, no 64-bit division)
+__device__ __forceinline__ uint64_t smod_q(int64_t v, const ModQ &m) {
+    const uint64_t a = v < 0 ? 0ull - (uint64_t)v : (uint64_t)v;
+    const uint64_t r = reduce128(0, a, m);
+    return (v < 0 && r) ? m.q - r : r;
+}
 // 128-bit accumulate
 __device__ __forceinline__ void mac128(uint64_t &hi, uint64_t &lo, uint64_t a, uint64_t b) {
     uint64_t l = a * b, h = __umul64hi(a, b);
@@ -139,10 +145,8 @@ __host__ __device__ __forceinline__ uint64_t hk_rng64(uint64_t seed, uint64_t st
 __device__ __forceinline__ int64_t cbd21(uint64_t x) {
     return (int64_t)__popcll(x & 0x1FFFFFull) - (int64_t)__popcll((x >> 21) & 0x1FFFFFull);
 }
-__device__ __forceinline__ uint64_t smod_dev(int64_t v, uint64_t q) {
-    if (v >= 0) return (uint64_t)v % q;
-    uint64_t m = (uint64_t)(-(v + 1)) % q;
-    return q - 1 - m;
+__device__ __forceinline__ uint64_t smod_dev(int64_t v, uint64_t q) {  // |v| < q only (sampled noise)
+    return v < 0 ? q - (uint64_t)(-v) : (uint64_t)v;
 }
 enum { ST_SECRET = 1, ST_ENC_A = 2, ST_ENC_E = 3, ST_KEY_A = 0x100, ST_KEY_E = 0x200 };
 

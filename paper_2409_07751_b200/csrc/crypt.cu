@@ -57,9 +57,9 @@ __global__ void ks_sample(uint64_t *__restrict__ b, uint64_t *__restrict__ a, ui
     if (gid >= (long long)rows * N) return;
     const int r = (int)(gid >> log_n), k = (int)(gid & (N - 1));
     const int m = key_row_mod(r, top, n_q);
-    const uint64_t q = mq[m].q;
-    a[gid] = hk_rng64(seed, stream_a, (uint64_t)m * N + k) % q;
-    b[gid] = smod_dev(cbd21(hk_rng64(seed, stream_e, (uint64_t)k)), q);
+    const ModQ mm = mq[m];
+    a[gid] = reduce128(0, hk_rng64(seed, stream_a, (uint64_t)m * N + k), mm);  // == rng % q (exact Barrett)
+    b[gid] = smod_dev(cbd21(hk_rng64(seed, stream_e, (uint64_t)k)), mm.q);
 }
 
 // b = e_ntt - a*s (+ P*s' on digit limbs); s, sp are full [n_mod][N]
@@ -86,9 +86,9 @@ __global__ void enc_sample(uint64_t *__restrict__ c0, uint64_t *__restrict__ c1,
     const int k = (int)(gid & (N - 1));
     const long long lb = gid >> log_n;
     const int l = (int)(lb / B), b = (int)(lb - (long long)l * B);
-    const uint64_t q = mq[l].q;
-    c1[gid] = hk_rng64(seed, ST_ENC_A, ((uint64_t)b * nl + l) * N + k) % q;
-    c0[gid] = smod_dev(cbd21(hk_rng64(seed, ST_ENC_E, (uint64_t)b * N + k)), q);
+    const ModQ mm = mq[l];
+    c1[gid] = reduce128(0, hk_rng64(seed, ST_ENC_A, ((uint64_t)b * nl + l) * N + k), mm);  // == rng % q
+    c0[gid] = smod_dev(cbd21(hk_rng64(seed, ST_ENC_E, (uint64_t)b * N + k)), mm.q);
 }
 
 __global__ void enc_finish(uint64_t *__restrict__ c0, const uint64_t *__restrict__ c1,

@@ -80,10 +80,10 @@ __global__ void round_to_limbs(const double2 *__restrict__ w, int S, int log_n, 
     const long long ci = __double2ll_rn(__dmul_rn(__dmul_rn(x.y, inv_s), scale));
     const int N = 1 << log_n;
     for (int l = 0; l < n_limbs; ++l) {
-        const uint64_t q = mq[l].q;
+        const ModQ m = mq[l];
         uint64_t *dst = pt + ((size_t)l * B + b) * N;
-        dst[i] = smod_dev(cr, q);
-        dst[i + S] = smod_dev(ci, q);
+        dst[i] = smod_q(cr, m);
+        dst[i + S] = smod_q(ci, m);
     }
 }
 
