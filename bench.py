@@ -176,7 +176,7 @@ def run_product(args):
     del outs
     err = None
     gpath = os.path.join(ROOT, "tests", "golden", f"{args.config}.npz")
-    if os.path.exists(gpath) and args.log_n == (17 if args.config == "c5" else 16):
+    if os.path.exists(gpath):  # decrypted values: comparable at any ring degree
         gold = np.load(gpath)["mirrored"]
         n = min(B, gold.shape[0])
         err = float(np.max(np.abs(dec[:n] - gold[:n])))

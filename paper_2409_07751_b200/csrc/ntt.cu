@@ -65,62 +65,13 @@ __global__ void scale_ninv(uint64_t *__restrict__ buf, int limb0, int B, int log
     buf[gid] = mul_shoup(buf[gid], ni.x, ni.y, mq[m].q);
 }
 
-// ---------------------------------------------------------------- N = 2^17
-// Forward: stage 0 (pairs i, i + H, twiddle w = psi^H) fused with the pre-twist
-// that turns each half into a 2^16 negacyclic transform with root psi^2:
-//   half 0: (x_i + w x_{i+H}) psi^-i,  half 1: (x_i - w x_{i+H}) psi^i.
-// The 2^16 kernel then leaves half h in positions [hH, (h+1)H) in exactly the
-// 2^17 bit-reversed order (brv17(j) = 2 brv16(j) + h). Inverse: the 2^16
-// inverse per half, then x_i = (z0 psi^i + z1 psi^-i) / 2,
-// x_{i+H} = (z0 psi^i - z1 psi^-i) / (2 w).
-constexpr int kH17 = 1 << 16;
-
-__global__ void ntt17_pre(uint64_t *__restrict__ buf, int limb0, int B, const ulonglong2 *__restrict__ t17,
-                          const ulonglong2 *__restrict__ w17, const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;
-    const long long poly = gid >> 16;  // l * B + b
-    const int i = (int)(gid & (kH17 - 1));
-    const int m = limb0 + (int)(poly / B);
-    const uint64_t q = mq[m].q;
-    uint64_t *a = buf + (poly << 17);
-    const ulonglong2 w = w17[2 * m];
-    const ulonglong2 *tm = t17 + (size_t)m * 4 * kH17;
-    const uint64_t x = a[i], t = mul_shoup(a[i + kH17], w.x, w.y, q);
-    const ulonglong2 pa = tm[i], pb = tm[kH17 + i];
-    a[i] = mul_shoup(add_mod(x, t, q), pa.x, pa.y, q);
-    a[i + kH17] = mul_shoup(sub_mod(x, t, q), pb.x, pb.y, q);
-}
-
-__global__ void ntt17_post(uint64_t *__restrict__ buf, int limb0, int B, const ulonglong2 *__restrict__ t17,
-                           const ulonglong2 *__restrict__ w17, const ModQ *__restrict__ mq, long long total) {
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= total) return;
-    const long long poly = gid >> 16;
-    const int i = (int)(gid & (kH17 - 1));
-    const int m = limb0 + (int)(poly / B);
-    const uint64_t q = mq[m].q;
-    uint64_t *a = buf + (poly << 17);
-    const ulonglong2 wi = w17[2 * m + 1];
-    const ulonglong2 *tm = t17 + (size_t)m * 4 * kH17;
-    const ulonglong2 qa = tm[2 * kH17 + i], qb = tm[3 * kH17 + i];
-    const uint64_t u0 = mul_shoup(a[i], qa.x, qa.y, q), u1 = mul_shoup(a[i + kH17], qb.x, qb.y, q);
-    a[i] = add_mod(u0, u1, q);
-    a[i + kH17] = mul_shoup(sub_mod(u0, u1, q), wi.x, wi.y, q);
-}
-
 }  // namespace
 
 int ntt_fwd_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int B, int) {
     if (n_limbs <= 0 || B <= 0) return HK_OK;
-    if (c->log_n == kLogN16) {
-        return ntt16::launch_fwd(c, buf, limb0, n_limbs, B, ntt16::ProPlain{buf}, ntt16::EpiPlain{buf});
-    } else if (c->log_n == kLogN16 + 1) {
-        const long long total = (long long)n_limbs * B * kH17;
-        ntt17_pre<<<hk_grid(total, 256), 256, 0, c->stream>>>(buf, limb0, B, c->d_n17, c->d_n17w, c->d_modq, total);
-        ++c->launches;
-        HK_LAUNCH_CHECK(c, "ntt17 pre");
-        return ntt16::launch_fwd(c, buf, limb0, n_limbs, 2 * B, ntt16::ProPlain{buf}, ntt16::EpiPlain{buf});
+    if (ntt16::fused(c)) {
+        return ntt16::launch_fwd(c, buf, limb0, n_limbs, B, ntt16::ProPlain{buf, c->log_n},
+                                 ntt16::EpiPlain{buf, c->log_n});
     } else {
         const long long total = (long long)n_limbs * B * (c->n / 2);
         for (int s = 0; s < c->log_n; ++s) {
@@ -135,14 +86,9 @@ int ntt_fwd_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int B, int)
 
 int ntt_inv_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int B, int) {
     if (n_limbs <= 0 || B <= 0) return HK_OK;
-    if (c->log_n == kLogN16) {
-        return ntt16::launch_inv(c, buf, limb0, n_limbs, B, ntt16::ProPlain{buf}, ntt16::EpiPlain{buf});
-    } else if (c->log_n == kLogN16 + 1) {
-        int rc = ntt16::launch_inv(c, buf, limb0, n_limbs, 2 * B, ntt16::ProPlain{buf}, ntt16::EpiPlain{buf});
-        if (rc) return rc;
-        const long long total = (long long)n_limbs * B * kH17;
-        ntt17_post<<<hk_grid(total, 256), 256, 0, c->stream>>>(buf, limb0, B, c->d_n17, c->d_n17w, c->d_modq, total);
-        ++c->launches;
+    if (ntt16::fused(c)) {
+        return ntt16::launch_inv(c, buf, limb0, n_limbs, B, ntt16::ProPlain{buf, c->log_n},
+                                 ntt16::EpiPlain{buf, c->log_n});
     } else {
         const long long total = (long long)n_limbs * B * (c->n / 2);
         for (int s = c->log_n - 1; s >= 0; --s) {

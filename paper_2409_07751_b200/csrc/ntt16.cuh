@@ -330,19 +330,93 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
 }
 
 // ---------------------------------------------------------------- functors
+// (l, P, idx): limb l of the launch, polynomial P = l * B + b, coefficient idx < N
+// of the context's ring (N = 2^16 or 2^17).
 struct ProPlain {  // in[P][idx]
     const uint64_t *in;
-    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const { return in[P * kN + idx]; }
+    int log_n = kLogN;
+    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const { return in[(P << log_n) + idx]; }
 };
 struct EpiPlain {  // out[P][idx] = v
     uint64_t *out;
-    __device__ __forceinline__ void operator()(int, long long P, int idx, uint64_t v) const { out[P * kN + idx] = v; }
+    int log_n = kLogN;
+    __device__ __forceinline__ void operator()(int, long long P, int idx, uint64_t v) const {
+        out[(P << log_n) + idx] = v;
+    }
 };
 
+// ---------------------------------------------------------------- N = 2^17
+// One radix-2 stage (pairs i, i + H, twiddle w = psi^H) plus a twist makes each
+// half a 2^16 negacyclic transform with root psi^2 (half 0: (x_i + w x_{i+H}) psi^-i,
+// half 1: (x_i - w x_{i+H}) psi^i), run by the kernels above as 2B sub-polynomials
+// 2b + h of the same buffer; brv17(j) = 2 brv16(j) + h puts half h in positions
+// [hH, (h+1)H) in exactly the 2^17 bit-reversed order. The inverse runs the 2^16
+// inverse per half, then x_i = (z0 psi^i + z1 psi^-i) / 2, x_{i+H} = (z0 psi^i -
+// z1 psi^-i) / (2w). Prologue / epilogue functors see the 2^17 indexing.
+constexpr int kH17 = 1 << 16;
+
+template <class Epi>
+struct EpiHalf {  // sub-polynomial P2 = l * 2B + 2b + h, idx < 2^16 -> (l * B + b, h * H + idx)
+    Epi epi;
+    int B;
+    __device__ __forceinline__ void operator()(int l, long long P2, int idx, uint64_t v) const {
+        const long long pb = P2 - (long long)l * 2 * B;
+        epi(l, (long long)l * B + (pb >> 1), (int)((pb & 1) << 16) + idx, v);
+    }
+};
+template <class Pro>
+struct ProHalf {
+    Pro pro;
+    int B;
+    __device__ __forceinline__ uint64_t operator()(int l, long long P2, int idx) const {
+        const long long pb = P2 - (long long)l * 2 * B;
+        return pro(l, (long long)l * B + (pb >> 1), (int)((pb & 1) << 16) + idx);
+    }
+};
+
+template <class Pro>
+__global__ void k17_pre(Pro pro, uint64_t *__restrict__ inter, int limb0, int B, const ulonglong2 *__restrict__ t17,
+                        const ulonglong2 *__restrict__ w17, const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;
+    const long long P = gid >> 16;  // l * B + b
+    const int i = (int)(gid & (kH17 - 1));
+    const int l = (int)(P / B), m = limb0 + l;
+    const uint64_t q = mq[m].q;
+    const ulonglong2 w = w17[2 * m];
+    const ulonglong2 *tm = t17 + (size_t)m * 4 * kH17;
+    const uint64_t x = pro(l, P, i), t = mul_shoup(pro(l, P, i + kH17), w.x, w.y, q);
+    const ulonglong2 pa = tm[i], pb = tm[kH17 + i];
+    uint64_t *a = inter + (P << 17);
+    a[i] = mul_shoup(add_mod(x, t, q), pa.x, pa.y, q);
+    a[i + kH17] = mul_shoup(sub_mod(x, t, q), pb.x, pb.y, q);
+}
+
+template <class Epi>
+__global__ void k17_post(Epi epi, const uint64_t *__restrict__ inter, int limb0, int B,
+                         const ulonglong2 *__restrict__ t17, const ulonglong2 *__restrict__ w17,
+                         const ModQ *__restrict__ mq, long long total) {
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= total) return;
+    const long long P = gid >> 16;
+    const int i = (int)(gid & (kH17 - 1));
+    const int l = (int)(P / B), m = limb0 + l;
+    const uint64_t q = mq[m].q;
+    const ulonglong2 wi = w17[2 * m + 1];
+    const ulonglong2 *tm = t17 + (size_t)m * 4 * kH17;
+    const ulonglong2 qa = tm[2 * kH17 + i], qb = tm[3 * kH17 + i];
+    const uint64_t *a = inter + (P << 17);
+    const uint64_t u0 = mul_shoup(a[i], qa.x, qa.y, q), u1 = mul_shoup(a[i + kH17], qb.x, qb.y, q);
+    epi(l, P, i, add_mod(u0, u1, q));
+    epi(l, P, i + kH17, mul_shoup(sub_mod(u0, u1, q), wi.x, wi.y, q));
+}
+
 // ---------------------------------------------------------------- launchers
+// Forward / inverse NTT of n_limbs x B polynomials (primes limb0 ..) of the
+// context's ring (2^16, or 2^17 via the radix-2 pass), input through `pro`,
+// output through `epi`; `inter` ([n_limbs][B][N] words) may alias the output.
 template <class Pro, class Epi>
-inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
-    if (n_limbs <= 0 || B <= 0) return HK_OK;
+inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(fwd_kernel<Pro, Epi>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -359,8 +433,7 @@ inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B,
 }
 
 template <class Pro, class Epi>
-inline int launch_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
-    if (n_limbs <= 0 || B <= 0) return HK_OK;
+inline int launch16_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(inv_kernel<Pro, Epi>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -373,6 +446,35 @@ inline int launch_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B,
                                                              (const FpMod *)c->d_fmod, pro, epi);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "ntt16 inv");
+    return HK_OK;
+}
+
+// rings served by the fused kernels
+inline bool fused(const hk_ctx *c) { return c->log_n == kLogN || c->log_n == kLogN + 1; }
+
+template <class Pro, class Epi>
+inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
+    if (n_limbs <= 0 || B <= 0) return HK_OK;
+    if (c->log_n == kLogN) return launch16_fwd(c, inter, limb0, n_limbs, B, pro, epi);
+    const long long total = (long long)n_limbs * B * kH17;
+    k17_pre<Pro><<<hk_grid(total, 256), 256, 0, c->stream>>>(pro, inter, limb0, B, c->d_n17, c->d_n17w, c->d_modq,
+                                                             total);
+    ++c->launches;
+    HK_LAUNCH_CHECK(c, "ntt17 pre");
+    return launch16_fwd(c, inter, limb0, n_limbs, 2 * B, ProPlain{inter, kLogN}, EpiHalf<Epi>{epi, B});
+}
+
+template <class Pro, class Epi>
+inline int launch_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
+    if (n_limbs <= 0 || B <= 0) return HK_OK;
+    if (c->log_n == kLogN) return launch16_inv(c, inter, limb0, n_limbs, B, pro, epi);
+    int rc = launch16_inv(c, inter, limb0, n_limbs, 2 * B, ProHalf<Pro>{pro, B}, EpiPlain{inter, kLogN});
+    if (rc) return rc;
+    const long long total = (long long)n_limbs * B * kH17;
+    k17_post<Epi><<<hk_grid(total, 256), 256, 0, c->stream>>>(epi, inter, limb0, B, c->d_n17, c->d_n17w, c->d_modq,
+                                                              total);
+    ++c->launches;
+    HK_LAUNCH_CHECK(c, "ntt17 post");
     return HK_OK;
 }
 

@@ -530,20 +530,20 @@ struct EpiScale {
     uint64_t *out;
     const uint64_t *inv, *inv_sh;
     const ModQ *mq;
-    int mi0;
+    int mi0, log_n;
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
-        out[P * ntt16::kN + idx] = mul_shoup(v, inv[l], inv_sh[l], mq[mi0 + l].q);
+        out[(P << log_n) + idx] = mul_shoup(v, inv[l], inv_sh[l], mq[mi0 + l].q);
     }
 };
 // same, per-digit tables (ModUp sources at one level)
 struct EpiScaleDigits {
     uint64_t *out;
     const uint64_t *inv[8], *inv_sh[8];
-    int alpha;
+    int alpha, log_n;
     const ModQ *mq;
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         const int j = l / alpha, i = l - j * alpha;
-        out[P * ntt16::kN + idx] = mul_shoup(v, inv[j][i], inv_sh[j][i], mq[l].q);
+        out[(P << log_n) + idx] = mul_shoup(v, inv[j][i], inv_sh[j][i], mq[l].q);
     }
 };
 
@@ -629,9 +629,9 @@ struct Tensor {
 struct ProD2 {
     Tensor T;
     long long BN;
-    int B;
+    int B, log_n;
     __device__ __forceinline__ uint64_t operator()(int l, long long P, int idx) const {
-        return T.d(2, l, (long long)l * BN + (P - (long long)l * B) * ntt16::kN + idx);
+        return T.d(2, l, (long long)l * BN + ((P - (long long)l * B) << log_n) + idx);
     }
 };
 // NTT epilogue, merged ModDown + rescale with d_p formed from (a, b)
@@ -660,8 +660,9 @@ struct ProMdYT {
     long long BN;
     const ulonglong2 *pmod;
     const ModQ *mq;
+    int log_n;
     __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
-        const long long o = (long long)l * BN + P * ntt16::kN + idx;
+        const long long o = (long long)l * BN + (P << log_n) + idx;
         const uint64_t q = mq[l].q;
         const ulonglong2 Pm = pmod[l];
         return add_mod(acc[o], mul_shoup(T.d(which, l, o), Pm.x, Pm.y, q), q);
@@ -673,9 +674,9 @@ struct ProMdY {
     const uint64_t *acc_l, *d_l;
     const ulonglong2 *pmod;
     const ModQ *mq;
-    int l;
+    int l, log_n;
     __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
-        const long long o = P * ntt16::kN + idx;
+        const long long o = (P << log_n) + idx;
         const uint64_t q = mq[l].q;
         const ulonglong2 Pm = pmod[l];
         return add_mod(acc_l[o], mul_shoup(d_l[o], Pm.x, Pm.y, q), q);
@@ -763,7 +764,7 @@ template <int KIND>
 static int rescale_fused(hk_ctx *c, const RsSrc<KIND> &src, int l, int B, uint64_t *out, uint64_t *scratch) {
     const long long BN = (long long)B * c->n;
     uint64_t *L = scratch, *inter = scratch + 2 * BN;
-    int rc = ntt16::launch_inv(c, L, l, 1, 2 * B, ProLast<KIND>{src, B}, ntt16::EpiPlain{L});
+    int rc = ntt16::launch_inv(c, L, l, 1, 2 * B, ProLast<KIND>{src, B}, ntt16::EpiPlain{L, c->log_n});
     if (rc) return rc;
     ProRsBcast pro{L, c->mod_h[l], 2 * B, c->log_n, c->d_modq};
     EpiRescale<KIND> epi{src, out, c->d_rs_qinv + (size_t)l * c->n_q, B};
@@ -815,20 +816,21 @@ static KsBufs ks_bufs(const hk_ctx *c, int l, int B, uint64_t *scratch) {
 static int ks_modup(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
     const long long BN = (long long)B * c->n;
-    const bool fused = c->log_n == ntt16::kLogN;
+    const bool fused = ntt16::fused(c);
     int rc;
     if (fused) {
         EpiScaleDigits esd;
         memset(&esd, 0, sizeof esd);
         esd.out = kb.dc;
         esd.alpha = c->alpha;
+        esd.log_n = c->log_n;
         esd.mq = c->d_modq;
         if (nd > 8) return hk_fail(c, HK_E_ARG, "more than 8 key-switching digits");
         for (int j = 0; j < nd; ++j) {
             esd.inv[j] = c->modup[l][j].d_inv;
             esd.inv_sh[j] = c->modup[l][j].d_inv_sh;
         }
-        if ((rc = ntt16::launch_inv(c, kb.dc, 0, l + 1, B, ntt16::ProPlain{d}, esd))) return rc;
+        if ((rc = ntt16::launch_inv(c, kb.dc, 0, l + 1, B, ntt16::ProPlain{d, c->log_n}, esd))) return rc;
     } else {
         HK_CUDA(c, cudaMemcpyAsync(kb.dc, d, sizeof(uint64_t) * (l + 1) * BN, cudaMemcpyDeviceToDevice, c->stream));
         if ((rc = ntt_inv_launch(c, kb.dc, 0, l + 1, B, 0))) return rc;
@@ -888,12 +890,12 @@ static int ks_moddown(hk_ctx *c, const uint64_t *a, int l, int B, const KsBufs &
     const long long BN = (long long)B * c->n;
     const ConvTable &T = c->moddown;
     int rc;
-    if (c->log_n == ntt16::kLogN) {
-        EpiScale es{kb.sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q};
-        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{a + (size_t)(l + 1) * BN}, es))) return rc;
+    if (ntt16::fused(c)) {
+        EpiScale es{kb.sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q, c->log_n};
+        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{a + (size_t)(l + 1) * BN, c->log_n}, es))) return rc;
         if ((rc = conv_launch(c, T, kb.sp, kb.conv, 1, l, BN, l + 1, 1))) return rc;
         EpiModDown epi{a, add0, out, c->d_pinv, c->d_modq, g, B, c->log_n, BN};
-        return ntt16::launch_fwd(c, kb.conv, 0, l + 1, B, ntt16::ProPlain{kb.conv}, epi);
+        return ntt16::launch_fwd(c, kb.conv, 0, l + 1, B, ntt16::ProPlain{kb.conv, c->log_n}, epi);
     }
     HK_CUDA(c, cudaMemcpyAsync(kb.sp, a + (size_t)(l + 1) * BN, sizeof(uint64_t) * np * BN, cudaMemcpyDeviceToDevice,
                                c->stream));
@@ -915,15 +917,15 @@ static int ks_moddown_rescale(hk_ctx *c, const uint64_t *a, const uint64_t *dp, 
     const ConvTable &T = c->mdrs[l];
     const ulonglong2 *mqinv = c->d_mqinv + (size_t)l * c->n_q;
     int rc;
-    if (c->log_n == ntt16::kLogN) {
-        EpiScale es{kb.sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q};
-        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{a + (size_t)(l + 1) * BN}, es))) return rc;
-        ProMdY py{a + (size_t)l * BN, dp + (size_t)l * BN, c->d_pmod, c->d_modq, l};
-        EpiScale es2{kb.sp + (size_t)np * BN, T.d_inv + np, T.d_inv_sh + np, c->d_modq, l};
+    if (ntt16::fused(c)) {
+        EpiScale es{kb.sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q, c->log_n};
+        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{a + (size_t)(l + 1) * BN, c->log_n}, es))) return rc;
+        ProMdY py{a + (size_t)l * BN, dp + (size_t)l * BN, c->d_pmod, c->d_modq, l, c->log_n};
+        EpiScale es2{kb.sp + (size_t)np * BN, T.d_inv + np, T.d_inv_sh + np, c->d_modq, l, c->log_n};
         if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * BN, l, 1, B, py, es2))) return rc;
         if ((rc = conv_launch(c, T, kb.sp, kb.conv, 1, l, BN, l, 1))) return rc;
         EpiMdRs epi{a, dp, out, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN};
-        return ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv}, epi);
+        return ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv, c->log_n}, epi);
     }
     HK_CUDA(c, cudaMemcpyAsync(kb.sp, a + (size_t)(l + 1) * BN, sizeof(uint64_t) * np * BN, cudaMemcpyDeviceToDevice,
                                c->stream));
@@ -952,13 +954,14 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
     memset(&esd, 0, sizeof esd);
     esd.out = kb.dc;
     esd.alpha = c->alpha;
+    esd.log_n = c->log_n;
     esd.mq = c->d_modq;
     if (nd > 8) return hk_fail(c, HK_E_ARG, "more than 8 key-switching digits");
     for (int j = 0; j < nd; ++j) {
         esd.inv[j] = c->modup[l][j].d_inv;
         esd.inv_sh[j] = c->modup[l][j].d_inv_sh;
     }
-    int rc = ntt16::launch_inv(c, kb.dc, 0, l + 1, B, ProD2{T, BN, B}, esd);
+    int rc = ntt16::launch_inv(c, kb.dc, 0, l + 1, B, ProD2{T, BN, B, c->log_n}, esd);
     if (rc) return rc;
     for (int j = 0; j < nd; ++j) {
         const ConvTable &Tc = c->modup[l][j];
@@ -977,15 +980,15 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
     const ulonglong2 *mqinv = c->d_mqinv + (size_t)l * c->n_q;
     for (int p = 0; p < 2; ++p) {
         const uint64_t *acc = kb.acc + (size_t)p * ne * BN;
-        EpiScale es{kb.sp, Tm.d_inv, Tm.d_inv_sh, c->d_modq, c->n_q};
-        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{acc + (size_t)(l + 1) * BN}, es)))
+        EpiScale es{kb.sp, Tm.d_inv, Tm.d_inv_sh, c->d_modq, c->n_q, c->log_n};
+        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{acc + (size_t)(l + 1) * BN, c->log_n}, es)))
             return rc;
-        ProMdYT py{acc, T, p, l, BN, c->d_pmod, c->d_modq};
-        EpiScale es2{kb.sp + (size_t)np * BN, Tm.d_inv + np, Tm.d_inv_sh + np, c->d_modq, l};
+        ProMdYT py{acc, T, p, l, BN, c->d_pmod, c->d_modq, c->log_n};
+        EpiScale es2{kb.sp + (size_t)np * BN, Tm.d_inv + np, Tm.d_inv_sh + np, c->d_modq, l, c->log_n};
         if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * BN, l, 1, B, py, es2))) return rc;
         if ((rc = conv_launch(c, Tm, kb.sp, kb.conv, 1, l, BN, l, 1))) return rc;
         EpiMdRsT epi{acc, T, p, out + (size_t)p * l * BN, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN};
-        if ((rc = ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv}, epi))) return rc;
+        if ((rc = ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv, c->log_n}, epi))) return rc;
     }
     return HK_OK;
 }
@@ -1053,7 +1056,7 @@ int hk_rescale(hk_ctx *c, const uint64_t *a, int32_t la, uint64_t *out, int32_t 
     if (la < 1 || la >= c->n_q) return hk_fail(c, HK_E_DEPTH, "rescale at level %d", la);
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "rescale workspace");
-    if (c->log_n == ntt16::kLogN) return rescale_fused(c, make_src<SRC_PLAIN>(c, a, la, B), la, B, out, ws);
+    if (ntt16::fused(c)) return rescale_fused(c, make_src<SRC_PLAIN>(c, a, la, B), la, B, out, ws);
     return rescale_launch(c, a, la, B, out, ws);
 }
 
@@ -1063,7 +1066,7 @@ int hk_mul_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, i
     if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
     if (pb != 1 && pb != B) return hk_fail(c, HK_E_LENGTH, "mul_plain: plaintext batch");
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
-    if (c->log_n == ntt16::kLogN) {
+    if (ntt16::fused(c)) {
         uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
         if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_plain workspace");
         RsSrc<SRC_MULPT> src = make_src<SRC_MULPT>(c, a, la, B);
@@ -1084,7 +1087,7 @@ int hk_mul_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
     Residues r;
     for (int l = 0; l <= la; ++l) r.v[l] = res[l];
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
-    if (c->log_n == ntt16::kLogN) {
+    if (ntt16::fused(c)) {
         uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
         if (!ws) return hk_fail(c, HK_E_NOMEM, "mul_const workspace");
         RsSrc<SRC_MULCONST> src = make_src<SRC_MULCONST>(c, a, la, B);
@@ -1104,7 +1107,7 @@ int hk_mac_plain(hk_ctx *c, const uint64_t *const *babies, const uint64_t *const
     if (la < 0 || la >= c->n_q || lp < la || n < 1 || pt_stride < 1) return hk_fail(c, HK_E_ARG, "mac_plain: args");
     if (la < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", la);
     const long long BN = (long long)B * c->n, tot = 2LL * (la + 1) * BN;
-    if (c->log_n == ntt16::kLogN && n <= kMacMax) {
+    if (ntt16::fused(c) && n <= kMacMax) {
         uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * rs_scratch_words(c, la, B));
         if (!ws) return hk_fail(c, HK_E_NOMEM, "mac_plain workspace");
         RsSrc<SRC_MAC> src = make_src<SRC_MAC>(c, babies[0], la, B);
@@ -1172,7 +1175,7 @@ int hk_mac_plain_blocks(hk_ctx *c, const uint64_t *const *babies, int32_t n, int
     uint64_t *rs = ws + (size_t)G * tot;
     for (int g = 0; g < G; ++g) {
         int rc;
-        if (c->log_n == ntt16::kLogN)
+        if (ntt16::fused(c))
             rc = rescale_fused(c, make_src<SRC_PLAIN>(c, ws + (size_t)g * tot, la, B), la, B, outs[g], rs);
         else
             rc = rescale_launch(c, ws + (size_t)g * tot, la, B, outs[g], rs);
@@ -1191,7 +1194,7 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
     uint64_t *d = ws;
     const KsBufs kb = ks_bufs(c, l, B, ws + 3 * pl);
-    if (c->log_n == ntt16::kLogN) return mul_fused(c, a, la, b, lb, l, B, kb, out);
+    if (ntt16::fused(c)) return mul_fused(c, a, la, b, lb, l, B, kb, out);
     k_tensor<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");

@@ -485,6 +485,108 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 4)
     }
 }
 
+
+// V10: persistent, software-pipelined 16-CTA clusters: the next polynomial's
+// column phase runs between the cluster barrier's arrive and wait of the current
+// one, hiding the barrier; the twiddle table is staged once per CTA.
+__device__ __forceinline__ void v10_col(const uint64_t *__restrict__ in, double *inter, long long P, int cb,
+                                        const double2 *st, const FpMod &m, double *smd) {
+    const int c = threadIdx.x & 15, k = threadIdx.x >> 4, col = cb * 16 + c;
+    double x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = u2d(in[P * kN + (k + 16 * u) * 256 + col]);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int d = 8 >> s;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (!(u & d)) ct_f<false>(x[u], x[u + d], st[(1 << s) + (u >> (4 - s))], m);
+    }
+    __syncthreads();  // previous row phase done with smd
+#pragma unroll
+    for (int u = 0; u < 16; ++u) smd[(k + 16 * u) * 16 + c] = x[u];
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = smd[(16 * k + v) * 16 + c];
+#pragma unroll
+    for (int s = 4; s < 8; ++s) {
+        const int d = 128 >> s;
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+            if (!(v & d)) ct_f<false>(x[v], x[v + d], st[(1 << s) + ((16 * k + v) >> (8 - s))], m);
+    }
+#pragma unroll
+    for (int v = 0; v < 16; ++v) inter[P * kN + (16 * k + v) * 256 + col] = x[v];
+}
+__device__ __forceinline__ void v10_row(const double *inter, uint64_t *__restrict__ out, long long P, int cb,
+                                        const double2 *__restrict__ twist, const double2 *st, const FpMod &m,
+                                        double *smd) {
+    const int rs = threadIdx.x >> 4, r = cb * 16 + rs;
+    const int k = threadIdx.x & 15;
+    double x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = __ldcg(inter + P * kN + r * 256 + k + 16 * u);
+    const double2 *tr = twist + r * 256;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const double2 t = __ldg(tr + k + 16 * u);
+        x[u] = f_mulmod(x[u], t.x, t.y, m.q);
+    }
+#pragma unroll
+    for (int sp = 0; sp < 4; ++sp) {
+        const int d = 8 >> sp;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (!(u & d)) ct_f<false>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m);
+    }
+    __syncthreads();  // column phase done with smd (it is reused as row buffers)
+    double *srow = smd + rs * kRowPad;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = x[u];
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < 16; ++v) x[v] = srow[pad16(16 * k + v)];
+#pragma unroll
+    for (int sp = 4; sp < 8; ++sp) {
+        const int d = 128 >> sp;
+#pragma unroll
+        for (int v = 0; v < 16; ++v)
+            if (!(v & d)) ct_f<false>(x[v], x[v + d], st[(1 << sp) + ((16 * k + v) >> (8 - sp))], m);
+    }
+    __syncwarp();
+    uint64_t *su = reinterpret_cast<uint64_t *>(srow);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) su[pad16(16 * k + v)] = d2canon(x[v], m);
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) out[P * kN + r * 256 + k + 16 * u] = su[pad16(k + 16 * u)];
+}
+__global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(256, 4)
+    lab_fwd10(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
+              const double2 *__restrict__ tw, const double2 *__restrict__ twist, FpMod m, int polys) {
+    extern __shared__ double smd[];
+    double2 *st = reinterpret_cast<double2 *>(smd + 16 * kRowPad);
+    const int cb = blockIdx.x & 15;
+    const int cl = blockIdx.x >> 4, ncl = gridDim.x >> 4;
+    double *inter = reinterpret_cast<double *>(inter_base);
+    st[threadIdx.x] = tw[threadIdx.x];
+    __syncthreads();
+    long long p = cl;
+    if (p >= polys) return;
+    v10_col(in, inter, p, cb, st, m, smd);
+    cl_arrive();
+    for (;;) {
+        const long long pn = p + ncl;
+        const bool more = pn < polys;
+        if (more) v10_col(in, inter, pn, cb, st, m, smd);
+        cl_wait();
+        v10_row(inter, out, p, cb, twist, st, m, smd);
+        if (!more) break;
+        cl_arrive();
+        p = pn;
+    }
+}
+
 #define CK(x)                                                                    \
     do {                                                                         \
         cudaError_t e_ = (x);                                                    \
@@ -611,6 +713,24 @@ int main(int argc, char **argv) {
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         printf("%-22s %8.3f ms  %6.3f us/limb-poly\n", "V9 const twiddles", ms / reps, 1e3 * ms / reps / polys);
+    }
+    for (int cpm : {4, 8, 16}) {  // clusters per 148 SMs x 4 CTAs: 37 resident clusters
+        CK(cudaFuncSetAttribute(lab_fwd10, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(lab_fwd10, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem8));
+        const int ncl = 37 * cpm / 4;
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        lab_fwd10<<<16 * ncl, 256, kSmem8>>>(in, inter, out, tw, twist, m, polys);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(a);
+        for (int i = 0; i < reps; ++i) lab_fwd10<<<16 * ncl, 256, kSmem8>>>(in, inter, out, tw, twist, m, polys);
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("V10 pipelined ncl=%-4d %8.3f ms  %6.3f us/limb-poly\n", ncl, ms / reps, 1e3 * ms / reps / polys);
     }
     for (int i = 0; i < 5; ++i)
         printf("%-22s %8.3f ms  %6.3f us/limb-poly\n", names[i], t[i], 1e3 * t[i] / polys);
