@@ -155,7 +155,7 @@ def run_product(args):
     inputs = inputs[:B] if B <= inputs.shape[0] else np.resize(inputs, (B, inputs.shape[1]))
     pcfg = inf.PipelineConfig()
     depth = inf.plan_model(model, pcfg).total
-    params = kan_params(depth, log_n=args.log_n)
+    params = kan_params(depth, log_n=args.log_n, dnum=args.dnum)
     be = make_backend(BackendConfig(slot_count=params.slot_count, depth_budget=depth, rng_seed=rank),
                       params=params, device=local)
     eng = be.engine
@@ -438,7 +438,7 @@ def cpu_baseline(args, budget_s: float = 20.0) -> dict:
     cfg, model, inputs = configs.workload(args.config, batch=1)
     pcfg = inf.PipelineConfig()
     depth = inf.plan_model(model, pcfg).total
-    params = kan_params(depth, log_n=args.log_n)
+    params = kan_params(depth, log_n=args.log_n, dnum=args.dnum)
     t_setup = time.perf_counter()
     be = BudgetBackend(BackendConfig(slot_count=params.slot_count, depth_budget=depth), params,
                        engine=OracleEngine(params))
@@ -606,6 +606,7 @@ def main():
     ap.add_argument("--impl", choices=("product", "reference"), default="product")
     ap.add_argument("--config", default="c1")
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--dnum", type=int, default=3, help="key-switching digits over the full chain")
     ap.add_argument("--chunk", type=int, default=None,
                     help="ciphertexts per batched launch (default 32; 8 for c5 at N=2^17)")
     ap.add_argument("--log-n", type=int, default=None,

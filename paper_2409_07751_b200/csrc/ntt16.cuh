@@ -89,14 +89,23 @@ __device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMo
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// stage the shared 256-entry twiddle table of prime mi into shared memory
+__device__ __forceinline__ void stage_table(double2 *st, const double2 *__restrict__ T) {
+    for (int i = threadIdx.x; i < 256; i += kTh) st[i] = T[i];
+}
+
 // ---------------------------------------------------------------- forward
+// The column data is loaded before the twiddle table is staged (the table's
+// load latency and the CTA barrier overlap the data loads).
 template <bool kBig, class Pro>
 __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, double *inter, int tile,
-                                         const double2 *__restrict__ T, const FpMod &m, double *sm) {
+                                         double2 *T, const double2 *__restrict__ Tg, const FpMod &m, double *sm) {
     const int c = threadIdx.x % kTc, k = threadIdx.x / kTc, col = tile * kTc + c;
     double x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = u2d(pro(l, P, (k + 16 * u) * 256 + col));
+    stage_table(T, Tg);
+    __syncthreads();
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         const int d = 8 >> s;
@@ -179,11 +188,6 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
     for (int u = 0; u < 16; ++u) epi(l, P, r * 256 + k + 16 * u, su[pad16(k + 16 * u)]);
 }
 
-// stage the shared 256-entry twiddle table of prime mi into shared memory
-__device__ __forceinline__ void stage_table(double2 *st, const double2 *__restrict__ T) {
-    for (int i = threadIdx.x; i < 256; i += kTh) st[i] = T[i];
-}
-
 template <class Pro, class Epi>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
     fwd_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ tw,
@@ -196,16 +200,14 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
     const FpMod m = fm[mi];
     const double2 *T = tw + (size_t)mi * kN;
     const double2 *tau = twist + (size_t)mi * kN;
-    stage_table(st, T);
-    __syncthreads();
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
     const int rs = threadIdx.x >> 4, r = c * kTc + rs;
     if (m.q < (double)kSmallPrime) {
-        fwd_cols<false>(pro, l, P, inter, c, st, m, smd);
+        fwd_cols<false>(pro, l, P, inter, c, st, T, m, smd);
         cluster_sync_all();
         fwd_row<false>(epi, l, P, inter, r, tau, st, m, smd + rs * kRowPad);
     } else {
-        fwd_cols<true>(pro, l, P, inter, c, st, m, smd);
+        fwd_cols<true>(pro, l, P, inter, c, st, T, m, smd);
         cluster_sync_all();
         fwd_row<true>(epi, l, P, inter, r, tau, st, m, smd + rs * kRowPad);
     }
