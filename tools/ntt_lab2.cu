@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 
 #include "ntt16.cuh"
 
@@ -89,6 +90,118 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, MINB)
         cluster_sync_all();
     }
     fwd_row<false>(EpiPlain{out, kLogN}, 0, P, inter, r, twist, st, m, smd + rs * kRowPad);
+}
+
+// persistent: each cluster loops over polynomials P = cluster, cluster + n_cl, ...;
+// STAGGER > 0 delays cluster c by (c % 4) * STAGGER ns once at start so the four
+// CTAs resident on an SM run their latency phases at different times.
+template <int STAGGER>
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
+    lab_persist(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
+                const double2 *__restrict__ tw, const double2 *__restrict__ twist, FpMod m, int polys) {
+    extern __shared__ double smd[];
+    double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
+    const int c = blockIdx.x % kCl;
+    const int cl = blockIdx.x / kCl, ncl = gridDim.x / kCl;
+    if (STAGGER > 0) __nanosleep((unsigned)((cl & 3) * STAGGER));
+    stage_table(st, tw);
+    __syncthreads();
+    const int rs = threadIdx.x >> 4, r = c * kTc + rs;
+    for (long long P = cl; P < polys; P += ncl) {
+        double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
+        lab_cols<0>(in, P, inter, c, st, m, smd);
+        cluster_sync_all();
+        fwd_row<false>(EpiPlain{out, kLogN}, 0, P, inter, r, twist, st, m, smd + rs * kRowPad);
+        __syncthreads();  // row buffers are reused by the next column phase
+    }
+}
+
+template <int STAGGER>
+void run_persist(const char *name, int polys, int ncl, const uint64_t *in, uint64_t *inter, uint64_t *out,
+                 const double2 *tw, const double2 *twist, FpMod m, int reps) {
+    CK(cudaFuncSetAttribute(lab_persist<STAGGER>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(lab_persist<STAGGER>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    const float ms = time_it(
+        [&] { lab_persist<STAGGER><<<kCl * ncl, kTh, kSmem>>>(in, inter, out, tw, twist, m, polys); }, reps);
+    printf("%-26s ncl=%-4d %8.3f ms  %6.3f us/limb-poly\n", name, ncl, ms, 1e3 * ms / polys);
+}
+
+// production-shaped kernel that records each CTA's start / end (globaltimer, ns)
+// and SM id, to measure how many CTAs are co-resident
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
+    lab_timed(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
+              const double2 *__restrict__ tw, const double2 *__restrict__ twist, FpMod m, ulonglong2 *rec, int *smid) {
+    extern __shared__ double smd[];
+    const unsigned long long t0 = gtime();
+    double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
+    const int c = blockIdx.x % kCl;
+    const long long P = blockIdx.x / kCl;
+    stage_table(st, tw);
+    __syncthreads();
+    double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
+    const int rs = threadIdx.x >> 4, r = c * kTc + rs;
+    lab_cols<0>(in, P, inter, c, st, m, smd);
+    cluster_sync_all();
+    fwd_row<false>(EpiPlain{out, kLogN}, 0, P, inter, r, twist, st, m, smd + rs * kRowPad);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        rec[blockIdx.x] = make_ulonglong2(t0, gtime());
+        int id;
+        asm("mov.u32 %0, %%smid;" : "=r"(id));
+        smid[blockIdx.x] = id;
+    }
+}
+
+// cooperative persistent kernel without clusters: groups of 16 CTAs (one
+// polynomial at a time) joined by a self-resetting software barrier in global
+// memory; the grid fills every SM (4 CTAs each), unlike 16-CTA clusters which
+// leave whole SMs idle when a GPC's SM count is not a multiple of 4.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void group_bar(unsigned *cnt, unsigned *gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire(gen);
+        __threadfence();
+        if (atomicAdd(cnt, 1u) == kCl - 1) {
+            atomicExch(cnt, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (ld_acquire(gen) == g) {
+            }
+        }
+    }
+    __syncthreads();
+}
+template <int SLEEP>
+__global__ void __launch_bounds__(kTh, 4)
+    lab_coop(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
+             const double2 *__restrict__ tw, const double2 *__restrict__ twist, FpMod m, int polys, unsigned *bars) {
+    extern __shared__ double smd[];
+    double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
+    const int c = blockIdx.x % kCl;
+    const int grp = blockIdx.x / kCl, ngrp = gridDim.x / kCl;
+    unsigned *cnt = bars + 64 * grp, *gen = cnt + 32;
+    if (SLEEP > 0) __nanosleep((unsigned)((blockIdx.x / (gridDim.x / 4)) * SLEEP));
+    stage_table(st, tw);
+    __syncthreads();
+    const int rs = threadIdx.x >> 4, r = c * kTc + rs;
+    for (long long P = grp; P < polys; P += ngrp) {
+        double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
+        lab_cols<0>(in, P, inter, c, st, m, smd);
+        group_bar(cnt, gen);
+        fwd_row<false>(EpiPlain{out, kLogN}, 0, P, inter, r, twist, st, m, smd + rs * kRowPad);
+        __syncthreads();
+    }
 }
 
 template <class K>
@@ -169,6 +282,91 @@ int main(int argc, char **argv) {
             },
             reps);
         printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "P production inverse", ms, 1e3 * ms / polys);
+    }
+    {
+        int ncl = 0;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kCl * 1024);
+        cfg.blockDim = dim3(kTh);
+        cfg.dynamicSmemBytes = kSmem;
+        cudaLaunchAttribute at;
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = kCl;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        CK(cudaFuncSetAttribute(lab_persist<0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(lab_persist<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        CK(cudaOccupancyMaxActiveClusters(&ncl, (void *)lab_persist<0>, &cfg));
+        printf("max active 16-CTA clusters: %d\n", ncl);
+        for (int f : {1, 2}) {
+            run_persist<0>("T1 persistent", polys, ncl * f, in, inter, out, tw, twist, m, reps);
+            run_persist<2000>("T2 persistent stagger 2us", polys, ncl * f, in, inter, out, tw, twist, m, reps);
+            run_persist<5000>("T3 persistent stagger 5us", polys, ncl * f, in, inter, out, tw, twist, m, reps);
+        }
+    }
+    {
+        ulonglong2 *rec;
+        int *smid;
+        CK(cudaMalloc(&rec, sizeof(ulonglong2) * kCl * polys));
+        CK(cudaMalloc(&smid, sizeof(int) * kCl * polys));
+        CK(cudaFuncSetAttribute(lab_timed, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(lab_timed, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        for (int i = 0; i < 2; ++i) lab_timed<<<kCl * polys, kTh, kSmem>>>(in, inter, out, tw, twist, m, rec, smid);
+        CK(cudaDeviceSynchronize());
+        std::vector<ulonglong2> h(kCl * polys);
+        std::vector<int> sm(kCl * polys);
+        CK(cudaMemcpy(h.data(), rec, sizeof(ulonglong2) * h.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sm.data(), smid, sizeof(int) * sm.size(), cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull, t1 = 0;
+        double life = 0;
+        for (auto &x : h) {
+            t0 = std::min(t0, (unsigned long long)x.x);
+            t1 = std::max(t1, (unsigned long long)x.y);
+            life += (double)(x.y - x.x);
+        }
+        // sample concurrency every 1 us
+        int maxc = 0;
+        double sumc = 0;
+        int ns = 0;
+        for (unsigned long long t = t0; t < t1; t += 1000, ++ns) {
+            int cnt = 0;
+            for (auto &x : h) cnt += (x.x <= t && t < x.y);
+            maxc = std::max(maxc, cnt);
+            sumc += cnt;
+        }
+        std::vector<int> per(256, 0);
+        for (int v : sm) per[v & 255]++;
+        int nsm = 0;
+        for (int v : per) nsm += v > 0;
+        printf("timed: span %.1f us, mean CTA life %.2f us, co-resident CTAs max %d mean %.1f, SMs used %d\n",
+               (t1 - t0) / 1e3, life / h.size() / 1e3, maxc, sumc / ns, nsm);
+    }
+    {
+        unsigned *bars;
+        CK(cudaMalloc(&bars, 4096 * 64 * 4));
+        CK(cudaMemset(bars, 0, 4096 * 64 * 4));
+        CK(cudaFuncSetAttribute(lab_coop<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        int per_sm = 0, sms = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lab_coop<0>, kTh, kSmem));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+        const int grid = (per_sm * sms / kCl) * kCl;
+        printf("coop: %d CTAs/SM, grid %d CTAs (%d groups)\n", per_sm, grid, grid / kCl);
+        int np = polys;
+        void *args[] = {(void *)&in, (void *)&inter, (void *)&out, (void *)&tw, (void *)&twist, (void *)&m, (void *)&np,
+                        (void *)&bars};
+        float ms = time_it(
+            [&] { CK(cudaLaunchCooperativeKernel((void *)lab_coop<0>, dim3(grid), dim3(kTh), args, kSmem, 0)); }, reps);
+        printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "T4 cooperative, software barrier", ms, 1e3 * ms / polys);
+        CK(cudaFuncSetAttribute(lab_coop<2000>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        CK(cudaFuncSetAttribute(lab_coop<4000>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        ms = time_it(
+            [&] { CK(cudaLaunchCooperativeKernel((void *)lab_coop<2000>, dim3(grid), dim3(kTh), args, kSmem, 0)); }, reps);
+        printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "T5 coop, stagger 2us per quarter", ms, 1e3 * ms / polys);
+        ms = time_it(
+            [&] { CK(cudaLaunchCooperativeKernel((void *)lab_coop<4000>, dim3(grid), dim3(kTh), args, kSmem, 0)); }, reps);
+        printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "T6 coop, stagger 4us per quarter", ms, 1e3 * ms / polys);
     }
     run_lab<0, 4>("L0 lab copy", polys, in, inter, out, tw, twist, m, reps);
     run_lab<1, 4>("L1 split barrier + L2 prefetch", polys, in, inter, out, tw, twist, m, reps);
