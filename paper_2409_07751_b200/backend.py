@@ -29,11 +29,12 @@ import hashlib
 import itertools
 import json
 import math
+import struct
 from dataclasses import dataclass, field, fields, replace
 
 import numpy as np
 
-from .errors import DepthExhausted, InputTooLong, LengthMismatch
+from .errors import CorruptFile, DepthExhausted, InputTooLong, LengthMismatch, SchemaMismatch
 from .params import CkksParams, kan_params
 
 OP_KINDS = ("add", "sub", "mul_ct", "mul_pt")
@@ -577,6 +578,70 @@ class HeBackend:
         if limbs.shape != (2, level + 1, B, self.n):
             raise LengthMismatch(f"limb array shape {limbs.shape}")
         return self._wrap(self.engine.put_u64(limbs), level, B, batched)
+
+    # ------------------------------------------------------------------
+    # ciphertext (de)serialisation (client boundary; the
+    # reference has none). Little-endian, self-describing:
+    #   magic "HKCT" | u32 version | 8-byte parameter fingerprint |
+    #   i32 level | i32 batch | i32 log_n | u8 batched | 3 pad bytes |
+    #   u64 limbs [2][level+1][batch][N] | 8-byte blake2b of all prior bytes
+    # ------------------------------------------------------------------
+    _CT_MAGIC = b"HKCT"
+    _CT_VERSION = 1
+    _CT_HEAD = struct.Struct("<4sI8siiiB3x")
+
+    def params_fingerprint(self) -> bytes:
+        """8-byte digest of the ring degree and every prime of the chain."""
+        h = hashlib.blake2b(digest_size=8)
+        h.update(struct.pack("<i", self.params.log_n))
+        h.update(np.asarray(self.params.q, dtype=np.uint64).tobytes())
+        h.update(np.asarray(self.params.p, dtype=np.uint64).tobytes())
+        return h.digest()
+
+    def serialize_ct(self, a: CipherText) -> bytes:
+        self._check_ours(a)
+        head = self._CT_HEAD.pack(self._CT_MAGIC, self._CT_VERSION, self.params_fingerprint(), a.level, a.batch,
+                                  self.params.log_n, 1 if a.batched else 0)
+        body = head + self.export_ct(a).astype("<u8", copy=False).tobytes()
+        return body + hashlib.blake2b(body, digest_size=8).digest()
+
+    def deserialize_ct(self, blob: bytes) -> CipherText:
+        """Inverse of serialize_ct. CorruptFile on a bad magic, length or
+        checksum; SchemaMismatch for another parameter set or version."""
+        blob = bytes(blob)
+        hs = self._CT_HEAD.size
+        if len(blob) < hs + 8:
+            raise CorruptFile(f"ciphertext blob of {len(blob)} bytes is shorter than its header")
+        magic, ver, fp, level, batch, log_n, batched = self._CT_HEAD.unpack_from(blob)
+        if magic != self._CT_MAGIC:
+            raise CorruptFile(f"bad magic {magic!r}")
+        if hashlib.blake2b(blob[:-8], digest_size=8).digest() != blob[-8:]:
+            raise CorruptFile("ciphertext checksum mismatch")
+        if ver != self._CT_VERSION:
+            raise SchemaMismatch(f"ciphertext format version {ver}, expected {self._CT_VERSION}")
+        if fp != self.params_fingerprint() or log_n != self.params.log_n:
+            raise SchemaMismatch("ciphertext was made under another parameter set")
+        if not 0 <= level <= self.config.depth_budget or batch < 1:
+            raise CorruptFile(f"level {level} / batch {batch} out of range")
+        want = 2 * (level + 1) * batch * self.n * 8
+        if len(blob) != hs + want + 8:
+            raise CorruptFile(f"limb payload of {len(blob) - hs - 8} bytes, expected {want}")
+        limbs = np.frombuffer(blob, dtype="<u8", count=want // 8, offset=hs)
+        limbs = limbs.reshape(2, level + 1, batch, self.n)
+        qs = np.asarray(self.params.q[:level + 1], dtype=np.uint64)
+        if np.any(limbs >= qs[None, :, None, None]):
+            raise CorruptFile("limb residue not below its prime")
+        return self.import_ct(limbs.astype(np.uint64), level, batched=bool(batched))
+
+
+def save_ciphertext(path: str, a: CipherText) -> None:
+    with open(path, "wb") as f:
+        f.write(a.backend.serialize_ct(a))
+
+
+def load_ciphertext(path: str, backend: "HeBackend") -> CipherText:
+    with open(path, "rb") as f:
+        return backend.deserialize_ct(f.read())
 
 
 CkksBackend = HeBackend

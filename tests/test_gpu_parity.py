@@ -175,3 +175,16 @@ def test_rotate_sum_bitexact(gpu_lib, log_n, depth):
     _same(g, o, g.rotate_sum(gc[:1], [0]), o.rotate_sum(oc[:1], [0]), "rotate_sum identity only")
     ref = sum(np.roll(x, -t, axis=1) for x, t in zip(xs, steps))
     np.testing.assert_allclose(g.decrypt(g.rotate_sum(gc, steps)), ref, atol=1e-6)
+
+
+def test_serialised_ciphertexts_cross_engines(gpu_lib):
+    # client boundary: bytes written by the GPU backend load into the oracle
+    # backend (same parameters and seed) and vice versa, limbs unchanged
+    g, o, p = _pair(13, 3)
+    X = np.random.default_rng(11).uniform(-1, 1, (2, p.slot_count))
+    cg = g.rotate(g.mul(g.encrypt(X), g.encrypt(X)), 3)
+    co = o.deserialize_ct(g.serialize_ct(cg))
+    assert np.array_equal(o.export_ct(co), g.export_ct(cg))
+    np.testing.assert_allclose(o.decrypt(co), np.roll(X * X, -3, axis=1), atol=1e-6)
+    back = g.deserialize_ct(o.serialize_ct(co))
+    assert np.array_equal(g.export_ct(back), g.export_ct(cg))
