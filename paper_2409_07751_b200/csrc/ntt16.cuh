@@ -1,7 +1,8 @@
 // ntt16.cuh — fused N = 2^16 negacyclic NTT kernels with prologue/epilogue hooks.
 //
-// One 16-CTA thread-block cluster (non-portable size, 256 threads per CTA,
-// four CTAs per SM) per polynomial (see ntt.cu for the stage split). The first phase reads its inputs through a prologue functor and the
+// One cluster of 2 or 4 CTAs (256 threads each, four CTAs per SM) per
+// polynomial; the polynomial is 16 column tiles / 16 row blocks of 16 (see
+// ntt.cu for the stage split). The first phase reads its inputs through a prologue functor and the
 // second phase hands canonical outputs to an epilogue functor, so element-wise
 // work that surrounds an NTT in CKKS (basis conversion, the rescale
 // remainder broadcast, plaintext products, the ModDown / rescale finish) runs
@@ -28,7 +29,7 @@ namespace ntt16 {
 
 constexpr int kLogN = 16;
 constexpr int kN = 1 << kLogN;
-constexpr int kCl = 16;                      // CTAs per cluster (non-portable size): one polynomial
+constexpr int kCl = 16;                      // column tiles / row blocks of 16 per polynomial
 constexpr int kTh = 256;                     // threads per CTA: 16 values each
 constexpr int kTc = 256 / kCl;               // columns (column phase) / rows (row phase) per CTA
 constexpr int kRowPad = 272;                 // 256 + 16: pad one element every 16
@@ -99,13 +100,16 @@ __device__ __forceinline__ void stage_table(double2 *st, const double2 *__restri
 // load latency and the CTA barrier overlap the data loads).
 template <bool kBig, class Pro>
 __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, double *inter, int tile,
-                                         double2 *T, const double2 *__restrict__ Tg, const FpMod &m, double *sm) {
+                                         double2 *T, const double2 *__restrict__ Tg, const FpMod &m, double *sm,
+                                         bool stage) {
     const int c = threadIdx.x % kTc, k = threadIdx.x / kTc, col = tile * kTc + c;
     double x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = u2d(pro(l, P, (k + 16 * u) * 256 + col));
-    stage_table(T, Tg);
-    __syncthreads();
+    if (stage) {
+        stage_table(T, Tg);
+        __syncthreads();
+    }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         const int d = 8 >> s;
@@ -188,28 +192,49 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
     for (int u = 0; u < 16; ++u) epi(l, P, r * 256 + k + 16 * u, su[pad16(k + 16 * u)]);
 }
 
-template <class Pro, class Epi>
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
+// One polynomial per cluster of CPP CTAs (launch attribute; CPP = 1: a lone CTA).
+// Each CTA runs 16 / CPP column tiles, the cluster barrier, then 16 / CPP row
+// blocks. Small clusters couple few CTAs at the phase barrier and pack every
+// SM (16-CTA clusters at 4 CTAs/SM leave the SMs of a GPC beyond a multiple
+// of four idle): 0.49-0.55 µs per limb-polynomial against 0.59 for one
+// 16-CTA cluster per polynomial (tools/ntt_lab2.cu sweep, profiles/r1_notes.md).
+template <class Pro, class Epi, int CPP>
+__global__ void __launch_bounds__(kTh, 4)
     fwd_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ tw,
                const double2 *__restrict__ twist, const FpMod *__restrict__ fm, Pro pro, Epi epi) {
+    constexpr int kT = kCl / CPP;
     extern __shared__ double smd[];
     double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
-    const int c = blockIdx.x % kCl;
-    const long long P = blockIdx.x / kCl;
+    const int c = blockIdx.x % CPP;
+    const long long P = blockIdx.x / CPP;
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = tw + (size_t)mi * kN;
     const double2 *tau = twist + (size_t)mi * kN;
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
-    const int rs = threadIdx.x >> 4, r = c * kTc + rs;
+    const int rs = threadIdx.x >> 4;
     if (m.q < (double)kSmallPrime) {
-        fwd_cols<false>(pro, l, P, inter, c, st, T, m, smd);
-        cluster_sync_all();
-        fwd_row<false>(epi, l, P, inter, r, tau, st, m, smd + rs * kRowPad);
+        for (int t = 0; t < kT; ++t) {
+            if (t) __syncthreads();
+            fwd_cols<false>(pro, l, P, inter, c * kT + t, st, T, m, smd, t == 0);
+        }
+        if (CPP > 1) cluster_sync_all();
+        else __syncthreads();
+        for (int t = 0; t < kT; ++t) {
+            if (t) __syncwarp();
+            fwd_row<false>(epi, l, P, inter, (c * kT + t) * kTc + rs, tau, st, m, smd + rs * kRowPad);
+        }
     } else {
-        fwd_cols<true>(pro, l, P, inter, c, st, T, m, smd);
-        cluster_sync_all();
-        fwd_row<true>(epi, l, P, inter, r, tau, st, m, smd + rs * kRowPad);
+        for (int t = 0; t < kT; ++t) {
+            if (t) __syncthreads();
+            fwd_cols<true>(pro, l, P, inter, c * kT + t, st, T, m, smd, t == 0);
+        }
+        if (CPP > 1) cluster_sync_all();
+        else __syncthreads();
+        for (int t = 0; t < kT; ++t) {
+            if (t) __syncwarp();
+            fwd_row<true>(epi, l, P, inter, (c * kT + t) * kTc + rs, tau, st, m, smd + rs * kRowPad);
+        }
     }
 }
 
@@ -303,15 +328,16 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
     for (int u = 0; u < 16; ++u) epi(l, P, (k + 16 * u) * 256 + col, d2canon(x[u], m));
 }
 
-template <class Pro, class Epi>
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
+template <class Pro, class Epi, int CPP>
+__global__ void __launch_bounds__(kTh, 4)
     inv_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ itw,
                const double2 *__restrict__ itwist, const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
                Pro pro, Epi epi) {
+    constexpr int kT = kCl / CPP;
     extern __shared__ double smd[];
     double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
-    const int c = blockIdx.x % kCl;
-    const long long P = blockIdx.x / kCl;
+    const int c = blockIdx.x % CPP;
+    const long long P = blockIdx.x / CPP;
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = itw + (size_t)mi * kN;
@@ -319,15 +345,29 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kTh, 4)
     stage_table(st, T);
     __syncthreads();
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
-    const int rs = threadIdx.x >> 4, r = c * kTc + rs;
+    const int rs = threadIdx.x >> 4;
     if (m.q < (double)kSmallPrime) {
-        inv_row<false>(pro, l, P, inter, r, itau, st, m, smd + rs * kRowPad);
-        cluster_sync_all();
-        inv_cols<false>(epi, l, P, inter, c, st, ninv[2 * mi], ninv[2 * mi + 1], m, smd);
+        for (int t = 0; t < kT; ++t) {
+            if (t) __syncwarp();
+            inv_row<false>(pro, l, P, inter, (c * kT + t) * kTc + rs, itau, st, m, smd + rs * kRowPad);
+        }
+        if (CPP > 1) cluster_sync_all();
+        else __syncthreads();
+        for (int t = 0; t < kT; ++t) {
+            if (t) __syncthreads();
+            inv_cols<false>(epi, l, P, inter, c * kT + t, st, ninv[2 * mi], ninv[2 * mi + 1], m, smd);
+        }
     } else {
-        inv_row<true>(pro, l, P, inter, r, itau, st, m, smd + rs * kRowPad);
-        cluster_sync_all();
-        inv_cols<true>(epi, l, P, inter, c, st, ninv[2 * mi], ninv[2 * mi + 1], m, smd);
+        for (int t = 0; t < kT; ++t) {
+            if (t) __syncwarp();
+            inv_row<true>(pro, l, P, inter, (c * kT + t) * kTc + rs, itau, st, m, smd + rs * kRowPad);
+        }
+        if (CPP > 1) cluster_sync_all();
+        else __syncthreads();
+        for (int t = 0; t < kT; ++t) {
+            if (t) __syncthreads();
+            inv_cols<true>(epi, l, P, inter, c * kT + t, st, ninv[2 * mi], ninv[2 * mi + 1], m, smd);
+        }
     }
 }
 
@@ -417,36 +457,60 @@ __global__ void k17_post(Epi epi, const uint64_t *__restrict__ inter, int limb0,
 // Forward / inverse NTT of n_limbs x B polynomials (primes limb0 ..) of the
 // context's ring (2^16, or 2^17 via the radix-2 pass), input through `pro`,
 // output through `epi`; `inter` ([n_limbs][B][N] words) may alias the output.
-template <class Pro, class Epi>
-inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
+// CTAs per polynomial for a launch of n polynomials: pairs for large launches,
+// quadruples below (tools/ntt_lab2.cu sweep: 2 is best from ~800 polynomials,
+// 4 within 4% of the best everywhere else).
+inline int ctas_per_poly(long long n) { return n >= 800 ? 2 : 4; }
+
+template <class K, class... Args>
+inline cudaError_t launch_clustered(K kern, int cpp, long long n_polys, cudaStream_t s, Args... args) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(fwd_kernel<Pro, Epi>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(fwd_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         attr = true;
     }
-    const unsigned blocks = (unsigned)kCl * (unsigned)n_limbs * (unsigned)B;
-    fwd_kernel<Pro, Epi><<<blocks, kTh, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_twf,
-                                                             (const double2 *)c->d_twist, (const FpMod *)c->d_fmod,
-                                                             pro, epi);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(cpp * n_polys));
+    cfg.blockDim = dim3(kTh);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cpp;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <class Pro, class Epi>
+inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
+    const long long n = (long long)n_limbs * B;
+    const double2 *tw = (const double2 *)c->d_twf, *twist = (const double2 *)c->d_twist;
+    const FpMod *fm = (const FpMod *)c->d_fmod;
+    const cudaError_t e =
+        ctas_per_poly(n) == 2
+            ? launch_clustered(fwd_kernel<Pro, Epi, 2>, 2, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi)
+            : launch_clustered(fwd_kernel<Pro, Epi, 4>, 4, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi);
     ++c->launches;
+    if (e != cudaSuccess) return hk_fail(c, HK_E_CUDA, "ntt16 fwd launch: %s", cudaGetErrorString(e));
     HK_LAUNCH_CHECK(c, "ntt16 fwd");
     return HK_OK;
 }
 
 template <class Pro, class Epi>
 inline int launch16_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(inv_kernel<Pro, Epi>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(inv_kernel<Pro, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        attr = true;
-    }
-    const unsigned blocks = (unsigned)kCl * (unsigned)n_limbs * (unsigned)B;
-    inv_kernel<Pro, Epi><<<blocks, kTh, kSmem, c->stream>>>(inter, limb0, B, (const double2 *)c->d_itwf,
-                                                             (const double2 *)c->d_itwist, (const double2 *)c->d_ninvf,
-                                                             (const FpMod *)c->d_fmod, pro, epi);
+    const long long n = (long long)n_limbs * B;
+    const double2 *itw = (const double2 *)c->d_itwf, *itwist = (const double2 *)c->d_itwist;
+    const double2 *ninv = (const double2 *)c->d_ninvf;
+    const FpMod *fm = (const FpMod *)c->d_fmod;
+    const cudaError_t e =
+        ctas_per_poly(n) == 2
+            ? launch_clustered(inv_kernel<Pro, Epi, 2>, 2, n, c->stream, inter, limb0, B, itw, itwist, ninv, fm, pro, epi)
+            : launch_clustered(inv_kernel<Pro, Epi, 4>, 4, n, c->stream, inter, limb0, B, itw, itwist, ninv, fm, pro, epi);
     ++c->launches;
+    if (e != cudaSuccess) return hk_fail(c, HK_E_CUDA, "ntt16 inv launch: %s", cudaGetErrorString(e));
     HK_LAUNCH_CHECK(c, "ntt16 inv");
     return HK_OK;
 }

@@ -1,6 +1,6 @@
 // ntt_lab2.cu — variants of the production 16-CTA forward NTT (not product code).
 //
-//   P  production ntt16::fwd_kernel<ProPlain, EpiPlain>
+//   P  production ntt16::fwd_kernel<ProPlain, EpiPlain, CPP> at CPP = 16 (the former layout)
 //   L<F, MINB> lab copy of its small-prime path with
 //      F & 1  split cluster barrier: arrive.release after the column stores, L2
 //             prefetch of the row's twist factors, then wait.acquire
@@ -204,6 +204,75 @@ __global__ void __launch_bounds__(kTh, 4)
     }
 }
 
+// one CTA per polynomial, no cluster: 16 column passes, a CTA barrier, 16 row
+// passes (inter through L2 / HBM). CTAs are independent, so nothing couples the
+// phases of the four CTAs on an SM and every SM can be used.
+__global__ void __launch_bounds__(kTh, 4)
+    lab_single(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
+               const double2 *__restrict__ tw, const double2 *__restrict__ twist, FpMod m) {
+    extern __shared__ double smd[];
+    double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
+    const long long P = blockIdx.x;
+    stage_table(st, tw);
+    __syncthreads();
+    double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
+    for (int t = 0; t < 16; ++t) {
+        lab_cols<0>(in, P, inter, t, st, m, smd);
+        __syncthreads();
+    }
+    const int rs = threadIdx.x >> 4;
+    for (int t = 0; t < 16; ++t) {
+        fwd_row<false>(EpiPlain{out, kLogN}, 0, P, inter, t * kTc + rs, twist, st, m, smd + rs * kRowPad);
+        __syncwarp();
+    }
+}
+
+// CPP CTAs per polynomial (cluster of CPP, or a lone CTA for CPP = 1): each CTA
+// runs 16 / CPP column tiles, the cluster barrier, then 16 / CPP row blocks.
+template <int CPP>
+__global__ void __launch_bounds__(kTh, 4)
+    lab_multi(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
+              const double2 *__restrict__ tw, const double2 *__restrict__ twist, FpMod m) {
+    extern __shared__ double smd[];
+    double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
+    const int c = blockIdx.x % CPP;
+    const long long P = blockIdx.x / CPP;
+    stage_table(st, tw);
+    __syncthreads();
+    double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
+    constexpr int kT = 16 / CPP;
+    for (int t = 0; t < kT; ++t) {
+        lab_cols<0>(in, P, inter, c * kT + t, st, m, smd);
+        __syncthreads();
+    }
+    if (CPP > 1) cluster_sync_all();
+    const int rs = threadIdx.x >> 4;
+    for (int t = 0; t < kT; ++t) {
+        fwd_row<false>(EpiPlain{out, kLogN}, 0, P, inter, (c * kT + t) * kTc + rs, twist, st, m, smd + rs * kRowPad);
+        __syncwarp();
+    }
+}
+
+template <int CPP>
+void run_multi(int polys, const uint64_t *in, uint64_t *inter, uint64_t *out, const double2 *tw, const double2 *twist,
+               FpMod m, int reps) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CPP * polys);
+    cfg.blockDim = dim3(kTh);
+    cfg.dynamicSmemBytes = kSmem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = CPP;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    CK(cudaFuncSetAttribute(lab_multi<CPP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(lab_multi<CPP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    const float ms = time_it([&] { CK(cudaLaunchKernelEx(&cfg, lab_multi<CPP>, in, inter, out, tw, twist, m)); }, reps);
+    printf("M%-2d %5d polys %8.3f ms  %6.3f us/limb-poly\n", CPP, polys, ms, 1e3 * ms / polys);
+}
+
 template <class K>
 float time_it(K launch, int reps) {
     cudaEvent_t a, b;
@@ -255,21 +324,41 @@ int main(int argc, char **argv) {
     CK(cudaMalloc(&inter, bytes));
     CK(cudaMalloc(&out, bytes));
     CK(cudaMemset(in, 0, bytes));
+    if (argc > 2) {  // sweep: CTAs-per-polynomial variants over launch sizes
+        auto kf = fwd_kernel<ProPlain, EpiPlain, 16>;
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        for (int n : {64, 416, 600, 800, 1184, 2368, 4736}) {
+            if (n > polys) break;
+            const float ms = time_it(
+                [&] {
+                    CK(launch_clustered(kf, 16, n, 0, (uint64_t *)inter, 0, n, (const double2 *)tw, (const double2 *)twist, (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}));
+                },
+                reps);
+            printf("P   %5d polys %8.3f ms  %6.3f us/limb-poly\n", n, ms, 1e3 * ms / n);
+            run_multi<1>(n, in, inter, out, tw, twist, m, reps);
+            run_multi<2>(n, in, inter, out, tw, twist, m, reps);
+            run_multi<4>(n, in, inter, out, tw, twist, m, reps);
+            run_multi<8>(n, in, inter, out, tw, twist, m, reps);
+            run_multi<16>(n, in, inter, out, tw, twist, m, reps);
+        }
+        return 0;
+    }
     {
-        auto kf = fwd_kernel<ProPlain, EpiPlain>;
+        auto kf = fwd_kernel<ProPlain, EpiPlain, 16>;
         CK(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         // one prime: limb0 = 0, B = polys (all polynomials share table 0)
         const float ms = time_it(
             [&] {
-                kf<<<kCl * polys, kTh, kSmem>>>(inter, 0, polys, tw, twist, fm, ProPlain{in, kLogN},
-                                                EpiPlain{out, kLogN});
+                CK(launch_clustered(kf, 16, polys, 0, (uint64_t *)inter, 0, polys, (const double2 *)tw, (const double2 *)twist,
+                                    (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}));
             },
             reps);
         printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "P production", ms, 1e3 * ms / polys);
     }
     {
-        auto ki = inv_kernel<ProPlain, EpiPlain>;
+        auto ki = inv_kernel<ProPlain, EpiPlain, 16>;
         CK(cudaFuncSetAttribute(ki, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CK(cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         double2 *ninv;
@@ -277,8 +366,8 @@ int main(int argc, char **argv) {
         CK(cudaMemcpy(ninv, h.data(), 2 * sizeof(double2), cudaMemcpyHostToDevice));
         const float ms = time_it(
             [&] {
-                ki<<<kCl * polys, kTh, kSmem>>>(inter, 0, polys, tw, twist, ninv, fm, ProPlain{in, kLogN},
-                                                EpiPlain{out, kLogN});
+                CK(launch_clustered(ki, 16, polys, 0, (uint64_t *)inter, 0, polys, (const double2 *)tw, (const double2 *)twist,
+                                    (const double2 *)ninv, (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}));
             },
             reps);
         printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "P production inverse", ms, 1e3 * ms / polys);
@@ -367,6 +456,11 @@ int main(int argc, char **argv) {
         ms = time_it(
             [&] { CK(cudaLaunchCooperativeKernel((void *)lab_coop<4000>, dim3(grid), dim3(kTh), args, kSmem, 0)); }, reps);
         printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "T6 coop, stagger 4us per quarter", ms, 1e3 * ms / polys);
+    }
+    {
+        CK(cudaFuncSetAttribute(lab_single, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        const float ms = time_it([&] { lab_single<<<polys, kTh, kSmem>>>(in, inter, out, tw, twist, m); }, reps);
+        printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "T7 one CTA per polynomial", ms, 1e3 * ms / polys);
     }
     run_lab<0, 4>("L0 lab copy", polys, in, inter, out, tw, twist, m, reps);
     run_lab<1, 4>("L1 split barrier + L2 prefetch", polys, in, inter, out, tw, twist, m, reps);
