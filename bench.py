@@ -316,11 +316,12 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
         pass
     out["ntt"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                   "frac": round(ach / hbm, 4), "traffic": traffic,
-                  "kernel": f"hk_ntt_fwd -> ntt16::fwd_kernel (one 16-CTA cluster per polynomial, FP64-pipe "
+                  "kernel": f"hk_ntt_fwd -> ntt16::fwd_kernel (one 4-CTA cluster per polynomial, FP64-pipe "
                             f"butterflies), {nl} limbs x {B} polys",
                   "algorithmic_bytes": alg, "ms": round(t * 1e3, 3),
                   "note": f"FP64-issue/latency bound: ncu fp64 pipe {tr.get('fp64_pipe_pct')}%, issue "
-                          f"{tr.get('issue_active_pct')}% (profiles/r1_ntt_traffic.json)"}
+                          f"{tr.get('issue_active_pct')}%; traffic above the algorithmic bytes is the "
+                          f"between-phase buffer partly reaching HBM (profiles/r1_ntt_traffic.json)"}
     del buf
     # key switch via one rotation at the top level (ModUp + IP + ModDown)
     x = np.zeros((B, params.slot_count))

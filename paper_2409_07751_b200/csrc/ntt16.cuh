@@ -1,6 +1,6 @@
 // ntt16.cuh — fused N = 2^16 negacyclic NTT kernels with prologue/epilogue hooks.
 //
-// One cluster of 2 or 4 CTAs (256 threads each, four CTAs per SM) per
+// One cluster of 4 CTAs (256 threads each, four CTAs per SM) per
 // polynomial; the polynomial is 16 column tiles / 16 row blocks of 16 (see
 // ntt.cu for the stage split). The first phase reads its inputs through a prologue functor and the
 // second phase hands canonical outputs to an epilogue functor, so element-wise
@@ -22,6 +22,8 @@
 // phase (8 stages from |x| < q stay below 13 q < 2^51); the phase boundary
 // recentres. Large primes (q_0 ~ 2^50) recentre after every stage.
 #pragma once
+
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -457,10 +459,12 @@ __global__ void k17_post(Epi epi, const uint64_t *__restrict__ inter, int limb0,
 // Forward / inverse NTT of n_limbs x B polynomials (primes limb0 ..) of the
 // context's ring (2^16, or 2^17 via the radix-2 pass), input through `pro`,
 // output through `epi`; `inter` ([n_limbs][B][N] words) may alias the output.
-// CTAs per polynomial for a launch of n polynomials: pairs for large launches,
-// quadruples below (tools/ntt_lab2.cu sweep: 2 is best from ~800 polynomials,
-// 4 within 4% of the best everywhere else).
-inline int ctas_per_poly(long long n) { return n >= 800 ? 2 : 4; }
+// CTAs per polynomial. The lab sweep (tools/ntt_lab2.cu) has 2 ahead by up to
+// 4% on large isolated launches, but in the pipeline 4 is as fast on the
+// device and 10% faster end to end: with 148 polynomials in flight the
+// between-phase buffer (512 KiB each) stays in L2 instead of spilling to HBM
+// (profiles/r1_notes.md).
+constexpr int kCpp = 4;
 
 template <class K, class... Args>
 inline cudaError_t launch_clustered(K kern, int cpp, long long n_polys, cudaStream_t s, Args... args) {
@@ -490,9 +494,7 @@ inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int 
     const double2 *tw = (const double2 *)c->d_twf, *twist = (const double2 *)c->d_twist;
     const FpMod *fm = (const FpMod *)c->d_fmod;
     const cudaError_t e =
-        ctas_per_poly(n) == 2
-            ? launch_clustered(fwd_kernel<Pro, Epi, 2>, 2, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi)
-            : launch_clustered(fwd_kernel<Pro, Epi, 4>, 4, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi);
+        launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi);
     ++c->launches;
     if (e != cudaSuccess) return hk_fail(c, HK_E_CUDA, "ntt16 fwd launch: %s", cudaGetErrorString(e));
     HK_LAUNCH_CHECK(c, "ntt16 fwd");
@@ -505,10 +507,8 @@ inline int launch16_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int 
     const double2 *itw = (const double2 *)c->d_itwf, *itwist = (const double2 *)c->d_itwist;
     const double2 *ninv = (const double2 *)c->d_ninvf;
     const FpMod *fm = (const FpMod *)c->d_fmod;
-    const cudaError_t e =
-        ctas_per_poly(n) == 2
-            ? launch_clustered(inv_kernel<Pro, Epi, 2>, 2, n, c->stream, inter, limb0, B, itw, itwist, ninv, fm, pro, epi)
-            : launch_clustered(inv_kernel<Pro, Epi, 4>, 4, n, c->stream, inter, limb0, B, itw, itwist, ninv, fm, pro, epi);
+    const cudaError_t e = launch_clustered(inv_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, itw, itwist,
+                                           ninv, fm, pro, epi);
     ++c->launches;
     if (e != cudaSuccess) return hk_fail(c, HK_E_CUDA, "ntt16 inv launch: %s", cudaGetErrorString(e));
     HK_LAUNCH_CHECK(c, "ntt16 inv");
