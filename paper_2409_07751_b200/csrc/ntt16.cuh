@@ -89,6 +89,23 @@ __device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMo
     if (kBig) y = f_center(y, m);
 }
 
+// The between-phase buffer is written once and read once by the cluster: its
+// stores carry an L2 evict_last policy (keep it on chip until the other phase
+// reads it) and its loads evict_first (dead after the read), so the streaming
+// inputs and outputs do not push it out to HBM.
+__device__ __forceinline__ void st_inter(double *p, double v) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_inter(const double *p) {
+    uint64_t pol;
+    double v;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -134,7 +151,7 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
 #pragma unroll
     // no recentre for small primes: |x| < 13 q < 2^51 and the row phase starts with the
     // twist multiply (f_mulmod, exact for |x| < 2^51); the large prime is centred already
-    for (int v = 0; v < 16; ++v) inter[(16 * k + v) * 256 + col] = x[v];
+    for (int v = 0; v < 16; ++v) st_inter(inter + (16 * k + v) * 256 + col, x[v]);
 }
 
 // Row phase (four-step form): Z[r][c] = X[r][c] * tau(r, c) with
@@ -152,7 +169,7 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
     const double2 *tr = tau + r * 256;
     double x[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) x[u] = __ldcg(rd + k + 16 * u);
+    for (int u = 0; u < 16; ++u) x[u] = ld_inter(rd + k + 16 * u);
     // twist fused with stage 0 (pairs c, c+128, twiddle T[1]): the table holds
     // tau(r, c) for c < 128 and tau(r, c) * T[1] for c >= 128
 #pragma unroll
@@ -287,8 +304,8 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         // stages keep |x| < 6 q); the large prime needs it for the next f_mulmod's range
         const double a = f_mulmod(__dadd_rn(U, V), ta.x, ta.y, m.q);
         const double b = f_mulmod(__dsub_rn(U, V), tb.x, tb.y, m.q);
-        rd[k + 16 * u] = kBig ? f_center(a, m) : a;
-        rd[k + 16 * (u + 8)] = kBig ? f_center(b, m) : b;
+        st_inter(rd + k + 16 * u, kBig ? f_center(a, m) : a);
+        st_inter(rd + k + 16 * (u + 8), kBig ? f_center(b, m) : b);
     }
 }
 
@@ -299,7 +316,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
     const int c = threadIdx.x % kTc, k = threadIdx.x / kTc, col = tile * kTc + c;
     double x[16];
 #pragma unroll
-    for (int v = 0; v < 16; ++v) x[v] = __ldcg(inter + (16 * k + v) * 256 + col);
+    for (int v = 0; v < 16; ++v) x[v] = ld_inter(inter + (16 * k + v) * 256 + col);
 #pragma unroll
     for (int s = 7; s >= 4; --s) {
         const int d = 128 >> s;
