@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(kTh, 4)
 
 // CPP CTAs per polynomial (cluster of CPP, or a lone CTA for CPP = 1): each CTA
 // runs 16 / CPP column tiles, the cluster barrier, then 16 / CPP row blocks.
-template <int CPP>
-__global__ void __launch_bounds__(kTh, 4)
+template <int CPP, int MINB = 4>
+__global__ void __launch_bounds__(kTh, MINB)
     lab_multi(const uint64_t *__restrict__ in, uint64_t *__restrict__ inter_base, uint64_t *__restrict__ out,
               const double2 *__restrict__ tw, const double2 *__restrict__ twist, FpMod m) {
     extern __shared__ double smd[];
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kTh, 4)
     }
 }
 
-template <int CPP>
+template <int CPP, int MINB = 4>
 void run_multi(int polys, const uint64_t *in, uint64_t *inter, uint64_t *out, const double2 *tw, const double2 *twist,
                FpMod m, int reps) {
     cudaLaunchConfig_t cfg = {};
@@ -267,10 +267,11 @@ void run_multi(int polys, const uint64_t *in, uint64_t *inter, uint64_t *out, co
     at.val.clusterDim.z = 1;
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    CK(cudaFuncSetAttribute(lab_multi<CPP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CK(cudaFuncSetAttribute(lab_multi<CPP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    const float ms = time_it([&] { CK(cudaLaunchKernelEx(&cfg, lab_multi<CPP>, in, inter, out, tw, twist, m)); }, reps);
-    printf("M%-2d %5d polys %8.3f ms  %6.3f us/limb-poly\n", CPP, polys, ms, 1e3 * ms / polys);
+    CK(cudaFuncSetAttribute(lab_multi<CPP, MINB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(lab_multi<CPP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    const float ms =
+        time_it([&] { CK(cudaLaunchKernelEx(&cfg, lab_multi<CPP, MINB>, in, inter, out, tw, twist, m)); }, reps);
+    printf("M%-2d minB %d %5d polys %8.3f ms  %6.3f us/limb-poly\n", CPP, MINB, polys, ms, 1e3 * ms / polys);
 }
 
 template <class K>
@@ -341,6 +342,8 @@ int main(int argc, char **argv) {
             run_multi<4>(n, in, inter, out, tw, twist, m, reps);
             run_multi<8>(n, in, inter, out, tw, twist, m, reps);
             run_multi<16>(n, in, inter, out, tw, twist, m, reps);
+            run_multi<4, 5>(n, in, inter, out, tw, twist, m, reps);
+            run_multi<4, 6>(n, in, inter, out, tw, twist, m, reps);
         }
         return 0;
     }
