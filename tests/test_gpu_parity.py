@@ -188,3 +188,18 @@ def test_serialised_ciphertexts_cross_engines(gpu_lib):
     np.testing.assert_allclose(o.decrypt(co), np.roll(X * X, -3, axis=1), atol=1e-6)
     back = g.deserialize_ct(o.serialize_ct(co))
     assert np.array_equal(g.export_ct(back), g.export_ct(cg))
+
+
+@pytest.mark.parametrize("B", [1, 3, 5, 6])
+def test_ragged_batches_bitexact(gpu_lib, B):
+    # batch sizes that are not multiples of the key inner product's 4-sample walk,
+    # and a single ciphertext, at the bench ring (N = 2^16)
+    g, o, p = _pair(16, 3)
+    rng = np.random.default_rng(20 + B)
+    x, y = rng.uniform(-1, 1, (B, p.slot_count)), rng.uniform(-1, 1, (B, p.slot_count))
+    ga, gb, oa, ob = g.encrypt(x), g.encrypt(y), o.encrypt(x), o.encrypt(y)
+    _same(g, o, g.mul(ga, gb), o.mul(oa, ob), f"mul B={B}")
+    _same(g, o, g.rotate(ga, -5), o.rotate(oa, -5), f"rotate B={B}")
+    _same(g, o, g.mul(ga, 0.75), o.mul(oa, 0.75), f"mul_const B={B}")
+    for cg, co in zip(g.rotate_many(ga, [1, 2, 7]), o.rotate_many(oa, [1, 2, 7])):
+        _same(g, o, cg, co, f"hoisted B={B}")
