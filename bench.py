@@ -621,9 +621,13 @@ def main():
     if args.log_n is None:
         args.log_n = 17 if args.config == "c5" else 16
     if args.chunk is None:
-        # ciphertexts per launch: c3's 55-limb chain (depth 54) holds ~1.5x the live
-        # intermediates of the 37-limb configs, so it runs 16 at a time to stay in HBM
-        args.chunk = 8 if args.log_n > 16 else (16 if args.config == "c3" else 32)
+        # ciphertexts per launch (the whole resident batch where it fits in HBM): c1 and
+        # c3 run their batch in one chunk; c4 / c5 hold 80 / 157 hoisted BSGS baby
+        # steps at once, which bounds them to 32 at N = 2^16 and 8 at N = 2^17
+        if args.log_n > 16:
+            args.chunk = 8 if args.config == "c5" else 32
+        else:
+            args.chunk = {"c4": 32, "c5": 8}.get(args.config, 128)
     if args.impl == "reference":
         run_reference(args)
     else:
