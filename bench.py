@@ -574,6 +574,24 @@ class _Recorder:
         return self.Ct(self, babies[0].level - 1)
 
 
+def reference_config(args):
+    """The product arm's workload description (same model, batch, chunking and ring),
+    so the driver compares like with like; the CPU measures a bounded sample of it."""
+    from paper_2409_07751_b200 import configs, inference as inf
+    from paper_2409_07751_b200.params import kan_params
+    cfg = configs.CONFIGS[args.config]
+    B = args.batch or (cfg.batch if cfg.batch <= 128 else 64)
+    chunk = min(args.chunk or B, B)
+    _, model, _ = configs.workload(args.config)
+    depth = inf.plan_model(model, inf.PipelineConfig()).total
+    params = kan_params(depth, log_n=args.log_n, dnum=args.dnum)
+    return {"workload": f"{args.config}: KAN {list(cfg.dims)} G={cfg.g} k={cfg.k}, "
+                        f"{B} ciphertexts/GPU in chunks of {chunk}, RNS-CKKS N=2^{args.log_n} L={depth} "
+                        f"dnum={params.dnum} alpha={params.alpha}",
+            "global_batch": B, "parallelism": "cpu (OpenMP, all host cores, one ciphertext at a time)",
+            "sample": "bounded prefix of one inference per step (cpu_baseline.sample)"}
+
+
 def run_reference(args):
     """--impl reference: the CPU path (oracle port) on host cores, rank 0 only."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -593,7 +611,7 @@ def run_reference(args):
             "ms_per_step": round(1e3 / v, 3) if v else None, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)",
             "data": "synthetic (seeded PCG64, SURVEY §8d)", "impl": "reference",
-            "config": {"workload": f"{args.config} one ciphertext per step sample, N=2^{args.log_n}"},
+            "config": reference_config(args),
             "cpu_baseline": dict(base or {}, value=v),
             "e2e": {"value": v, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
