@@ -502,9 +502,18 @@ struct ProRsBcast {
         const uint64_t x = L[(pb << log_n) + idx];
         const bool neg = x > (ql >> 1);
         const uint64_t mag = neg ? ql - x : x;
+        // KAN chains: mag <= q_l / 2 < 2^46 and every prime exceeds 2^44, so mag < 4 q
+        // and two conditional subtractions reduce it; Barrett otherwise
         const ModQ m = mq[l];
-        const uint64_t r = reduce128(0, mag, m);
-        return neg ? (r ? m.q - r : 0) : r;
+        const uint64_t q = m.q;
+        uint64_t r;
+        if (mag < 4 * q) {
+            r = mag >= 2 * q ? mag - 2 * q : mag;
+            r = r >= q ? r - q : r;
+        } else {
+            r = reduce128(0, mag, m);
+        }
+        return neg ? (r ? q - r : 0) : r;
     }
 };
 
