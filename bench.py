@@ -512,6 +512,11 @@ class BudgetBackend(HeBackend):
         self._tick(len(babies) * self.op_weight("mul_pt", babies[0].level))
         return out
 
+    def mul_lin(self, a, b, x, k):
+        out = super().mul_lin(a, b, x, k)
+        self._tick(self.op_weight("mul_ct", min(a.level, b.level)))
+        return out
+
     def prepare_keys_for(self, model, pcfg):
         """Generate every Galois key the program needs (untimed)."""
         from paper_2409_07751_b200 import inference as inf
@@ -572,6 +577,11 @@ class _Recorder:
     def mac_plain(self, babies, plains):
         self.ops.append(("mul_pt", babies[0].level, len(babies)))
         return self.Ct(self, babies[0].level - 1)
+
+    def mul_lin(self, a, b, x, k):
+        lvl = min(a.level, b.level)
+        self.ops.append(("mul_ct", lvl, 1))
+        return self.Ct(self, lvl - 1)
 
 
 def reference_config(args):

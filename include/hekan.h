@@ -140,6 +140,14 @@ int hk_mul_const(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *res
 /* ct x ct: tensor product, relinearisation (hybrid key switch), rescale */
 int hk_mul(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
            uint64_t *out, int32_t batch);
+/* a x b + k x: a relinearised product and a constant multiple of a third
+ * ciphertext x (level lx >= min(la, lb)) sharing one ModDown + rescale, the
+ * Estrin / Chebyshev combine `hi * T + c * x` of approx.py:_combine
+ * (reference approx.py:381-405: mul_ct, mul_pt by a scalar, add). res = HOST
+ * residues of k for limbs 0..min(la, lb) (hk_encode_const at the scale that
+ * puts k x / q_l on the product's scale). out is at level min(la, lb) - 1. */
+int hk_mul_lin(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
+               const uint64_t *x, int32_t lx, const uint64_t *res, uint64_t *out, int32_t batch);
 /* rescale only (drop q_la): out level la-1 */
 int hk_rescale(hk_ctx *ctx, const uint64_t *a, int32_t la, uint64_t *out, int32_t batch);
 

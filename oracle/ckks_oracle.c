@@ -1003,7 +1003,24 @@ int hk_mac_plain_blocks(hk_ctx *c, const uint64_t *const *babies, int32_t n, int
     return rc;
 }
 
+/* a x b (+ k x): with a linear term, d0 += k x0 and d1 += k x1 (limbs 0..l) before
+ * the merged ModDown + rescale, so Y = acc + P (d + k x) is divided by P q_l once. */
+static int mul_lin_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
+                        const uint64_t *x, int32_t lx, const uint64_t *res, uint64_t *out, int32_t B);
+
 int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {
+    return mul_lin_impl(c, a, la, b, lb, NULL, 0, NULL, out, B);
+}
+
+int hk_mul_lin(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, const uint64_t *x,
+               int32_t lx, const uint64_t *res, uint64_t *out, int32_t B) {
+    if (lx < 0 || lx >= c->n_q) return fail(c, HK_E_ARG, "mul_lin: level");
+    if (lx < (la < lb ? la : lb)) return fail(c, HK_E_ARG, "mul_lin: linear term below the product's level");
+    return mul_lin_impl(c, a, la, b, lb, x, lx, res, out, B);
+}
+
+static int mul_lin_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
+                        const uint64_t *x, int32_t lx, const uint64_t *res, uint64_t *out, int32_t B) {
     if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return fail(c, HK_E_ARG, "mul: level");
     const int l = la < lb ? la : lb, N = c->n;
@@ -1019,6 +1036,11 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
             d[o] = mulmod(a0, b0, q);
             d[pl + o] = addmod(mulmod(a0, b1, q), mulmod(a1, b0, q), q);
             d[2 * pl + o] = mulmod(a1, b1, q);
+            if (x) {
+                const size_t px = (size_t)(lx + 1) * B * N;
+                d[o] = addmod(d[o], mulmod(x[o], res[i], q), q);
+                d[pl + o] = addmod(d[pl + o], mulmod(x[px + o], res[i], q), q);
+            }
         }
     }
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;

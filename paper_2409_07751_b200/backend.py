@@ -368,6 +368,37 @@ class HeBackend:
             level -= 1
         return self._wrap(out, level, B, a.batched or (is_ct and b.batched))
 
+    def mul_lin(self, a: CipherText, b: CipherText, x: CipherText, k: float) -> CipherText:
+        """a * b + k * x: the Estrin / Chebyshev combine `hi * T + k * x`
+        (reference approx.py:381-405 as mul_ct, mul_pt by a scalar, add) with
+        the scalar product folded into the relinearised product's merged
+        ModDown + rescale: one rescale instead of two and no separate add.
+        Counts, levels and errors are those of the three reference ops; the
+        output is at level min(a, b) - 1. Falls back to the three ops when x
+        sits below the product's level."""
+        self._check_ours(a)
+        self._check_ours(b)
+        self._check_ours(x)
+        l = min(a.level, b.level)
+        if l < 1:
+            raise DepthExhausted(f"multiplication at level {l} (tag {a.tag})")
+        if x.level < l or k == 0.0:
+            return self.add(self.mul(a, b), self.mul(x, float(k)))
+        if not (a.batch == b.batch == x.batch):
+            raise LengthMismatch("mul_lin: batch sizes differ")
+        B = a.batch
+        # k x / q_l must land on the product's scale scales[l-1]
+        scale = self.params.scale(l - 1) * self.params.q[l] / self.params.scale(x.level)
+        res = self._const_residues(float(k), l, scale)
+        eng = self.engine
+        out = eng.alloc_u64(2 * l * B * self.n)
+        eng.call("hk_mul_lin", eng.addr(a.data), a.level, eng.addr(b.data), b.level, eng.addr(x.data), x.level,
+                 res, eng.addr(out), B)
+        self.counter.ct_mults += 1
+        self.counter.pt_mults += 1
+        self.counter.adds += 1
+        return self._wrap(out, l - 1, B, a.batched or b.batched or x.batched)
+
     def add(self, a: CipherText, b) -> CipherText:
         return self.slotwise("add", a, b)
 

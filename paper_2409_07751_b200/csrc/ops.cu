@@ -634,6 +634,21 @@ struct Tensor {
         return acc3_reduce(acc, m);
     }
 };
+// Optional linear term k * x folded into a relinearised product before its
+// merged ModDown + rescale (hk_mul_lin): d_p += k_l * x_p at limb l, so the
+// product and k x share one division by P q_l. x is a ciphertext at level
+// >= l (poly 1 at offset px); k / ksh are the constant's residues and Shoup
+// companions per limb.
+struct LinTerm {
+    const uint64_t *x;
+    long long px;
+    Residues k, ksh;
+    __device__ __forceinline__ uint64_t apply(int which, int l, long long o, uint64_t d, uint64_t q) const {
+        if (!x) return d;
+        const uint64_t xv = x[which ? px + o : o];
+        return add_mod(d, mul_shoup_fast(xv, k.v[l], ksh.v[l], q), q);
+    }
+};
 // iNTT prologue for the relinearisation ModUp: d2 = a1 b1 on the fly
 struct ProD2 {
     Tensor T;
@@ -653,11 +668,13 @@ struct EpiMdRsT {
     const ModQ *mq;
     int B, log_n;
     long long BN;
+    LinTerm lin;
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
         const uint64_t q = mq[l].q;
         const ulonglong2 Pm = pmod[l], w = mqinv[l];
-        const uint64_t y = add_mod(acc[o], mul_shoup(T.d(which, l, o), Pm.x, Pm.y, q), q);
+        const uint64_t d = lin.apply(which, l, o, T.d(which, l, o), q);
+        const uint64_t y = add_mod(acc[o], mul_shoup(d, Pm.x, Pm.y, q), q);
         out[o] = mul_shoup(sub_mod(y, v, q), w.x, w.y, q);
     }
 };
@@ -670,13 +687,23 @@ struct ProMdYT {
     const ulonglong2 *pmod;
     const ModQ *mq;
     int log_n;
+    LinTerm lin;
     __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
         const long long o = (long long)l * BN + (P << log_n) + idx;
         const uint64_t q = mq[l].q;
         const ulonglong2 Pm = pmod[l];
-        return add_mod(acc[o], mul_shoup(T.d(which, l, o), Pm.x, Pm.y, q), q);
+        const uint64_t d = lin.apply(which, l, o, T.d(which, l, o), q);
+        return add_mod(acc[o], mul_shoup(d, Pm.x, Pm.y, q), q);
     }
 };
+
+// generic-ring path of hk_mul_lin: d_p += k x_p over the materialised tensor
+__global__ void k_add_lin(uint64_t *__restrict__ d, long long pl, LinTerm lin, long long BN,
+                          const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    const long long o = (long long)l * BN + e;
+    d[p * pl + o] = lin.apply(p, l, o, d[p * pl + o], mq[l].q);
+}
 
 // iNTT prologue: y = acc_l + P d_l (prime l)
 struct ProMdY {
@@ -955,7 +982,7 @@ static int ks_moddown_rescale(hk_ctx *c, const uint64_t *a, const uint64_t *dp, 
 // ModUp iNTT prologue, d0 / d1 are recomputed inside the merged ModDown +
 // rescale (prologue of the q_l limb, epilogue of every output limb).
 static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, int lb, int l, int B,
-                     const KsBufs &kb, uint64_t *out) {
+                     const KsBufs &kb, uint64_t *out, const LinTerm &lin) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
     const long long BN = (long long)B * c->n;
     const Tensor T{a, b, (long long)(la + 1) * BN, (long long)(lb + 1) * BN, c->d_modq};
@@ -992,11 +1019,11 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
         EpiScale es{kb.sp, Tm.d_inv, Tm.d_inv_sh, c->d_modq, c->n_q, c->log_n};
         if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{acc + (size_t)(l + 1) * BN, c->log_n}, es)))
             return rc;
-        ProMdYT py{acc, T, p, l, BN, c->d_pmod, c->d_modq, c->log_n};
+        ProMdYT py{acc, T, p, l, BN, c->d_pmod, c->d_modq, c->log_n, lin};
         EpiScale es2{kb.sp + (size_t)np * BN, Tm.d_inv + np, Tm.d_inv_sh + np, c->d_modq, l, c->log_n};
         if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * BN, l, 1, B, py, es2))) return rc;
         if ((rc = conv_launch(c, Tm, kb.sp, kb.conv, 1, l, BN, l, 1))) return rc;
-        EpiMdRsT epi{acc, T, p, out + (size_t)p * l * BN, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN};
+        EpiMdRsT epi{acc, T, p, out + (size_t)p * l * BN, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN, lin};
         if ((rc = ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv, c->log_n}, epi))) return rc;
     }
     return HK_OK;
@@ -1193,26 +1220,58 @@ int hk_mac_plain_blocks(hk_ctx *c, const uint64_t *const *babies, int32_t n, int
     return HK_OK;
 }
 
-int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {
-    if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
-    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "mul: level");
+static int mul_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B,
+                    const LinTerm &lin) {
     const int l = std::min(la, lb);
-    if (l < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", l);
     const long long BN = (long long)B * c->n, pl = (long long)(l + 1) * BN;
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (3 * pl + ks_words(c, l, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
     uint64_t *d = ws;
     const KsBufs kb = ks_bufs(c, l, B, ws + 3 * pl);
-    if (ntt16::fused(c)) return mul_fused(c, a, la, b, lb, l, B, kb, out);
+    if (ntt16::fused(c)) return mul_fused(c, a, la, b, lb, l, B, kb, out, lin);
     k_tensor<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");
+    if (lin.x) {
+        k_add_lin<<<egrid(BN, l + 1, 2), 256, 0, c->stream>>>(d, pl, lin, BN, c->d_modq);
+        ++c->launches;
+        HK_LAUNCH_CHECK(c, "linear term");
+    }
     int rc = ks_modup(c, d + 2 * pl, l, B, kb);
     if (!rc) rc = ks_ip(c, d + 2 * pl, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u);
     const int ne = l + 1 + c->n_p;
     if (!rc) rc = ks_moddown_rescale(c, kb.acc, d, l, B, kb, out);
     if (!rc) rc = ks_moddown_rescale(c, kb.acc + (size_t)ne * BN, d + pl, l, B, kb, out + (size_t)l * BN);
     return rc;
+}
+
+int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {
+    if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "mul: level");
+    const int l = std::min(la, lb);
+    if (l < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", l);
+    LinTerm lin;
+    memset(&lin, 0, sizeof lin);
+    return mul_impl(c, a, la, b, lb, out, B, lin);
+}
+
+int hk_mul_lin(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, const uint64_t *x,
+               int32_t lx, const uint64_t *res, uint64_t *out, int32_t B) {
+    if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q || lx < 0 || lx >= c->n_q)
+        return hk_fail(c, HK_E_ARG, "mul_lin: level");
+    const int l = std::min(la, lb);
+    if (l < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", l);
+    if (lx < l) return hk_fail(c, HK_E_ARG, "mul_lin: linear term at level %d below the product's %d", lx, l);
+    LinTerm lin;
+    memset(&lin, 0, sizeof lin);
+    lin.x = x;
+    lin.px = (long long)(lx + 1) * B * c->n;
+    for (int i = 0; i <= l; ++i) {
+        lin.k.v[i] = res[i];
+        lin.ksh.v[i] = (uint64_t)(((u128)res[i] << 64) / c->mod_h[i]);
+    }
+    return mul_impl(c, a, la, b, lb, out, B, lin);
 }
 
 int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *gs, int32_t n,

@@ -97,6 +97,8 @@ def test_ops_bitexact(gpu_lib, log_n, depth):
         ("rot", lambda be, a, b: be.rotate(a, 1)),
         ("rot_neg", lambda be, a, b: be.rotate(a, -3)),
         ("mac", lambda be, a, b: be.mac_plain([a, b], [pv, w[1]])),
+        ("mul_lin", lambda be, a, b: be.mul_lin(be.mul(a, 0.5), be.mul(b, 2.0), a, -0.375)),
+        ("mul_lin_same_level", lambda be, a, b: be.mul_lin(a, b, be.add(a, b), 1.5)),
     ]
     for name, fn in checks:
         _same(g, o, fn(g, ga, gb), fn(o, oa, ob), name)
