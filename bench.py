@@ -517,6 +517,11 @@ class BudgetBackend(HeBackend):
         self._tick(self.op_weight("mul_ct", min(a.level, b.level)))
         return out
 
+    def mul_affine(self, a, b, mult, c):
+        out = super().mul_affine(a, b, mult, c)
+        self._tick(self.op_weight("mul_ct", min(a.level, b.level)))
+        return out
+
     def prepare_keys_for(self, model, pcfg):
         """Generate every Galois key the program needs (untimed)."""
         from paper_2409_07751_b200 import inference as inf
@@ -579,6 +584,11 @@ class _Recorder:
         return self.Ct(self, babies[0].level - 1)
 
     def mul_lin(self, a, b, x, k):
+        lvl = min(a.level, b.level)
+        self.ops.append(("mul_ct", lvl, 1))
+        return self.Ct(self, lvl - 1)
+
+    def mul_affine(self, a, b, mult, c):
         lvl = min(a.level, b.level)
         self.ops.append(("mul_ct", lvl, 1))
         return self.Ct(self, lvl - 1)

@@ -148,6 +148,14 @@ int hk_mul(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_
  * puts k x / q_l on the product's scale). out is at level min(la, lb) - 1. */
 int hk_mul_lin(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
                const uint64_t *x, int32_t lx, const uint64_t *res, uint64_t *out, int32_t batch);
+/* mult * (a x b) + c: a relinearised product with the Chebyshev power step's
+ * doubling and constant folded into its last epilogue (T_2k = 2 T_k^2 - 1,
+ * reference approx.py:381-405 as mul_ct, add, add of a scalar); bit-identical
+ * to hk_mul, hk_add(out, out), hk_add_const. mult is 1 or 2; res = HOST
+ * residues of c for limbs 0..min(la, lb) - 1 (hk_encode_const at the output
+ * level), or NULL for no constant. */
+int hk_mul_affine(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, int32_t mult,
+                  const uint64_t *res, uint64_t *out, int32_t batch);
 /* rescale only (drop q_la): out level la-1 */
 int hk_rescale(hk_ctx *ctx, const uint64_t *a, int32_t la, uint64_t *out, int32_t batch);
 

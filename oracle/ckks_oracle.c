@@ -1019,6 +1019,26 @@ int hk_mul_lin(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int3
     return mul_lin_impl(c, a, la, b, lb, x, lx, res, out, B);
 }
 
+int hk_mul_affine(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, int32_t mult,
+                  const uint64_t *res, uint64_t *out, int32_t B) {
+    if (mult != 1 && mult != 2) return fail(c, HK_E_ARG, "mul_affine: multiplier %d not 1 or 2", mult);
+    const int rc = mul_lin_impl(c, a, la, b, lb, NULL, 0, NULL, out, B);
+    if (rc) return rc;
+    const int l = la < lb ? la : lb, N = c->n;
+    for (int p = 0; p < 2; ++p)
+        for (int i = 0; i < l; ++i) {
+            const uint64_t q = c->mod[i];
+            uint64_t *o = out + ((size_t)p * l + i) * B * N;
+            for (size_t k = 0; k < (size_t)B * N; ++k) {
+                uint64_t r = o[k];
+                if (mult == 2) r = addmod(r, r, q);
+                if (res && p == 0) r = addmod(r, res[i], q);
+                o[k] = r;
+            }
+        }
+    return HK_OK;
+}
+
 static int mul_lin_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
                         const uint64_t *x, int32_t lx, const uint64_t *res, uint64_t *out, int32_t B) {
     if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");

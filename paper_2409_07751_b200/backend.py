@@ -399,6 +399,30 @@ class HeBackend:
         self.counter.adds += 1
         return self._wrap(out, l - 1, B, a.batched or b.batched or x.batched)
 
+    def mul_affine(self, a: CipherText, b: CipherText, mult: int, c: float) -> CipherText:
+        """mult * (a * b) + c, the Chebyshev power step T_2k = 2 T_k^2 - 1
+        (reference: mul_ct, add(sq, sq), add of a scalar) with the doubling and
+        the constant applied in the product's last epilogue. Bit-identical to
+        the three ops and counted as them."""
+        self._check_ours(a)
+        self._check_ours(b)
+        if mult not in (1, 2):
+            raise ValueError(f"mul_affine: multiplier {mult} not 1 or 2")
+        l = min(a.level, b.level)
+        if l < 1:
+            raise DepthExhausted(f"multiplication at level {l} (tag {a.tag})")
+        if a.batch != b.batch:
+            raise LengthMismatch("mul_affine: batch sizes differ")
+        B = a.batch
+        res = self._const_residues(float(c), l - 1, self.params.scale(l - 1)) if c != 0.0 else None
+        eng = self.engine
+        out = eng.alloc_u64(2 * l * B * self.n)
+        eng.call("hk_mul_affine", eng.addr(a.data), a.level, eng.addr(b.data), b.level, int(mult), res,
+                 eng.addr(out), B)
+        self.counter.ct_mults += 1
+        self.counter.adds += (1 if mult == 2 else 0) + (1 if c != 0.0 else 0)
+        return self._wrap(out, l - 1, B, a.batched or b.batched)
+
     def add(self, a: CipherText, b) -> CipherText:
         return self.slotwise("add", a, b)
 

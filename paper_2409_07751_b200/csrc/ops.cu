@@ -649,6 +649,18 @@ struct LinTerm {
         return add_mod(d, mul_shoup_fast(xv, k.v[l], ksh.v[l], q), q);
     }
 };
+// Optional affine finish of a relinearised product (hk_mul_affine):
+// out = mult * out (+ c on poly 0), bit-identical to hk_add(out, out) and
+// hk_add_const on the result (the Chebyshev power step T_2k = 2 T_k^2 - 1).
+struct Affine {
+    int dbl, has_c;
+    Residues c;
+    __device__ __forceinline__ uint64_t apply(int which, int l, uint64_t r, uint64_t q) const {
+        if (dbl) r = add_mod(r, r, q);
+        if (has_c && which == 0) r = add_mod(r, c.v[l], q);
+        return r;
+    }
+};
 // iNTT prologue for the relinearisation ModUp: d2 = a1 b1 on the fly
 struct ProD2 {
     Tensor T;
@@ -669,13 +681,14 @@ struct EpiMdRsT {
     int B, log_n;
     long long BN;
     LinTerm lin;
+    Affine aff;
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
         const uint64_t q = mq[l].q;
         const ulonglong2 Pm = pmod[l], w = mqinv[l];
         const uint64_t d = lin.apply(which, l, o, T.d(which, l, o), q);
         const uint64_t y = add_mod(acc[o], mul_shoup(d, Pm.x, Pm.y, q), q);
-        out[o] = mul_shoup(sub_mod(y, v, q), w.x, w.y, q);
+        out[o] = aff.apply(which, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
     }
 };
 // iNTT prologue: y = acc_l + P d_l with d_l from (a, b)
@@ -697,6 +710,13 @@ struct ProMdYT {
     }
 };
 
+// generic-ring path of hk_mul_affine: out_p = mult out_p (+ c on poly 0), l limbs
+__global__ void k_affine(uint64_t *__restrict__ out, long long pl, Affine aff, long long BN,
+                         const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    const long long o = p * pl + (long long)l * BN + e;
+    out[o] = aff.apply(p, l, out[o], mq[l].q);
+}
 // generic-ring path of hk_mul_lin: d_p += k x_p over the materialised tensor
 __global__ void k_add_lin(uint64_t *__restrict__ d, long long pl, LinTerm lin, long long BN,
                           const ModQ *__restrict__ mq) {
@@ -982,7 +1002,7 @@ static int ks_moddown_rescale(hk_ctx *c, const uint64_t *a, const uint64_t *dp, 
 // ModUp iNTT prologue, d0 / d1 are recomputed inside the merged ModDown +
 // rescale (prologue of the q_l limb, epilogue of every output limb).
 static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, int lb, int l, int B,
-                     const KsBufs &kb, uint64_t *out, const LinTerm &lin) {
+                     const KsBufs &kb, uint64_t *out, const LinTerm &lin, const Affine &aff) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
     const long long BN = (long long)B * c->n;
     const Tensor T{a, b, (long long)(la + 1) * BN, (long long)(lb + 1) * BN, c->d_modq};
@@ -1023,7 +1043,7 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
         EpiScale es2{kb.sp + (size_t)np * BN, Tm.d_inv + np, Tm.d_inv_sh + np, c->d_modq, l, c->log_n};
         if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * BN, l, 1, B, py, es2))) return rc;
         if ((rc = conv_launch(c, Tm, kb.sp, kb.conv, 1, l, BN, l, 1))) return rc;
-        EpiMdRsT epi{acc, T, p, out + (size_t)p * l * BN, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN, lin};
+        EpiMdRsT epi{acc, T, p, out + (size_t)p * l * BN, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN, lin, aff};
         if ((rc = ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv, c->log_n}, epi))) return rc;
     }
     return HK_OK;
@@ -1221,14 +1241,14 @@ int hk_mac_plain_blocks(hk_ctx *c, const uint64_t *const *babies, int32_t n, int
 }
 
 static int mul_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B,
-                    const LinTerm &lin) {
+                    const LinTerm &lin, const Affine &aff) {
     const int l = std::min(la, lb);
     const long long BN = (long long)B * c->n, pl = (long long)(l + 1) * BN;
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (3 * pl + ks_words(c, l, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
     uint64_t *d = ws;
     const KsBufs kb = ks_bufs(c, l, B, ws + 3 * pl);
-    if (ntt16::fused(c)) return mul_fused(c, a, la, b, lb, l, B, kb, out, lin);
+    if (ntt16::fused(c)) return mul_fused(c, a, la, b, lb, l, B, kb, out, lin, aff);
     k_tensor<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");
@@ -1242,6 +1262,11 @@ static int mul_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b,
     const int ne = l + 1 + c->n_p;
     if (!rc) rc = ks_moddown_rescale(c, kb.acc, d, l, B, kb, out);
     if (!rc) rc = ks_moddown_rescale(c, kb.acc + (size_t)ne * BN, d + pl, l, B, kb, out + (size_t)l * BN);
+    if (!rc && (aff.dbl || aff.has_c)) {
+        k_affine<<<egrid(BN, l, 2), 256, 0, c->stream>>>(out, (long long)l * BN, aff, BN, c->d_modq);
+        ++c->launches;
+        HK_LAUNCH_CHECK(c, "affine finish");
+    }
     return rc;
 }
 
@@ -1252,7 +1277,27 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     if (l < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", l);
     LinTerm lin;
     memset(&lin, 0, sizeof lin);
-    return mul_impl(c, a, la, b, lb, out, B, lin);
+    Affine aff;
+    memset(&aff, 0, sizeof aff);
+    return mul_impl(c, a, la, b, lb, out, B, lin, aff);
+}
+
+int hk_mul_affine(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, int32_t mult,
+                  const uint64_t *res, uint64_t *out, int32_t B) {
+    if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "mul_affine: level");
+    if (mult != 1 && mult != 2) return hk_fail(c, HK_E_ARG, "mul_affine: multiplier %d not 1 or 2", mult);
+    const int l = std::min(la, lb);
+    if (l < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", l);
+    LinTerm lin;
+    memset(&lin, 0, sizeof lin);
+    Affine aff;
+    memset(&aff, 0, sizeof aff);
+    aff.dbl = mult == 2;
+    aff.has_c = res != nullptr;
+    if (res)
+        for (int i = 0; i < l; ++i) aff.c.v[i] = res[i];
+    return mul_impl(c, a, la, b, lb, out, B, lin, aff);
 }
 
 int hk_mul_lin(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, const uint64_t *x,
@@ -1271,7 +1316,9 @@ int hk_mul_lin(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int3
         lin.k.v[i] = res[i];
         lin.ksh.v[i] = (uint64_t)(((u128)res[i] << 64) / c->mod_h[i]);
     }
-    return mul_impl(c, a, la, b, lb, out, B, lin);
+    Affine aff;
+    memset(&aff, 0, sizeof aff);
+    return mul_impl(c, a, la, b, lb, out, B, lin, aff);
 }
 
 int hk_rotate_hoisted(hk_ctx *c, const uint64_t *a, int32_t la, const uint32_t *gs, int32_t n,
