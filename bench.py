@@ -522,6 +522,11 @@ class BudgetBackend(HeBackend):
         self._tick(self.op_weight("mul_ct", min(a.level, b.level)))
         return out
 
+    def mul2(self, a, b, a2, b2):
+        out = super().mul2(a, b, a2, b2)
+        self._tick(self.op_weight("mul_ct", min(a.level, b.level, a2.level, b2.level)))
+        return out
+
     def prepare_keys_for(self, model, pcfg):
         """Generate every Galois key the program needs (untimed)."""
         from paper_2409_07751_b200 import inference as inf
@@ -590,6 +595,11 @@ class _Recorder:
 
     def mul_affine(self, a, b, mult, c):
         lvl = min(a.level, b.level)
+        self.ops.append(("mul_ct", lvl, 1))
+        return self.Ct(self, lvl - 1)
+
+    def mul2(self, a, b, a2, b2):
+        lvl = min(a.level, b.level, a2.level, b2.level)
         self.ops.append(("mul_ct", lvl, 1))
         return self.Ct(self, lvl - 1)
 

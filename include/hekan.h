@@ -148,6 +148,12 @@ int hk_mul(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_
  * puts k x / q_l on the product's scale). out is at level min(la, lb) - 1. */
 int hk_mul_lin(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
                const uint64_t *x, int32_t lx, const uint64_t *res, uint64_t *out, int32_t batch);
+/* a x b + a2 x b2: two products summed before one relinearisation and one
+ * rescale (the Cox-de Boor step b = w1 b + w2 rot(b), reference
+ * bspline.py:308-317 as two mul_ct and an add). out is at level
+ * min(la, lb, la2, lb2) - 1. */
+int hk_mul2(hk_ctx *ctx, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, const uint64_t *a2,
+            int32_t la2, const uint64_t *b2, int32_t lb2, uint64_t *out, int32_t batch);
 /* mult * (a x b) + c: a relinearised product with the Chebyshev power step's
  * doubling and constant folded into its last epilogue (T_2k = 2 T_k^2 - 1,
  * reference approx.py:381-405 as mul_ct, add, add of a scalar); bit-identical

@@ -1007,6 +1007,15 @@ int hk_mac_plain_blocks(hk_ctx *c, const uint64_t *const *babies, int32_t n, int
  * the merged ModDown + rescale, so Y = acc + P (d + k x) is divided by P q_l once. */
 static int mul_lin_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
                         const uint64_t *x, int32_t lx, const uint64_t *res, uint64_t *out, int32_t B);
+static int mul_pair_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
+                         const uint64_t *a2, int32_t la2, const uint64_t *b2, int32_t lb2, const uint64_t *x,
+                         int32_t lx, const uint64_t *res, uint64_t *out, int32_t B);
+
+int hk_mul2(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, const uint64_t *a2, int32_t la2,
+            const uint64_t *b2, int32_t lb2, uint64_t *out, int32_t B) {
+    if (la2 < 0 || lb2 < 0 || la2 >= c->n_q || lb2 >= c->n_q) return fail(c, HK_E_ARG, "mul2: level");
+    return mul_pair_impl(c, a, la, b, lb, a2, la2, b2, lb2, NULL, 0, NULL, out, B);
+}
 
 int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B) {
     return mul_lin_impl(c, a, la, b, lb, NULL, 0, NULL, out, B);
@@ -1041,9 +1050,21 @@ int hk_mul_affine(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, i
 
 static int mul_lin_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
                         const uint64_t *x, int32_t lx, const uint64_t *res, uint64_t *out, int32_t B) {
+    return mul_pair_impl(c, a, la, b, lb, NULL, 0, NULL, 0, x, lx, res, out, B);
+}
+
+/* a x b (+ a2 x b2) (+ k x), one relinearisation and one merged ModDown + rescale */
+static int mul_pair_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb,
+                         const uint64_t *a2, int32_t la2, const uint64_t *b2, int32_t lb2, const uint64_t *x,
+                         int32_t lx, const uint64_t *res, uint64_t *out, int32_t B) {
     if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return fail(c, HK_E_ARG, "mul: level");
-    const int l = la < lb ? la : lb, N = c->n;
+    int l = la < lb ? la : lb;
+    if (a2) {
+        if (la2 < l) l = la2;
+        if (lb2 < l) l = lb2;
+    }
+    const int N = c->n;
     if (l < 1) return fail(c, HK_E_DEPTH, "multiplication at level %d", l);
     const size_t pl = (size_t)(l + 1) * B * N;
     const size_t pa = (size_t)(la + 1) * B * N, pb = (size_t)(lb + 1) * B * N;
@@ -1056,6 +1077,13 @@ static int mul_lin_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t
             d[o] = mulmod(a0, b0, q);
             d[pl + o] = addmod(mulmod(a0, b1, q), mulmod(a1, b0, q), q);
             d[2 * pl + o] = mulmod(a1, b1, q);
+            if (a2) {
+                const size_t pa2 = (size_t)(la2 + 1) * B * N, pb2 = (size_t)(lb2 + 1) * B * N;
+                const uint64_t c0 = a2[o], c1 = a2[pa2 + o], e0 = b2[o], e1 = b2[pb2 + o];
+                d[o] = addmod(d[o], mulmod(c0, e0, q), q);
+                d[pl + o] = addmod(d[pl + o], addmod(mulmod(c0, e1, q), mulmod(c1, e0, q), q), q);
+                d[2 * pl + o] = addmod(d[2 * pl + o], mulmod(c1, e1, q), q);
+            }
             if (x) {
                 const size_t px = (size_t)(lx + 1) * B * N;
                 d[o] = addmod(d[o], mulmod(x[o], res[i], q), q);

@@ -52,6 +52,7 @@ SIGNATURES = {
     "hk_mul": (C.c_int, [vp, vp, i32, vp, i32, vp, i32]),
     "hk_mul_lin": (C.c_int, [vp, vp, i32, vp, i32, vp, i32, vp, vp, i32]),
     "hk_mul_affine": (C.c_int, [vp, vp, i32, vp, i32, i32, vp, vp, i32]),
+    "hk_mul2": (C.c_int, [vp, vp, i32, vp, i32, vp, i32, vp, i32, vp, i32]),
     "hk_rescale": (C.c_int, [vp, vp, i32, vp, i32]),
     "hk_rotate": (C.c_int, [vp, vp, i32, u32, vp, i32]),
     "hk_rotate_hoisted": (C.c_int, [vp, vp, i32, vp, i32, vp, i32]),

@@ -399,6 +399,26 @@ class HeBackend:
         self.counter.adds += 1
         return self._wrap(out, l - 1, B, a.batched or b.batched or x.batched)
 
+    def mul2(self, a: CipherText, b: CipherText, a2: CipherText, b2: CipherText) -> CipherText:
+        """a * b + a2 * b2 with one relinearisation and one rescale (the
+        Cox-de Boor step, reference bspline.py:308-317: two mul_ct and an add).
+        Counted as those three ops; output at level min(levels) - 1."""
+        for t in (a, b, a2, b2):
+            self._check_ours(t)
+        l = min(a.level, b.level, a2.level, b2.level)
+        if l < 1:
+            raise DepthExhausted(f"multiplication at level {l} (tag {a.tag})")
+        if not (a.batch == b.batch == a2.batch == b2.batch):
+            raise LengthMismatch("mul2: batch sizes differ")
+        B = a.batch
+        eng = self.engine
+        out = eng.alloc_u64(2 * l * B * self.n)
+        eng.call("hk_mul2", eng.addr(a.data), a.level, eng.addr(b.data), b.level, eng.addr(a2.data), a2.level,
+                 eng.addr(b2.data), b2.level, eng.addr(out), B)
+        self.counter.ct_mults += 2
+        self.counter.adds += 1
+        return self._wrap(out, l - 1, B, a.batched or b.batched or a2.batched or b2.batched)
+
     def mul_affine(self, a: CipherText, b: CipherText, mult: int, c: float) -> CipherText:
         """mult * (a * b) + c, the Chebyshev power step T_2k = 2 T_k^2 - 1
         (reference: mul_ct, add(sq, sq), add of a scalar) with the doubling and

@@ -229,6 +229,24 @@ __global__ void k_tensor(const uint64_t *__restrict__ a, int la, const uint64_t 
     d[2 * pl + o] = mul_mod(a1, b1, m);
 }
 
+// d += tensor(a, b) (generic-ring path of hk_mul2)
+__global__ void k_tensor_add(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb, int lt,
+                             uint64_t *__restrict__ d, long long BN, const ModQ *__restrict__ mq) {
+    ELEM_INDEX
+    (void)p;
+    const ModQ m = mq[l];
+    const long long o = (long long)l * BN + e;
+    const uint64_t a0 = a[o], a1 = a[(long long)(la + 1) * BN + o];
+    const uint64_t b0 = b[o], b1 = b[(long long)(lb + 1) * BN + o];
+    const long long pl = (long long)(lt + 1) * BN;
+    d[o] = add_mod(d[o], mul_mod(a0, b0, m), m.q);
+    uint64_t hi = 0, lo = 0;
+    mac128(hi, lo, a0, b1);
+    mac128(hi, lo, a1, b0);
+    d[pl + o] = add_mod(d[pl + o], reduce128(hi, lo, m), m.q);
+    d[2 * pl + o] = add_mod(d[2 * pl + o], mul_mod(a1, b1, m), m.q);
+}
+
 __global__ void k_tensor2(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb,
                           uint64_t *__restrict__ d2, long long BN, const ModQ *__restrict__ mq) {
     ELEM_INDEX
@@ -619,18 +637,36 @@ __global__ void k_mdrs_finish(const uint64_t *__restrict__ acc, const uint64_t *
 }
 // tensor-product terms of (a, b) at limb l, element o (NTT domain):
 // d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1
+// With a second pair (a2, b2: hk_mul2) the terms are those of a (x) b + a2 (x) b2,
+// relinearised and rescaled once.
 struct Tensor {
     const uint64_t *a, *b;
     long long pa, pb;  // offset of poly 1 in a / b
     const ModQ *mq;
+    const uint64_t *a2 = nullptr, *b2 = nullptr;
+    long long pa2 = 0, pb2 = 0;
     __device__ __forceinline__ uint64_t d(int which, int l, long long o) const {
         const ModQ m = mq[l];
-        if (which == 0) return mul_mod(a[o], b[o], m);
-        if (which == 2) return mul_mod(a[pa + o], b[pb + o], m);
+        if (!a2) {
+            if (which == 0) return mul_mod(a[o], b[o], m);
+            if (which == 2) return mul_mod(a[pa + o], b[pb + o], m);
+        }
         Acc3 acc;
         acc3_zero(acc);
-        acc3_mac(acc, a[o], b[pb + o]);
-        acc3_mac(acc, a[pa + o], b[o]);
+        if (which == 0) {
+            acc3_mac(acc, a[o], b[o]);
+            acc3_mac(acc, a2[o], b2[o]);
+        } else if (which == 2) {
+            acc3_mac(acc, a[pa + o], b[pb + o]);
+            acc3_mac(acc, a2[pa2 + o], b2[pb2 + o]);
+        } else {
+            acc3_mac(acc, a[o], b[pb + o]);
+            acc3_mac(acc, a[pa + o], b[o]);
+            if (a2) {
+                acc3_mac(acc, a2[o], b2[pb2 + o]);
+                acc3_mac(acc, a2[pa2 + o], b2[o]);
+            }
+        }
         return acc3_reduce(acc, m);
     }
 };
@@ -661,6 +697,13 @@ struct Affine {
         return r;
     }
 };
+__global__ void k_d2_sum(Tensor T, uint64_t *__restrict__ d2, long long BN) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= BN) return;
+    const int l = blockIdx.y;
+    const long long o = (long long)l * BN + e;
+    d2[o] = T.d(2, l, o);
+}
 // iNTT prologue for the relinearisation ModUp: d2 = a1 b1 on the fly
 struct ProD2 {
     Tensor T;
@@ -1001,11 +1044,23 @@ static int ks_moddown_rescale(hk_ctx *c, const uint64_t *a, const uint64_t *dp, 
 // ct x ct at N = 2^16: the tensor product is never materialised — d2 feeds the
 // ModUp iNTT prologue, d0 / d1 are recomputed inside the merged ModDown +
 // rescale (prologue of the q_l limb, epilogue of every output limb).
+struct Pair2 {
+    const uint64_t *a, *b;
+    int la, lb;
+};
+
 static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, int lb, int l, int B,
-                     const KsBufs &kb, uint64_t *out, const LinTerm &lin, const Affine &aff) {
+                     const KsBufs &kb, uint64_t *out, const LinTerm &lin, const Affine &aff,
+                     const Pair2 *pair2 = nullptr, uint64_t *d2buf = nullptr) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1, np = c->n_p;
     const long long BN = (long long)B * c->n;
-    const Tensor T{a, b, (long long)(la + 1) * BN, (long long)(lb + 1) * BN, c->d_modq};
+    Tensor T{a, b, (long long)(la + 1) * BN, (long long)(lb + 1) * BN, c->d_modq};
+    if (pair2) {
+        T.a2 = pair2->a;
+        T.b2 = pair2->b;
+        T.pa2 = (long long)(pair2->la + 1) * BN;
+        T.pb2 = (long long)(pair2->lb + 1) * BN;
+    }
     EpiScaleDigits esd;
     memset(&esd, 0, sizeof esd);
     esd.out = kb.dc;
@@ -1028,10 +1083,18 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
         if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
         if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
     }
-    // own-digit limbs of d2 are formed inside the key IP from a1 (.) b1
-    if ((rc = ks_ip(c, a + (size_t)(la + 1) * BN, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u,
-                    b + (size_t)(lb + 1) * BN)))
+    if (pair2) {
+        // two products: the key IP reads the own-digit limbs of d2 = a1 b1 + a2_1 b2_1
+        // from a materialised copy (limbs 0..l, NTT form)
+        k_d2_sum<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(T, d2buf, BN);
+        ++c->launches;
+        HK_LAUNCH_CHECK(c, "d2 of two products");
+        if ((rc = ks_ip(c, d2buf, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u))) return rc;
+    } else if ((rc = ks_ip(c, a + (size_t)(la + 1) * BN, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u,
+                           b + (size_t)(lb + 1) * BN))) {
+        // own-digit limbs of d2 are formed inside the key IP from a1 (.) b1
         return rc;
+    }
     const ConvTable &Tm = c->mdrs[l];
     const ulonglong2 *mqinv = c->d_mqinv + (size_t)l * c->n_q;
     for (int p = 0; p < 2; ++p) {
@@ -1241,17 +1304,23 @@ int hk_mac_plain_blocks(hk_ctx *c, const uint64_t *const *babies, int32_t n, int
 }
 
 static int mul_impl(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, uint64_t *out, int32_t B,
-                    const LinTerm &lin, const Affine &aff) {
-    const int l = std::min(la, lb);
+                    const LinTerm &lin, const Affine &aff, const Pair2 *pair2 = nullptr) {
+    const int l = pair2 ? std::min(std::min(la, lb), std::min(pair2->la, pair2->lb)) : std::min(la, lb);
     const long long BN = (long long)B * c->n, pl = (long long)(l + 1) * BN;
     uint64_t *ws = (uint64_t *)hk_workspace(c, sizeof(uint64_t) * (3 * pl + ks_words(c, l, B)));
     if (!ws) return hk_fail(c, HK_E_NOMEM, "mul workspace");
     uint64_t *d = ws;
     const KsBufs kb = ks_bufs(c, l, B, ws + 3 * pl);
-    if (ntt16::fused(c)) return mul_fused(c, a, la, b, lb, l, B, kb, out, lin, aff);
+    if (ntt16::fused(c)) return mul_fused(c, a, la, b, lb, l, B, kb, out, lin, aff, pair2, d);
     k_tensor<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(a, la, b, lb, l, d, BN, c->d_modq);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "tensor");
+    if (pair2) {
+        k_tensor_add<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(pair2->a, pair2->la, pair2->b, pair2->lb, l, d, BN,
+                                                                 c->d_modq);
+        ++c->launches;
+        HK_LAUNCH_CHECK(c, "tensor pair 2");
+    }
     if (lin.x) {
         k_add_lin<<<egrid(BN, l + 1, 2), 256, 0, c->stream>>>(d, pl, lin, BN, c->d_modq);
         ++c->launches;
@@ -1280,6 +1349,22 @@ int hk_mul(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     Affine aff;
     memset(&aff, 0, sizeof aff);
     return mul_impl(c, a, la, b, lb, out, B, lin, aff);
+}
+
+int hk_mul2(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, const uint64_t *a2, int32_t la2,
+            const uint64_t *b2, int32_t lb2, uint64_t *out, int32_t B) {
+    if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    const int lv[4] = {la, lb, la2, lb2};
+    for (int i = 0; i < 4; ++i)
+        if (lv[i] < 0 || lv[i] >= c->n_q) return hk_fail(c, HK_E_ARG, "mul2: level");
+    const int l = std::min(std::min(la, lb), std::min(la2, lb2));
+    if (l < 1) return hk_fail(c, HK_E_DEPTH, "multiplication at level %d", l);
+    LinTerm lin;
+    memset(&lin, 0, sizeof lin);
+    Affine aff;
+    memset(&aff, 0, sizeof aff);
+    const Pair2 p2{a2, b2, la2, lb2};
+    return mul_impl(c, a, la, b, lb, out, B, lin, aff, &p2);
 }
 
 int hk_mul_affine(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t lb, int32_t mult,

@@ -100,6 +100,7 @@ def test_ops_bitexact(gpu_lib, log_n, depth):
         ("mul_lin", lambda be, a, b: be.mul_lin(be.mul(a, 0.5), be.mul(b, 2.0), a, -0.375)),
         ("mul_lin_same_level", lambda be, a, b: be.mul_lin(a, b, be.add(a, b), 1.5)),
         ("mul_affine", lambda be, a, b: be.mul_affine(a, b, 2, -1.0)),
+        ("mul2", lambda be, a, b: be.mul2(a, b, be.rotate(a, 1), be.mul(b, 0.5))),
         ("mul_affine_levels", lambda be, a, b: be.mul_affine(be.mul(a, 0.5), b, 1, 0.25)),
     ]
     for name, fn in checks:
