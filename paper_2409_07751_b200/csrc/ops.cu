@@ -247,14 +247,6 @@ __global__ void k_tensor_add(const uint64_t *__restrict__ a, int la, const uint6
     d[2 * pl + o] = add_mod(d[2 * pl + o], mul_mod(a1, b1, m), m.q);
 }
 
-__global__ void k_tensor2(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ b, int lb,
-                          uint64_t *__restrict__ d2, long long BN, const ModQ *__restrict__ mq) {
-    ELEM_INDEX
-    (void)p;
-    const long long o = (long long)l * BN + e;
-    d2[o] = mul_mod(a[(long long)(la + 1) * BN + o], b[(long long)(lb + 1) * BN + o], mq[l]);
-}
-
 // ------------------------------------------------------------ key switching
 // Fast basis conversion: dst[t] = sum_i [src_i * inv_i]_{q_i} * hat[t][i] mod q_t.
 // The source residues of one coefficient stay in registers (NS >= n_src), the
@@ -571,24 +563,6 @@ struct EpiScaleDigits {
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         const int j = l / alpha, i = l - j * alpha;
         out[(P << log_n) + idx] = mul_shoup(v, inv[j][i], inv_sh[j][i], mq[l].q);
-    }
-};
-
-// NTT prologue: fast basis conversion from pre-scaled sources (launch limb l
-// is target row `row0 + l` of the conversion table)
-struct ProConv {
-    const uint64_t *src;  // [n_src][B][N], already multiplied by inv_i
-    const uint64_t *hat;  // [n_dst][n_src]
-    int n_src, row0, B, mi0, log_n;
-    long long BN;
-    const ModQ *mq;
-    __device__ __forceinline__ uint64_t operator()(int l, long long P, int idx) const {
-        const long long e = ((P - (long long)l * B) << log_n) + idx;
-        const uint64_t *h = hat + (long long)(row0 + l) * n_src;
-        Acc3 acc;
-        acc3_zero(acc);
-        for (int i = 0; i < n_src; ++i) acc3_mac(acc, src[i * BN + e], h[i]);
-        return acc3_reduce(acc, mq[mi0 + l]);
     }
 };
 
