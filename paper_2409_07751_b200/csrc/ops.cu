@@ -708,6 +708,59 @@ struct EpiMdRsT {
         out[o] = aff.apply(which, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
     }
 };
+// Merged ModDown + rescale of both halves of a relinearised product: launches
+// run over 2B "samples" pb = 2 b + p, so the two halves of one sample sit in
+// adjacent clusters and the tensor operands a0 / b0 both read are shared in L2.
+// iNTT prologue of the special limbs: acc_p limb (l + 1 + j), sample b
+struct ProAccSp2 {
+    const uint64_t *acc;
+    long long BN, pne;  // pne: offset of half 1 in acc
+    int l, B, log_n;
+    __device__ __forceinline__ uint64_t operator()(int j, long long P, int idx) const {
+        const long long pb = P - (long long)j * 2 * B;
+        return acc[(pb & 1) * pne + (long long)(l + 1 + j) * BN + ((pb >> 1) << log_n) + idx];
+    }
+};
+// iNTT prologue of limb l: y = acc_p,l + P d_p,l
+struct ProMdYT2 {
+    const uint64_t *acc;
+    Tensor T;
+    long long BN, pne;
+    int l, log_n;
+    const ulonglong2 *pmod;
+    const ModQ *mq;
+    LinTerm lin;
+    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
+        const int p = (int)(P & 1);
+        const long long o = (long long)l * BN + ((P >> 1) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 Pm = pmod[l];
+        const uint64_t d = lin.apply(p, l, o, T.d(p, l, o), q);
+        return add_mod(acc[p * pne + o], mul_shoup(d, Pm.x, Pm.y, q), q);
+    }
+};
+// forward NTT epilogue: out_p = (acc_p + P d_p - v) (P q_l)^-1 (+ affine)
+struct EpiMdRsT2 {
+    const uint64_t *acc;
+    Tensor T;
+    uint64_t *out;
+    const ulonglong2 *pmod, *mqinv;
+    const ModQ *mq;
+    int B, log_n;
+    long long BN, pne, pout;  // offsets of half 1 in acc / out
+    LinTerm lin;
+    Affine aff;
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        const long long pb = P - (long long)l * 2 * B;
+        const int p = (int)(pb & 1);
+        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 Pm = pmod[l], w = mqinv[l];
+        const uint64_t d = lin.apply(p, l, o, T.d(p, l, o), q);
+        const uint64_t y = add_mod(acc[p * pne + o], mul_shoup(d, Pm.x, Pm.y, q), q);
+        out[p * pout + o] = aff.apply(p, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
+    }
+};
 // iNTT prologue: y = acc_l + P d_l with d_l from (a, b)
 struct ProMdYT {
     const uint64_t *acc;
@@ -869,7 +922,7 @@ struct KsBufs {
 
 static size_t ks_words(const hk_ctx *c, int l, int B) {
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
-    return (size_t)B * c->n * ((size_t)(l + 1) + (size_t)nd * ne + 2 * (size_t)ne + (c->n_p + 1) + (l + 1));
+    return (size_t)B * c->n * ((size_t)(l + 1) + (size_t)nd * ne + 2 * (size_t)ne + 2 * (c->n_p + 1) + 2 * (l + 1));
 }
 
 static KsBufs ks_bufs(const hk_ctx *c, int l, int B, uint64_t *scratch) {
@@ -880,7 +933,7 @@ static KsBufs ks_bufs(const hk_ctx *c, int l, int B, uint64_t *scratch) {
     k.ext = k.dc + (size_t)(l + 1) * BN;
     k.acc = k.ext + (size_t)nd * ne * BN;
     k.sp = k.acc + 2 * (size_t)ne * BN;
-    k.conv = k.sp + (size_t)(c->n_p + 1) * BN;
+    k.conv = k.sp + 2 * (size_t)(c->n_p + 1) * BN;  // sp / conv hold both halves in the merged ModDown
     return k;
 }
 
@@ -1071,18 +1124,17 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
     }
     const ConvTable &Tm = c->mdrs[l];
     const ulonglong2 *mqinv = c->d_mqinv + (size_t)l * c->n_q;
-    for (int p = 0; p < 2; ++p) {
-        const uint64_t *acc = kb.acc + (size_t)p * ne * BN;
-        EpiScale es{kb.sp, Tm.d_inv, Tm.d_inv_sh, c->d_modq, c->n_q, c->log_n};
-        if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, B, ntt16::ProPlain{acc + (size_t)(l + 1) * BN, c->log_n}, es)))
-            return rc;
-        ProMdYT py{acc, T, p, l, BN, c->d_pmod, c->d_modq, c->log_n, lin};
-        EpiScale es2{kb.sp + (size_t)np * BN, Tm.d_inv + np, Tm.d_inv_sh + np, c->d_modq, l, c->log_n};
-        if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * BN, l, 1, B, py, es2))) return rc;
-        if ((rc = conv_launch(c, Tm, kb.sp, kb.conv, 1, l, BN, l, 1))) return rc;
-        EpiMdRsT epi{acc, T, p, out + (size_t)p * l * BN, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN, lin, aff};
-        if ((rc = ntt16::launch_fwd(c, kb.conv, 0, l, B, ntt16::ProPlain{kb.conv, c->log_n}, epi))) return rc;
-    }
+    // both halves at once: sp [K+1][2B][N], conv [l][2B][N], sample index 2 b + p
+    const long long pne = (long long)ne * BN;
+    EpiScale es{kb.sp, Tm.d_inv, Tm.d_inv_sh, c->d_modq, c->n_q, c->log_n};
+    if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, 2 * B, ProAccSp2{kb.acc, BN, pne, l, B, c->log_n}, es)))
+        return rc;
+    ProMdYT2 py{kb.acc, T, BN, pne, l, c->log_n, c->d_pmod, c->d_modq, lin};
+    EpiScale es2{kb.sp + (size_t)np * 2 * BN, Tm.d_inv + np, Tm.d_inv_sh + np, c->d_modq, l, c->log_n};
+    if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * 2 * BN, l, 1, 2 * B, py, es2))) return rc;
+    if ((rc = conv_launch(c, Tm, kb.sp, kb.conv, 1, l, 2 * BN, l, 1))) return rc;
+    EpiMdRsT2 epi{kb.acc, T, out, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN, pne, (long long)l * BN, lin, aff};
+    if ((rc = ntt16::launch_fwd(c, kb.conv, 0, l, 2 * B, ntt16::ProPlain{kb.conv, c->log_n}, epi))) return rc;
     return HK_OK;
 }
 
