@@ -761,6 +761,31 @@ struct EpiMdRsT2 {
         out[p * pout + o] = aff.apply(p, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
     }
 };
+// ModDown of both halves of a key switch (interleaved samples 2 b + p):
+// out_p = (acc_p - v) P^-1 (+ sigma_g(add_p))
+struct EpiModDown2 {
+    const uint64_t *acc, *add0, *add1;
+    uint64_t *out0, *out1;
+    const ulonglong2 *pinv;
+    const ModQ *mq;
+    uint32_t g;
+    int B, log_n;
+    long long BN, pne;
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        const long long pb = P - (long long)l * 2 * B;
+        const int p = (int)(pb & 1);
+        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 w = pinv[l];
+        uint64_t r = mul_shoup(sub_mod(acc[p * pne + o], v, q), w.x, w.y, q);
+        const uint64_t *addend = p ? add1 : add0;
+        if (addend) {
+            const long long src = g == 1u ? o : o - idx + auto_src((uint32_t)idx, g, log_n);
+            r = add_mod(r, addend[src], q);
+        }
+        (p ? out1 : out0)[o] = r;
+    }
+};
 // iNTT prologue: y = acc_l + P d_l with d_l from (a, b)
 struct ProMdYT {
     const uint64_t *acc;
@@ -1035,6 +1060,29 @@ static int ks_moddown(hk_ctx *c, const uint64_t *a, int l, int B, const KsBufs &
     return HK_OK;
 }
 
+// ModDown of both halves (acc [2][ne][B][N]) into out0 / out1 ([l+1][B][N]), adding
+// sigma_g(add0) to half 0 and sigma_g(add1) to half 1 when given. The fused rings
+// run both halves as one launch chain over 2B interleaved samples.
+static int ks_moddown2(hk_ctx *c, int l, int B, const KsBufs &kb, uint64_t *out0, uint64_t *out1,
+                       const uint64_t *add0, const uint64_t *add1, uint32_t g) {
+    const int ne = l + 1 + c->n_p, np = c->n_p;
+    const long long BN = (long long)B * c->n;
+    if (!ntt16::fused(c)) {
+        int rc = ks_moddown(c, kb.acc, l, B, kb, out0, add0, g);
+        if (!rc) rc = ks_moddown(c, kb.acc + (size_t)ne * BN, l, B, kb, out1, add1, g);
+        return rc;
+    }
+    const ConvTable &T = c->moddown;
+    const long long pne = (long long)ne * BN;
+    int rc;
+    EpiScale es{kb.sp, T.d_inv, T.d_inv_sh, c->d_modq, c->n_q, c->log_n};
+    if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, 2 * B, ProAccSp2{kb.acc, BN, pne, l, B, c->log_n}, es)))
+        return rc;
+    if ((rc = conv_launch(c, T, kb.sp, kb.conv, 1, l, 2 * BN, l + 1, 1))) return rc;
+    EpiModDown2 epi{kb.acc, add0, add1, out0, out1, c->d_pinv, c->d_modq, g, B, c->log_n, BN, pne};
+    return ntt16::launch_fwd(c, kb.conv, 0, l + 1, 2 * B, ntt16::ProPlain{kb.conv, c->log_n}, epi);
+}
+
 // ModDown merged with rescale: out ([l][B][N]) = (acc_p + P d_p) / (P q_l)
 static int ks_moddown_rescale(hk_ctx *c, const uint64_t *a, const uint64_t *dp, int l, int B, const KsBufs &kb,
                               uint64_t *out) {
@@ -1150,8 +1198,7 @@ static int keyswitch(hk_ctx *c, const uint64_t *d, int l, int B, int n, const Ke
     if (rc) return rc;
     for (int r = 0; r < n; ++r) {
         if ((rc = ks_ip(c, d, l, B, kb, keys[r], gal[r]))) return rc;
-        if ((rc = ks_moddown(c, kb.acc, l, B, kb, out0[r], add0, gal[r]))) return rc;
-        if ((rc = ks_moddown(c, kb.acc + (size_t)ne * BN, l, B, kb, out1[r], nullptr, gal[r]))) return rc;
+        if ((rc = ks_moddown2(c, l, B, kb, out0[r], out1[r], add0, nullptr, gal[r]))) return rc;
     }
     return HK_OK;
 }
@@ -1502,8 +1549,7 @@ int hk_rotate_sum(hk_ctx *c, const uint64_t *const *cts, int32_t la, const uint3
         return HK_OK;
     }
     const int ne = la + 1 + c->n_p;
-    if ((rc = ks_moddown(c, kb.acc, la, B, kb, out, c0sum, 1u))) return rc;
-    return ks_moddown(c, kb.acc + (size_t)ne * BN, la, B, kb, out + pl, n_id ? c1id : nullptr, 1u);
+    return ks_moddown2(c, la, B, kb, out, out + pl, c0sum, n_id ? c1id : nullptr, 1u);
 }
 
 int hk_rotate(hk_ctx *c, const uint64_t *a, int32_t la, uint32_t g, uint64_t *out, int32_t B) {
