@@ -220,12 +220,16 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
 template <class Pro, class Epi, int CPP>
 __global__ void __launch_bounds__(kTh, 4)
     fwd_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ tw,
-               const double2 *__restrict__ twist, const FpMod *__restrict__ fm, Pro pro, Epi epi) {
+               const double2 *__restrict__ twist, const FpMod *__restrict__ fm, Pro pro, Epi epi, int smaj) {
     constexpr int kT = kCl / CPP;
     extern __shared__ double smd[];
     double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
     const int c = blockIdx.x % CPP;
-    const long long P = blockIdx.x / CPP;
+    long long P = blockIdx.x / CPP;
+    if (smaj) {  // sample-major launch order: the smaj limbs of one sample are adjacent
+        const long long s = P / smaj;
+        P = (P - s * smaj) * B + s;
+    }
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = tw + (size_t)mi * kN;
@@ -506,12 +510,14 @@ inline cudaError_t launch_clustered(K kern, int cpp, long long n_polys, cudaStre
 }
 
 template <class Pro, class Epi>
-inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
+inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi,
+                        bool sample_major = false) {
     const long long n = (long long)n_limbs * B;
     const double2 *tw = (const double2 *)c->d_twf, *twist = (const double2 *)c->d_twist;
     const FpMod *fm = (const FpMod *)c->d_fmod;
     const cudaError_t e =
-        launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi);
+        launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi,
+                         sample_major ? n_limbs : 0);
     ++c->launches;
     if (e != cudaSuccess) return hk_fail(c, HK_E_CUDA, "ntt16 fwd launch: %s", cudaGetErrorString(e));
     HK_LAUNCH_CHECK(c, "ntt16 fwd");
@@ -536,15 +542,19 @@ inline int launch16_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int 
 inline bool fused(const hk_ctx *c) { return c->log_n == kLogN || c->log_n == kLogN + 1; }
 
 template <class Pro, class Epi>
-inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
+// sample_major: launch the limbs of one sample next to each other (epilogues /
+// prologues that read one per-sample operand for every limb, e.g. the rescale's
+// broadcast remainder, then hit L2 instead of HBM)
+inline int launch_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi,
+                      bool sample_major = false) {
     if (n_limbs <= 0 || B <= 0) return HK_OK;
-    if (c->log_n == kLogN) return launch16_fwd(c, inter, limb0, n_limbs, B, pro, epi);
+    if (c->log_n == kLogN) return launch16_fwd(c, inter, limb0, n_limbs, B, pro, epi, sample_major);
     const long long total = (long long)n_limbs * B * kH17;
     k17_pre<Pro><<<hk_grid(total, 256), 256, 0, c->stream>>>(pro, inter, limb0, B, c->d_n17, c->d_n17w, c->d_modq,
                                                              total);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "ntt17 pre");
-    return launch16_fwd(c, inter, limb0, n_limbs, 2 * B, ProPlain{inter, kLogN}, EpiHalf<Epi>{epi, B});
+    return launch16_fwd(c, inter, limb0, n_limbs, 2 * B, ProPlain{inter, kLogN}, EpiHalf<Epi>{epi, B}, sample_major);
 }
 
 template <class Pro, class Epi>

@@ -919,7 +919,7 @@ static int rescale_fused(hk_ctx *c, const RsSrc<KIND> &src, int l, int B, uint64
     if (rc) return rc;
     ProRsBcast pro{L, c->mod_h[l], 2 * B, c->log_n, c->d_modq};
     EpiRescale<KIND> epi{src, out, c->d_rs_qinv + (size_t)l * c->n_q, B};
-    return ntt16::launch_fwd(c, inter, 0, l, 2 * B, pro, epi);
+    return ntt16::launch_fwd(c, inter, 0, l, 2 * B, pro, epi, true);
 }
 
 template <int KIND>

@@ -333,7 +333,7 @@ int main(int argc, char **argv) {
             if (n > polys) break;
             const float ms = time_it(
                 [&] {
-                    CK(launch_clustered(kf, 16, n, 0, (uint64_t *)inter, 0, n, (const double2 *)tw, (const double2 *)twist, (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}));
+                    CK(launch_clustered(kf, 16, n, 0, (uint64_t *)inter, 0, n, (const double2 *)tw, (const double2 *)twist, (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}, 0));
                 },
                 reps);
             printf("P   %5d polys %8.3f ms  %6.3f us/limb-poly\n", n, ms, 1e3 * ms / n);
@@ -355,7 +355,7 @@ int main(int argc, char **argv) {
         const float ms = time_it(
             [&] {
                 CK(launch_clustered(kf, 16, polys, 0, (uint64_t *)inter, 0, polys, (const double2 *)tw, (const double2 *)twist,
-                                    (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}));
+                                    (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}, 0));
             },
             reps);
         printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "P production", ms, 1e3 * ms / polys);
@@ -370,7 +370,7 @@ int main(int argc, char **argv) {
         const float ms = time_it(
             [&] {
                 CK(launch_clustered(ki, 16, polys, 0, (uint64_t *)inter, 0, polys, (const double2 *)tw, (const double2 *)twist,
-                                    (const double2 *)ninv, (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}));
+                                    (const double2 *)ninv, (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}, 0));
             },
             reps);
         printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "P production inverse", ms, 1e3 * ms / polys);
