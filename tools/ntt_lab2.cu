@@ -370,7 +370,7 @@ int main(int argc, char **argv) {
         const float ms = time_it(
             [&] {
                 CK(launch_clustered(ki, 16, polys, 0, (uint64_t *)inter, 0, polys, (const double2 *)tw, (const double2 *)twist,
-                                    (const double2 *)ninv, (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}, 0));
+                                    (const double2 *)ninv, (const FpMod *)fm, ProPlain{in, kLogN}, EpiPlain{out, kLogN}));
             },
             reps);
         printf("%-34s %8.3f ms  %6.3f us/limb-poly\n", "P production inverse", ms, 1e3 * ms / polys);
