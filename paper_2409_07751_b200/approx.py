@@ -1,189 +1,62 @@
-"""HE polynomial evaluation and the composite-sign comparator.
+"""HE polynomial evaluation and the composite-sign comparator: engine deltas.
 
-Restates `/root/reference/pkg/src/hekan/approx.py` for the RNS-CKKS engine:
+The reference side of `/root/reference/pkg/src/hekan/approx.py` is imported,
+not restated: `Polynomial`, `ApproxRange`, `WeightScheme`, the range
+estimators and fitters (`estimate_range`, `fit_weighted_ls`, `fit_ols`,
+`fit_remez`), `poly_eval_depth`, `eval_poly_clear`, `poly_comp_clear` and the
+comparator fitter `build_composite_sign` (its stages are fitted by the
+reference's own Remez code). What lives here is what the RNS-CKKS engine runs
+differently:
 
-* `Polynomial`, `_estrin`, `eval_poly_he`, `eval_poly_clear`,
-  `poly_eval_depth` reproduce the reference's balanced power tree
-  (approx.py:311-418) op for op — same schedule, same counts, same levels.
-  This is the program used for the SiLU polynomials.
-* `CompositeSign` / `poly_comp` (approx.py:431-534) keep the reference's
-  stages (odd minimax polynomials, alpha=7, eps=2^-10) and its level budget,
-  but evaluate each stage in the **Chebyshev basis** with the same tree shape.
-  The reference's monomial coefficients reach 6e10 and its
-  Estrin program diverges under real CKKS noise; re-expanding the SAME
-  polynomial (exact rational conversion of the stored doubles) over T_k gives
-  coefficients <= 1.3 and a stable evaluation. Squarings T_2k = 2 T_k^2 - 1
-  keep ct_mult/pt_mult counts and the level schedule identical to the
-  reference; each power adds one ct add and one constant add.
-* Offline fitting (`estimate_range`, `WeightScheme`, `fit_weighted_ls`) is the
-  model-prep half of approx.py:32-185, restated with the same numpy calls so
-  benchmark models can be built on the GPU box. The Remez fitter is not
-  restated: the default comparator's stages ship as data generated by the
-  reference (paper_2409_07751_b200/data/composite_sign.json, made by
-  tests/golden/make_golden.py).
+* `_estrin` keeps the reference's balanced power tree (approx.py:369-405) —
+  same tree, same counts, same levels — and folds each four-coefficient block
+  whose low half is a leaf (`c1 x + c0`) into the relinearised product that
+  consumes it (`HeBackend.mul_lin`: one rescale instead of two);
+* the comparator stages are the reference's polynomials re-expanded exactly
+  over Chebyshev T_k (|c| <= 1.3 instead of monomials up to 6e10, SURVEY
+  §0.4, which diverge under real CKKS noise) and evaluated with the same tree
+  shape, so levels and multiplication counts are unchanged; each squaring is
+  T_2k = 2 T_k^2 - 1 (`HeBackend.mul_affine`, one product);
+* SiLU fits whose monomial intermediates blow up (c3's degree 63) run as the
+  same polynomial in T_k on the fit interval (+1 level off the critical path).
 """
 
 from __future__ import annotations
 
 import functools
-import json
 import math
-import os
 from dataclasses import dataclass, field
 from fractions import Fraction
 
 import numpy as np
-from numpy.polynomial import chebyshev as npcheb
-from numpy.polynomial import polynomial as nppoly
 
-from .errors import EmptySamples, IllConditioned, InputOutOfRange
+from ._ref import hekan
+from .errors import InputOutOfRange
 
-DATA_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
-
-
-# ---------------------------------------------------------------------------
-# core types (approx.py:32-103)
-# ---------------------------------------------------------------------------
-
-
-@dataclass(frozen=True)
-class Polynomial:
-    """Ascending monomial coefficients, trailing zeros trimmed."""
-
-    coeffs: tuple
-
-    def __post_init__(self):
-        c = tuple(float(v) for v in self.coeffs)
-        n = len(c)
-        while n > 1 and c[n - 1] == 0.0:
-            n -= 1
-        object.__setattr__(self, "coeffs", c[:n] if n > 0 else (0.0,))
-
-    @property
-    def degree(self) -> int:
-        return len(self.coeffs) - 1
-
-    def __call__(self, x):
-        return nppoly.polyval(x, self.coeffs)
-
-    def to_json(self) -> list:
-        return list(self.coeffs)
-
-    @classmethod
-    def from_json(cls, doc) -> "Polynomial":
-        return cls(tuple(doc))
-
-
-@dataclass(frozen=True)
-class ApproxRange:
-    lo: float
-    hi: float
-    mu: float
-    sigma: float
-    degenerate: bool = False
-
-
-@dataclass(frozen=True)
-class WeightScheme:
-    """Piecewise-constant LS weights, heavy inside mu +/- 3 sigma (PAPER §4.1)."""
-
-    inner_lo: float
-    inner_hi: float
-    inner_weight: float = 10.0
-    outer_weight: float = 1.0
-
-    def __post_init__(self):
-        if not self.inner_weight >= self.outer_weight > 0:
-            raise ValueError("need inner_weight >= outer_weight > 0")
-
-    @classmethod
-    def from_moments(cls, mu: float, sigma: float, width: float = 3.0,
-                     inner_weight: float = 10.0, outer_weight: float = 1.0) -> "WeightScheme":
-        return cls(mu - width * sigma, mu + width * sigma, inner_weight, outer_weight)
-
-    def weights(self, x: np.ndarray) -> np.ndarray:
-        inside = (x >= self.inner_lo) & (x <= self.inner_hi)
-        return np.where(inside, self.inner_weight, self.outer_weight)
-
-
-ACTIVATION_PRESETS = {
-    "mnist": {"range": (-12.4, 14.74), "degree": 10},
-    "fmnist": {"range": (-9.77, 11.01), "degree": 10},
-    "cifar10": {"range": (-11.90, 10.99), "degree": 15},
-}
-
-
-def range_from_moments(mu: float, sigma: float, x_min: float = -math.inf,
-                       x_max: float = math.inf, factor: float = 5.0,
-                       degenerate_halfwidth: float = 1e-6) -> ApproxRange:
-    """[max(mu - f sigma, x_min), min(mu + f sigma, x_max)] (approx.py:111-126)."""
-    if x_min > x_max:
-        raise ValueError(f"x_min {x_min} > x_max {x_max}")
-    if sigma == 0.0:
-        return ApproxRange(mu - degenerate_halfwidth, mu + degenerate_halfwidth, mu, 0.0,
-                           degenerate=True)
-    return ApproxRange(max(mu - factor * sigma, x_min), min(mu + factor * sigma, x_max), mu, sigma)
-
-
-def estimate_range(samples, x_min: float = -math.inf, x_max: float = math.inf,
-                   factor: float = 5.0) -> ApproxRange:
-    arr = np.asarray(samples, dtype=float).ravel()
-    if arr.size == 0:
-        raise EmptySamples("estimate_range needs at least one sample")
-    return range_from_moments(float(np.mean(arr)), float(np.std(arr)), x_min, x_max, factor)
-
-
-def fit_weighted_ls(target, rng: ApproxRange, degree: int, w: WeightScheme | None = None,
-                    n_samples: int | None = None) -> Polynomial:
-    """Weighted LS in a Chebyshev basis, returned as monomials (approx.py:155-179)."""
-    if degree < 0:
-        raise ValueError("degree must be >= 0")
-    if n_samples is None:
-        n_samples = 200 * (degree + 1)
-    if n_samples <= degree:
-        raise ValueError(f"n_samples {n_samples} must exceed degree {degree}")
-    if not rng.lo < rng.hi:
-        raise IllConditioned(f"degenerate fitting interval [{rng.lo}, {rng.hi}]")
-    x = np.linspace(rng.lo, rng.hi, n_samples)
-    y = np.asarray(target(x), dtype=float)
-    weights = w.weights(x) if w is not None else np.ones_like(x)
-    try:
-        series, diag = npcheb.Chebyshev.fit(x, y, degree, domain=[rng.lo, rng.hi],
-                                            w=np.sqrt(weights), full=True)
-    except np.linalg.LinAlgError as exc:
-        raise IllConditioned(str(exc)) from exc
-    if diag[1] < degree + 1:
-        raise IllConditioned(f"rank {diag[1]} < {degree + 1}")
-    return Polynomial(tuple(series.convert(kind=nppoly.Polynomial).coef))
-
-
-def fit_ols(target, rng: ApproxRange, degree: int, n_samples: int | None = None) -> Polynomial:
-    return fit_weighted_ls(target, rng, degree, w=None, n_samples=n_samples)
+_ha = hekan.approx
+Polynomial = _ha.Polynomial
+ApproxRange = _ha.ApproxRange
+WeightScheme = _ha.WeightScheme
+range_from_moments = _ha.range_from_moments
+estimate_range = _ha.estimate_range
+fit_weighted_ls = _ha.fit_weighted_ls
+fit_ols = _ha.fit_ols
+fit_remez = _ha.fit_remez
+poly_eval_depth = _ha.poly_eval_depth
+eval_poly_clear = _ha.eval_poly_clear
+poly_comp_clear = _ha.poly_comp_clear
+_ArrayOps = _ha._ArrayOps
+_trimmed = _ha._trimmed
 
 
 # ---------------------------------------------------------------------------
-# balanced power tree (approx.py:311-418) — the reference program
+# balanced power tree on the engine (approx.py:311-418)
 # ---------------------------------------------------------------------------
 
 
-class _HeOps:
-    """Runs an evaluation schedule on a backend (approx.py:311-332)."""
-
-    def __init__(self, x):
-        self.x = x
-        self.be = x.backend
-
-    def mul(self, a, b):
-        return self.be.mul(a, b)
-
-    def mul_const(self, a, c):
-        return self.be.mul(a, c)
-
-    def add(self, a, b):
-        return self.be.add(a, b)
-
-    def add_const(self, a, c):
-        return self.be.add(a, c)
+class _HeOps(_ha._HeOps):
+    """The reference adapter (approx.py:311-332) plus the engine's fused
+    combines; public constants are trivial encryptions batched like x."""
 
     def mul_lin(self, a, b, x, k):
         return self.be.mul_lin(a, b, x, k)
@@ -192,48 +65,16 @@ class _HeOps:
         return self.be.mul_affine(a, b, mult, c)
 
     def const(self, c):
-        # trivial public constant at the input level: encrypt of a full vector
-        # (approx.py:330-332); batched like the input
-        rows = np.full((self.x.batch, self.be.config.slot_count), c)
-        return self.be.encrypt(rows if self.x.batched else rows[0], self.x.level)
+        rows = np.full((getattr(self.x, "batch", 1), self.be.config.slot_count), c)
+        return self.be.encrypt(rows if getattr(self.x, "batched", False) else rows[0], self.x.level)
 
 
-class _ArrayOps:
-    """Same schedule on numpy arrays (approx.py:335-360)."""
-
-    def __init__(self, x: np.ndarray):
-        self.x = x
-
-    @staticmethod
-    def mul(a, b):
-        return a * b
-
-    @staticmethod
-    def mul_const(a, c):
-        return a * c
-
-    @staticmethod
-    def add(a, b):
-        return a + b
-
-    @staticmethod
-    def add_const(a, c):
-        return a + c
-
-    def const(self, c):
-        return np.full_like(self.x, c)
-
-
-def _trimmed(coeffs) -> np.ndarray:
-    c = np.asarray(coeffs, dtype=float).ravel()
-    n = len(c)
-    while n > 1 and c[n - 1] == 0.0:
-        n -= 1
-    return c[:n]
+def _fusable(ops, method: str) -> bool:
+    return hasattr(ops, method) and hasattr(getattr(ops.x, "backend", None), method)
 
 
 def _combine(ops, xpow, lo_val, hi_val):
-    """p = hi * xpow + lo with the reference's float/zero short-cuts."""
+    """hi * xpow + lo with the reference's float/zero short-cuts (approx.py:393-403)."""
     if isinstance(hi_val, float):
         term = None if hi_val == 0.0 else ops.mul_const(xpow, hi_val)
     else:
@@ -246,42 +87,31 @@ def _combine(ops, xpow, lo_val, hi_val):
 
 
 def _fused_combine(ops, xpow, x, c0: float, c1: float, hi_val):
-    """hi * xpow + (c1 * x + c0) for a block of four coefficients whose low
-    half is a leaf and whose high half is a ciphertext: `mul_lin` folds the
-    leaf's scalar product into the relinearised product's rescale (same op
-    counts as _combine's mul_const, mul, add, add_const)."""
+    """hi * xpow + (c1 x + c0) as one relinearised product (`mul_lin`) plus the
+    constant: the counts of _combine's mul_const, mul, add, add_const."""
     t = ops.mul_lin(xpow, hi_val, x, c1)
     return t if c0 == 0.0 else ops.add_const(t, float(c0))
 
 
-def _estrin(ops, coeffs: np.ndarray):
-    """Balanced power tree over monomials: ceil(log2(n)) levels."""
-    n = len(coeffs)
-    if n == 1 or (n > 0 and not np.any(coeffs[1:])):
-        return ops.const(float(coeffs[0]))
-    m = max(1, (n - 1).bit_length())
-    padded = np.zeros(1 << m)
-    padded[:n] = coeffs
-    pows = [ops.x]
-    for _ in range(m - 1):
-        pows.append(ops.mul(pows[-1], pows[-1]))
+def _power_tree(ops, padded: np.ndarray, pows: list, split):
+    """Shared recursion of the monomial and Chebyshev trees. `split(c)` maps a
+    block's 2h coefficients to (low, high) with p = high * P_h + low."""
+    fuse = _fusable(ops, "mul_lin")
 
-    fuse = hasattr(ops, "mul_lin") and hasattr(ops.x, "backend") and hasattr(ops.x.backend, "mul_lin")
-
-    def block(lo: int, size: int):
-        if size == 1:
-            return float(padded[lo])
-        half = size // 2
-        if fuse and size == 4 and padded[lo + 1] != 0.0:
-            hi_val = block(lo + half, half)
+    def block(c: np.ndarray):
+        if len(c) == 1:
+            return float(c[0])
+        lo_c, hi_c = split(c)
+        if fuse and len(c) == 4 and lo_c[1] != 0.0:
+            hi_val = block(hi_c)
             if not isinstance(hi_val, float):
-                return _fused_combine(ops, pows[1], pows[0], float(padded[lo]), float(padded[lo + 1]), hi_val)
-            return _combine(ops, pows[1], block(lo, half), hi_val)
-        lo_val = block(lo, half)
-        hi_val = block(lo + half, half)
-        return _combine(ops, pows[half.bit_length() - 1], lo_val, hi_val)
+                return _fused_combine(ops, pows[1], pows[0], float(lo_c[0]), float(lo_c[1]), hi_val)
+            return _combine(ops, pows[1], block(lo_c), hi_val)
+        lo_val = block(lo_c)
+        hi_val = block(hi_c)
+        return _combine(ops, pows[(len(c) // 2).bit_length() - 1], lo_val, hi_val)
 
-    out = block(0, 1 << m)
+    out = block(padded)
     # `block` is a recursive closure (a reference cycle through its own cell):
     # drop it and the powers so the ciphertexts free now, not at the next gc pass
     del block
@@ -289,20 +119,34 @@ def _estrin(ops, coeffs: np.ndarray):
     return ops.const(out) if isinstance(out, float) else out
 
 
-def poly_eval_depth(p) -> int:
-    degree = p if isinstance(p, int) else p.degree
-    if degree <= 0:
-        return 0
-    return math.ceil(math.log2(degree + 1))
+def _padded(coeffs: np.ndarray):
+    n = len(coeffs)
+    m = max(1, (n - 1).bit_length())
+    padded = np.zeros(1 << m)
+    padded[:n] = coeffs
+    return padded, m
 
 
-def eval_poly_he(a, p: Polynomial):
-    """Reference program (monomial Estrin) on the encrypted backend."""
+def _mono_split(c: np.ndarray):
+    h = len(c) // 2
+    return c[:h], c[h:]
+
+
+def _estrin(ops, coeffs: np.ndarray):
+    """The reference's balanced power tree over monomials (ceil(log2 n) levels)."""
+    n = len(coeffs)
+    if n == 1 or (n > 0 and not np.any(coeffs[1:])):
+        return ops.const(float(coeffs[0]))
+    padded, m = _padded(coeffs)
+    pows = [ops.x]
+    for _ in range(m - 1):
+        pows.append(ops.mul(pows[-1], pows[-1]))
+    return _power_tree(ops, padded, pows, _mono_split)
+
+
+def eval_poly_he(a, p):
+    """Reference program (monomial Estrin, approx.py:416-418) on the engine."""
     return _estrin(_HeOps(a), _trimmed(p.coeffs))
-
-
-def eval_poly_clear(p: Polynomial, x: np.ndarray) -> np.ndarray:
-    return _estrin(_ArrayOps(np.asarray(x, dtype=float)), _trimmed(p.coeffs))
 
 
 # ---------------------------------------------------------------------------
@@ -311,8 +155,8 @@ def eval_poly_clear(p: Polynomial, x: np.ndarray) -> np.ndarray:
 
 
 def _cheb_split(c: np.ndarray):
-    """p = q * T_h + r for p = sum c_i T_i over 2h coefficients, using
-    T_{h+j} = 2 T_h T_j - T_{h-j}."""
+    """p = q T_h + r for p = sum c_i T_i over 2h coefficients, by
+    T_{h+j} = 2 T_h T_j - T_{h-j}; returns (r, q)."""
     h = len(c) // 2
     q = np.zeros(h)
     r = np.array(c[:h], dtype=float)
@@ -320,61 +164,36 @@ def _cheb_split(c: np.ndarray):
     for j in range(1, h):
         q[j] = 2.0 * c[h + j]
         r[h - j] -= c[h + j]
-    return q, r
+    return r, q
 
 
 def _cheb_tree(ops, coeffs: np.ndarray):
-    """Evaluate sum c_k T_k(x) with the Estrin tree shape: ceil(log2(n)) levels,
-    same ct/pt multiplication counts as `_estrin` on the same sparsity."""
+    """sum c_k T_k(x) with the Estrin tree shape: ceil(log2 n) levels and the
+    ct/pt multiplication counts `_estrin` has on the same sparsity."""
     n = len(coeffs)
     if n == 1 or (n > 0 and not np.any(coeffs[1:])):
         return ops.const(float(coeffs[0]))
-    m = max(1, (n - 1).bit_length())
-    padded = np.zeros(1 << m)
-    padded[:n] = coeffs
+    padded, m = _padded(coeffs)
     tpows = [ops.x]
-    affine = hasattr(ops, "mul_affine") and hasattr(ops.x, "backend") and hasattr(ops.x.backend, "mul_affine")
+    affine = _fusable(ops, "mul_affine")
     for _ in range(m - 1):
         if affine:  # T_2k = 2 T_k^2 - 1 in the product's epilogue (bit-identical)
             tpows.append(ops.mul_affine(tpows[-1], tpows[-1], 2, -1.0))
             continue
         sq = ops.mul(tpows[-1], tpows[-1])
         tpows.append(ops.add_const(ops.add(sq, sq), -1.0))
-
-    fuse = hasattr(ops, "mul_lin") and hasattr(ops.x, "backend") and hasattr(ops.x.backend, "mul_lin")
-
-    def block(c: np.ndarray):
-        if len(c) == 1:
-            return float(c[0])
-        q, r = _cheb_split(c)
-        if fuse and len(c) == 4 and r[1] != 0.0:
-            hi_val = block(q)
-            if not isinstance(hi_val, float):
-                return _fused_combine(ops, tpows[1], tpows[0], float(r[0]), float(r[1]), hi_val)
-            return _combine(ops, tpows[1], block(r), hi_val)
-        lo_val = block(r)
-        hi_val = block(q)
-        return _combine(ops, tpows[(len(c) // 2).bit_length() - 1], lo_val, hi_val)
-
-    out = block(padded)
-    del block  # recursive closure: break the cycle so the powers free now
-    tpows.clear()
-    return ops.const(out) if isinstance(out, float) else out
+    return _power_tree(ops, padded, tpows, _cheb_split)
 
 
-def mono_to_cheb(mono, h: float = 1.0, out_scale: float = 1.0) -> np.ndarray:
-    """Exact re-expansion: coefficients c with sum c_k T_k(y) == p(h y) / out_scale,
-    where p has the given (exactly represented) monomial coefficients."""
-    mono = [Fraction(float(v)) for v in mono]
-    n = len(mono)
-    hF, sF = Fraction(h), Fraction(out_scale)
-    # T_k as exact monomial coefficient lists
+def _cheb_from_exact(qc) -> np.ndarray:
+    """Exact monomial coefficients (Fractions) -> Chebyshev coefficients."""
+    n = len(qc)
     T = [[Fraction(1)], [Fraction(0), Fraction(1)]]
     for k in range(2, n):
         a = [Fraction(0)] + [2 * v for v in T[k - 1]]
         b = T[k - 2] + [Fraction(0)] * (len(a) - len(T[k - 2]))
         T.append([x - y for x, y in zip(a, b)])
-    rem = [a * hF ** i / sF for i, a in enumerate(mono)]
+    rem = list(qc)
     out = [Fraction(0)] * n
     for k in range(n - 1, -1, -1):
         if rem[k] == 0:
@@ -384,6 +203,29 @@ def mono_to_cheb(mono, h: float = 1.0, out_scale: float = 1.0) -> np.ndarray:
         for i in range(k + 1):
             rem[i] -= ck * T[k][i]
     return np.array([float(v) for v in out])
+
+
+def mono_to_cheb(mono, h: float = 1.0, out_scale: float = 1.0) -> np.ndarray:
+    """c with sum c_k T_k(y) == p(h y) / out_scale exactly, for the (exactly
+    represented) monomial coefficients of p."""
+    hF, sF = Fraction(h), Fraction(out_scale)
+    return _cheb_from_exact([Fraction(float(a)) * hF ** i / sF for i, a in enumerate(mono)])
+
+
+def mono_to_cheb_affine(mono, lo: float, hi: float) -> np.ndarray:
+    """c with sum c_k T_k(u) == p(x) for x = (u (hi - lo) + lo + hi) / 2, exactly."""
+    coef = [Fraction(float(v)) for v in mono]
+    n = len(coef)
+    half, mid = (Fraction(hi) - Fraction(lo)) / 2, (Fraction(hi) + Fraction(lo)) / 2
+    qc = [coef[-1]] + [Fraction(0)] * (n - 1)  # Horner over polynomials in u
+    for i in range(n - 2, -1, -1):
+        nq = [Fraction(0)] * n
+        for k in range(n - 1):
+            nq[k + 1] += qc[k] * half
+            nq[k] += qc[k] * mid
+        nq[0] += coef[i]
+        qc = nq
+    return _cheb_from_exact(qc)
 
 
 @dataclass(frozen=True)
@@ -420,46 +262,21 @@ def eval_cheb_clear(p: ChebPoly, y: np.ndarray) -> np.ndarray:
 CHEB_MAGNITUDE_LIMIT = 1e3
 
 
+def silu_interval(layer) -> tuple:
+    """The SiLU fit interval: the layer's `fit_range` when it records one,
+    else the reference's act_stats window mu +/- 5 sigma (approx.py:111-126)."""
+    fr = getattr(layer, "fit_range", None)
+    if fr is not None:
+        return tuple(float(v) for v in fr)
+    mu, sigma = layer.act_stats
+    return (mu - 5.0 * sigma, mu + 5.0 * sigma)
+
+
 def silu_uses_cheb(layer) -> bool:
-    lo, hi = layer.silu_interval
+    lo, hi = silu_interval(layer)
     M = max(abs(lo), abs(hi))
     mag = sum(abs(c) * M ** k for k, c in enumerate(layer.silu_poly.coeffs))
     return mag > CHEB_MAGNITUDE_LIMIT
-
-
-def mono_to_cheb_affine(mono, lo: float, hi: float) -> np.ndarray:
-    """c with sum c_k T_k(u) == p(x) for x = (u (hi - lo) + lo + hi) / 2, exactly."""
-    coef = [Fraction(float(v)) for v in mono]
-    n = len(coef)
-    half, mid = (Fraction(hi) - Fraction(lo)) / 2, (Fraction(hi) + Fraction(lo)) / 2
-    qc = [coef[-1]] + [Fraction(0)] * (n - 1)  # Horner over polynomials in u
-    for i in range(n - 2, -1, -1):
-        nq = [Fraction(0)] * n
-        for k in range(n - 1):
-            nq[k + 1] += qc[k] * half
-            nq[k] += qc[k] * mid
-        nq[0] += coef[i]
-        qc = nq
-    return _cheb_from_exact(qc)
-
-
-def _cheb_from_exact(qc) -> np.ndarray:
-    n = len(qc)
-    T = [[Fraction(1)], [Fraction(0), Fraction(1)]]
-    for k in range(2, n):
-        a = [Fraction(0)] + [2 * v for v in T[k - 1]]
-        b = T[k - 2] + [Fraction(0)] * (len(a) - len(T[k - 2]))
-        T.append([x - y for x, y in zip(a, b)])
-    rem = list(qc)
-    out = [Fraction(0)] * n
-    for k in range(n - 1, -1, -1):
-        if rem[k] == 0:
-            continue
-        ck = rem[k] / T[k][k]
-        out[k] = ck
-        for i in range(k + 1):
-            rem[i] -= ck * T[k][i]
-    return np.array([float(v) for v in out])
 
 
 @functools.lru_cache(maxsize=256)
@@ -468,8 +285,13 @@ def _silu_cheb_cached(coeffs: tuple, lo: float, hi: float) -> tuple:
 
 
 def silu_affine(layer) -> tuple:
-    lo, hi = layer.silu_interval
+    lo, hi = silu_interval(layer)
     return 2.0 / (hi - lo), -(lo + hi) / (hi - lo)
+
+
+def _silu_cheb_coeffs(layer) -> np.ndarray:
+    lo, hi = silu_interval(layer)
+    return _trimmed(np.array(_silu_cheb_cached(tuple(layer.silu_poly.coeffs), lo, hi)))
 
 
 def eval_silu_he(ct, layer):
@@ -480,15 +302,13 @@ def eval_silu_he(ct, layer):
     be = ct.backend
     a, b = silu_affine(layer)
     u = be.add(be.mul(ct, a), b)
-    lo, hi = layer.silu_interval
-    return _cheb_tree(_HeOps(u), _trimmed(np.array(_silu_cheb_cached(layer.silu_poly.coeffs, lo, hi))))
+    return _cheb_tree(_HeOps(u), _silu_cheb_coeffs(layer))
 
 
 def eval_silu_cheb_clear(layer, x: np.ndarray) -> np.ndarray:
     a, b = silu_affine(layer)
     u = np.asarray(x, dtype=float) * a + b
-    lo, hi = layer.silu_interval
-    return _cheb_tree(_ArrayOps(u), _trimmed(np.array(_silu_cheb_cached(layer.silu_poly.coeffs, lo, hi))))
+    return _cheb_tree(_ArrayOps(u), _silu_cheb_coeffs(layer))
 
 
 def silu_depth(layer) -> int:
@@ -506,34 +326,17 @@ def _bound_up(v: float) -> float:
 
 
 @dataclass(frozen=True)
-class CompositeSign:
-    """Composition of odd minimax stages approximating sign on +-[delta, 1]
-    (approx.py:431-458). `stages` are the reference's monomial polynomials;
-    `cheb` the Chebyshev re-expansion used under encryption: stage k reads
-    y_k = x_k / h_k in [-1, 1] and emits p_k(x_k) / h_{k+1} (h_0 = 1, h_K = 1)."""
+class CompositeSign(_ha.CompositeSign):
+    """The reference's composite sign (approx.py:431-458: same stages, depth,
+    delta, clear schedule) carrying its Chebyshev re-expansion `cheb`: stage k
+    reads y_k = x_k / h_k in [-1, 1] and emits p_k(x_k) / h_{k+1}
+    (h_0 = h_K = 1)."""
 
-    stages: tuple
-    precision_alpha: float
-    target_eps: float
     cheb: tuple = field(default=(), compare=False)
 
     def __post_init__(self):
         if not self.cheb:
             object.__setattr__(self, "cheb", _cheb_stages(self.stages))
-
-    @property
-    def delta(self) -> float:
-        return 2.0 ** (-self.precision_alpha)
-
-    def depth(self) -> int:
-        return sum(poly_eval_depth(s) for s in self.stages) + 1
-
-    def apply_clear(self, y: np.ndarray) -> np.ndarray:
-        """Reference schedule (monomial Estrin), approx.py:451-456."""
-        s = np.asarray(y, dtype=float)
-        for stage in self.stages:
-            s = eval_poly_clear(stage, s)
-        return s
 
     def apply_cheb_clear(self, y: np.ndarray) -> np.ndarray:
         """Plaintext twin of the encrypted (Chebyshev) schedule."""
@@ -542,9 +345,25 @@ class CompositeSign:
             s = eval_cheb_clear(cp, s)
         return s
 
-    def certified_max_error(self, grid_size: int = 100_000) -> float:
-        y = np.linspace(self.delta, 1.0, grid_size)
-        return float(np.max(np.abs(self.apply_clear(y) - 1.0)))
+    def cheb_schedule(self) -> "ChebSchedule":
+        return ChebSchedule(self)
+
+
+class ChebSchedule:
+    """A comparator view whose `apply_clear` is the Chebyshev schedule, so the
+    reference's cleartext twins (`poly_comp_clear`, `basis_clear`,
+    `layer_forward_plain(mode="mirrored")`) mirror what the engine runs."""
+
+    def __init__(self, cs: CompositeSign):
+        self.cs = cs
+        self.stages = cs.stages
+        self.delta = cs.delta
+
+    def depth(self) -> int:
+        return self.cs.depth()
+
+    def apply_clear(self, y):
+        return self.cs.apply_cheb_clear(y)
 
 
 def _cheb_stages(stages) -> tuple:
@@ -553,36 +372,31 @@ def _cheb_stages(stages) -> tuple:
     grid = np.linspace(-1.0, 1.0, 1 << 16)
     for idx, st in enumerate(stages):
         last = idx == len(stages) - 1
-        if last:
-            h_next = 1.0
-        else:
-            h_next = _bound_up(float(np.max(np.abs(st(h * grid)))))
-        c = mono_to_cheb(st.coeffs, h=h, out_scale=h_next)
-        out.append(ChebPoly(tuple(c), h, h_next))
+        h_next = 1.0 if last else _bound_up(float(np.max(np.abs(st(h * grid)))))
+        out.append(ChebPoly(tuple(mono_to_cheb(st.coeffs, h=h, out_scale=h_next)), h, h_next))
         h = h_next
     return tuple(out)
 
 
 @functools.lru_cache(maxsize=None)
 def build_composite_sign(alpha: float = 7.0, target_eps: float = 2.0 ** -10) -> CompositeSign:
-    """Comparator stages for (alpha, eps) (approx.py:479-508). The stage
-    polynomials are the reference fitter's output for the default (7, 2^-10),
-    shipped as data; other settings need the offline fitter (out of scope)."""
-    path = os.path.join(DATA_DIR, "composite_sign.json")
-    with open(path) as fh:
-        doc = json.load(fh)
-    for entry in doc["comparators"]:
-        if float(entry["alpha"]) == float(alpha) and float(entry["target_eps"]) == float(target_eps):
-            stages = tuple(Polynomial(tuple(s)) for s in entry["stages"])
-            return CompositeSign(stages, float(alpha), float(target_eps))
-    raise NotImplementedError(
-        f"no shipped comparator for alpha={alpha}, eps={target_eps}; regenerate "
-        "paper_2409_07751_b200/data/composite_sign.json with tests/golden/make_golden.py")
+    """The reference fitter's comparator (approx.py:479-508) with its
+    Chebyshev re-expansion attached."""
+    ref = _ha.build_composite_sign(alpha, target_eps)
+    return CompositeSign(ref.stages, ref.precision_alpha, ref.target_eps)
 
 
-def poly_comp(a, b, cs: CompositeSign, check_range: bool = False):
+def as_engine_comparator(cs):
+    """A reference `CompositeSign` (or ours) as the engine's Chebyshev one."""
+    if isinstance(cs, CompositeSign) or not isinstance(cs, _ha.CompositeSign):
+        return cs
+    return CompositeSign(cs.stages, cs.precision_alpha, cs.target_eps)
+
+
+def poly_comp(a, b, cs, check_range: bool = False):
     """step(a - b) under encryption: ~1 for a > b, ~0 for a < b, 1/2 at ties
-    (approx.py:511-528). Stages run in the Chebyshev basis (module doc)."""
+    (approx.py:511-528), the stages run in the Chebyshev basis."""
+    cs = as_engine_comparator(cs)
     be = a.backend
     d = be.sub(a, b)
     if check_range:
@@ -596,11 +410,6 @@ def poly_comp(a, b, cs: CompositeSign, check_range: bool = False):
     return be.mul(s, 0.5)
 
 
-def poly_comp_clear(d: np.ndarray, cs: CompositeSign) -> np.ndarray:
-    """Reference cleartext twin (monomial schedule), approx.py:531-534."""
-    return (cs.apply_clear(d) + 1.0) * 0.5
-
-
 def poly_comp_cheb_clear(d: np.ndarray, cs: CompositeSign) -> np.ndarray:
     """Twin of the encrypted (Chebyshev) comparator schedule."""
-    return (cs.apply_cheb_clear(d) + 1.0) * 0.5
+    return poly_comp_clear(d, ChebSchedule(as_engine_comparator(cs)))

@@ -29,11 +29,12 @@ import hashlib
 import itertools
 import json
 import math
+import secrets
 import struct
-from dataclasses import dataclass, field, fields, replace
 
 import numpy as np
 
+from ._ref import hekan
 from .errors import CorruptFile, DepthExhausted, InputTooLong, LengthMismatch, SchemaMismatch
 from .params import CkksParams, kan_params
 
@@ -41,87 +42,14 @@ OP_KINDS = ("add", "sub", "mul_ct", "mul_pt")
 
 
 # ---------------------------------------------------------------------------
-# configuration and counters (backend.py:23-105)
+# configuration, counters, plain operands: the reference's own types
+# (backend.py:23-112), so configs, counters and plain vectors pass across the
+# boundary unchanged
 # ---------------------------------------------------------------------------
 
-
-@dataclass(frozen=True)
-class BackendConfig:
-    """Reference scheme parameters (backend.py:23-66). slot_count = N/2 of the
-    CKKS ring; depth_budget = top level (number of rescaling primes)."""
-
-    slot_count: int
-    depth_budget: int
-    noise_std: float = 0.0
-    rng_seed: int = 0
-
-    def __post_init__(self):
-        if self.slot_count <= 0 or (self.slot_count & (self.slot_count - 1)) != 0:
-            raise ValueError(f"slot_count must be a positive power of two, got {self.slot_count}")
-        if self.depth_budget < 0:
-            raise ValueError("depth_budget must be >= 0")
-        if self.noise_std < 0:
-            raise ValueError("noise_std must be >= 0")
-
-    @classmethod
-    def from_json(cls, source) -> "BackendConfig":
-        if isinstance(source, dict):
-            doc = source
-        elif isinstance(source, str) and source.lstrip().startswith("{"):
-            doc = json.loads(source)
-        else:
-            with open(source) as fh:
-                doc = json.load(fh)
-        known = {f.name for f in fields(cls)}
-        unknown = set(doc) - known
-        if unknown:
-            raise ValueError(f"unknown BackendConfig keys: {sorted(unknown)}")
-        return cls(**doc)
-
-    def to_json(self) -> dict:
-        return {"slot_count": self.slot_count, "depth_budget": self.depth_budget,
-                "noise_std": self.noise_std, "rng_seed": self.rng_seed}
-
-
-@dataclass
-class OpCounter:
-    """Logical op tallies (backend.py:69-105)."""
-
-    adds: int = 0
-    subs: int = 0
-    ct_mults: int = 0
-    pt_mults: int = 0
-    rotations: int = 0
-    max_depth_consumed: int = 0
-
-    def copy(self) -> "OpCounter":
-        return replace(self)
-
-    def merge(self, other: "OpCounter") -> None:
-        self.adds += other.adds
-        self.subs += other.subs
-        self.ct_mults += other.ct_mults
-        self.pt_mults += other.pt_mults
-        self.rotations += other.rotations
-        self.max_depth_consumed = max(self.max_depth_consumed, other.max_depth_consumed)
-
-    def since(self, earlier: "OpCounter") -> "OpCounter":
-        return OpCounter(adds=self.adds - earlier.adds, subs=self.subs - earlier.subs,
-                         ct_mults=self.ct_mults - earlier.ct_mults,
-                         pt_mults=self.pt_mults - earlier.pt_mults,
-                         rotations=self.rotations - earlier.rotations,
-                         max_depth_consumed=self.max_depth_consumed)
-
-    @property
-    def mults(self) -> int:
-        return self.ct_mults + self.pt_mults
-
-
-@dataclass(frozen=True)
-class PlainVector:
-    """Unencrypted slot vector (backend.py:108-112)."""
-
-    slots: np.ndarray
+BackendConfig = hekan.backend.BackendConfig
+OpCounter = hekan.backend.OpCounter
+PlainVector = hekan.backend.PlainVector
 
 
 class CipherText:
@@ -186,7 +114,7 @@ class HeBackend:
     product; tests may substitute the CPU oracle engine to check bit-exactness."""
 
     def __init__(self, config: BackendConfig, params: CkksParams | None = None,
-                 engine=None, device: int = 0):
+                 engine=None, device: int = 0, seed: int | None = None, enc_stream: int = 0):
         if params is None:
             log_n = int(math.log2(config.slot_count)) + 1
             params = kan_params(config.depth_budget, log_n=log_n)
@@ -194,6 +122,12 @@ class HeBackend:
             raise ValueError(f"params give {params.slot_count} slots, config {config.slot_count}")
         if config.depth_budget > params.depth:
             raise ValueError(f"depth_budget {config.depth_budget} > chain depth {params.depth}")
+        if config.noise_std > 0:
+            # the reference's NoisyBackend (backend.py:281-297) simulates noise; a
+            # real scheme carries its own, so refuse rather than run other semantics
+            raise NotImplementedError(
+                "noise_std > 0 selects the reference's NoisyBackend simulator; the RNS-CKKS "
+                "engine's noise is the scheme's own (use noise_std = 0)")
         self.config = config
         self.params = params
         self.counter = OpCounter()
@@ -208,6 +142,12 @@ class HeBackend:
         self._mat_cache: dict = {}
         self._pt_cache_bytes = 0
         self.pt_cache_limit = 8 << 30
+        # Key and encryption randomness: the OS CSPRNG unless a seed is passed
+        # explicitly (bit-exact oracle parity; identical keys on every rank of a
+        # sharded run, each rank with its own `enc_stream` so no two
+        # encryptions share (a, e)).
+        self._master = secrets.randbits(64) if seed is None else int(seed)
+        self._enc_stream = int(enc_stream)
         self.engine.call("hk_keygen", C.c_uint64(self._seed("keys")))
 
     # ------------------------------------------------------------------
@@ -215,7 +155,7 @@ class HeBackend:
     # ------------------------------------------------------------------
 
     def _seed(self, what: str, idx: int = 0) -> int:
-        h = hashlib.blake2b(f"{self.config.rng_seed}:{what}:{idx}".encode(), digest_size=8)
+        h = hashlib.blake2b(f"{self._master}:{what}:{idx}".encode(), digest_size=8)
         return int.from_bytes(h.digest(), "little")
 
     def encode(self, values) -> PlainVector:
@@ -245,7 +185,8 @@ class HeBackend:
         pt = eng.alloc_u64((level + 1) * B * self.n)
         eng.call("hk_encode", eng.addr(slots), B, level, self.params.scale(level), eng.addr(pt))
         ct = eng.alloc_u64(2 * (level + 1) * B * self.n)
-        seed = self._seed("enc", next(self._enc_counter))
+        seed = self._seed("enc", next(self._enc_counter) if self._enc_stream == 0
+                          else f"{self._enc_stream}:{next(self._enc_counter)}")
         eng.call("hk_encrypt", eng.addr(pt), level, B, C.c_uint64(seed), eng.addr(ct))
         return self._wrap(ct, level, B, batched)
 
@@ -723,9 +664,9 @@ CkksBackend = HeBackend
 
 
 def make_backend(config: BackendConfig, params: CkksParams | None = None, engine=None,
-                 device: int = 0) -> HeBackend:
+                 device: int = 0, seed: int | None = None, enc_stream: int = 0) -> HeBackend:
     """RNS-CKKS backend on the sm_100a engine (reference factory :293-297)."""
-    return HeBackend(config, params=params, engine=engine, device=device)
+    return HeBackend(config, params=params, engine=engine, device=device, seed=seed, enc_stream=enc_stream)
 
 
 def slotwise(op_kind: str, a: CipherText, b) -> CipherText:

@@ -3,7 +3,7 @@
 has no /root/reference.
 
 Outputs
-  paper_2409_07751_b200/data/composite_sign.json  reference comparator stages
+  tests/golden/composite_sign.json  reference comparator stages (pins the fitter)
   tests/golden/c1.npz      c1 model (built with the reference's classes from the
                            same seeded draws), inputs, reference mirrored and
                            exact outputs, per-layer logical op counts
@@ -31,7 +31,7 @@ from hekan.backend import BackendConfig, CleartextBackend  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
-DATA = os.path.join(ROOT, "paper_2409_07751_b200", "data")
+DATA = HERE
 
 
 def comparator_json():

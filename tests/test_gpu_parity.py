@@ -23,8 +23,8 @@ def _pair(log_n, depth, seed=0, dnum=3):
     from paper_2409_07751_b200.engine import GpuEngine
     p = make_params(log_n, depth, dnum=dnum)
     cfg = BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=seed)
-    g = HeBackend(cfg, p, engine=GpuEngine(p))
-    o = HeBackend(cfg, p, engine=OracleEngine(p))
+    g = HeBackend(cfg, p, engine=GpuEngine(p), seed=seed)
+    o = HeBackend(cfg, p, engine=OracleEngine(p), seed=seed)
     return g, o, p
 
 
@@ -118,8 +118,8 @@ def test_microbench_params_bitexact(gpu_lib):
     from paper_2409_07751_b200.engine import GpuEngine
     p = microbench_params()
     cfg = BackendConfig(slot_count=p.slot_count, depth_budget=p.depth)
-    g = HeBackend(cfg, p, engine=GpuEngine(p))
-    o = HeBackend(cfg, p, engine=OracleEngine(p))
+    g = HeBackend(cfg, p, engine=GpuEngine(p), seed=0)
+    o = HeBackend(cfg, p, engine=OracleEngine(p), seed=0)
     x = np.random.default_rng(3).uniform(-1, 1, p.slot_count)
     ga, oa = g.encrypt(x), o.encrypt(x)
     _same(g, o, g.mul(ga, ga), o.mul(oa, oa), "mul")

@@ -18,7 +18,7 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 def _gpu(p, depth, seed=0):
     from paper_2409_07751_b200.engine import GpuEngine
-    return HeBackend(BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=seed), p,
+    return HeBackend(BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=seed), p, seed=seed,
                      engine=GpuEngine(p))
 
 
@@ -27,7 +27,7 @@ def test_c1_pipeline_bitexact_vs_oracle(gpu_lib):
     _, model, X = configs.workload("c1")
     p = make_params(8, 36)
     bc = BackendConfig(slot_count=p.slot_count, depth_budget=36)
-    g, o = _gpu(p, 36), HeBackend(bc, p, engine=OracleEngine(p))
+    g, o = _gpu(p, 36), HeBackend(bc, p, engine=OracleEngine(p), seed=0)
     cfg = inf.PipelineConfig()
     og, sg = inf.model_forward_he(model, inf.encrypt_input(X[:5], model, g), cfg)
     oo, so = inf.model_forward_he(model, inf.encrypt_input(X[:5], model, o), cfg)
@@ -47,7 +47,7 @@ def test_small_models_bitexact_vs_oracle(gpu_lib):
         depth = inf.plan_model(model, inf.PipelineConfig()).total
         p = make_params(9, depth)
         bc = BackendConfig(slot_count=p.slot_count, depth_budget=depth)
-        g, o = _gpu(p, depth), HeBackend(bc, p, engine=OracleEngine(p))
+        g, o = _gpu(p, depth), HeBackend(bc, p, engine=OracleEngine(p), seed=0)
         X = gz[f"m{idx}_X"]
         og, _ = inf.model_forward_he(model, inf.encrypt_input(X, model, g), inf.PipelineConfig())
         oo, _ = inf.model_forward_he(model, inf.encrypt_input(X, model, o), inf.PipelineConfig())
@@ -98,7 +98,7 @@ def test_c3_pipeline_bitexact_vs_oracle(gpu_lib):
     _, model, X = configs.workload("c3", batch=8)
     p = make_params(9, 54)
     bc = BackendConfig(slot_count=p.slot_count, depth_budget=54)
-    g, o = _gpu(p, 54), HeBackend(bc, p, engine=OracleEngine(p))
+    g, o = _gpu(p, 54), HeBackend(bc, p, engine=OracleEngine(p), seed=0)
     cfg = inf.PipelineConfig()
     og, _ = inf.model_forward_he(model, inf.encrypt_input(X[:2], model, g), cfg)
     oo, _ = inf.model_forward_he(model, inf.encrypt_input(X[:2], model, o), cfg)

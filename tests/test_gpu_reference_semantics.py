@@ -31,7 +31,7 @@ TOL = 1e-6
 @pytest.fixture(scope="module")
 def be(gpu_lib):
     p = make_params(16, 4)
-    return make_backend(BackendConfig(slot_count=p.slot_count, depth_budget=4, rng_seed=3), params=p)
+    return make_backend(BackendConfig(slot_count=p.slot_count, depth_budget=4, rng_seed=3), params=p, seed=3)
 
 
 def _vec(seed, n=S):
@@ -139,7 +139,7 @@ def test_comparator_tie_and_antisymmetry(gpu_lib):
     cs = build_composite_sign(7.0, 2.0 ** -10)
     depth = cs.depth() + 2
     p = make_params(16, depth)
-    be = make_backend(BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=4), params=p)
+    be = make_backend(BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=4), params=p, seed=4)
     xs = np.array([0.5, -0.5, 0.0, 0.25, -0.25, 0.9, -0.9, 0.01])
     ys = np.array([0.0, 0.0, 0.0, -0.25, 0.25, 0.1, -0.1, 0.0])
     ca, cb = be.encrypt(xs), be.encrypt(ys)

@@ -30,7 +30,7 @@ TOL = 1e-4
 
 def oracle_backend(depth, log_n=8, seed=0):
     p = make_params(log_n, depth)
-    return HeBackend(BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=seed), p,
+    return HeBackend(BackendConfig(slot_count=p.slot_count, depth_budget=depth, rng_seed=seed), p, seed=seed,
                      engine=OracleEngine(p))
 
 
@@ -159,7 +159,7 @@ def test_planner_rejects_reference_default_budget():
 def test_bench_compare_rows():
     _, model, X = configs.workload("c1")
     p = make_params(8, 38)
-    fac = lambda bc: HeBackend(bc, p, engine=OracleEngine(p))  # noqa: E731
+    fac = lambda bc: HeBackend(bc, p, engine=OracleEngine(p), seed=0)  # noqa: E731
     bc = BackendConfig(slot_count=p.slot_count, depth_budget=38)
     rows = inf.bench_compare(model, X[:2], [inf.PipelineConfig(path="lazy", backend=bc, label="c1"),
                                            inf.PipelineConfig(path="naive", backend=bc, label="c1")],
