@@ -5,21 +5,30 @@
                   [--config c1|c3|c4|c5] [--batch B] [--chunk C] [--log-n 16]
 
 A step = one encrypted forward pass (`model_forward_he`) of the config's KAN
-over one batch of B ciphertexts (one sample per ciphertext, as
+over one batch of B ciphertexts per GPU (one sample per ciphertext, as
 `encrypt_input`, /root/reference/pkg/src/hekan/inference.py:115-124) on the
-sm_100a RNS-CKKS engine, N = 2^16, depth 36 (L = 37 limbs: the planner total,
-SURVEY §0.3). Inputs are already resident in HBM when the timed region starts;
-each ciphertext batch is 4.7 GB, far larger than the 126 MB L2, so no explicit
-flush is needed between steps. `e2e` times the public API end to end from host
-memory: encrypt_input (host slots -> HBM) + model_forward_he + decrypt (-> host).
+sm_100a RNS-CKKS engine, N = 2^16, L = 36 (the planner total),
+plus the gather of every rank's level-0 outputs to rank 0 (the path's only
+collective; a no-op at N = 1). Inputs are resident in HBM when the
+timed region starts; each ciphertext batch is 4.7 GB, far above the 126 MB
+L2, so no flush is needed between steps. `e2e` times the public API from host
+memory: encrypt_input (pinned host slots -> HBM) + model_forward_he + gather
++ decrypt on rank 0 (-> host).
 
-Multi-GPU (torchrun): every rank runs its own batch (weak scaling, the path
-shards by ciphertext with no data-path collective); the barrier +
-max-over-ranks device time gives the job time; value = total inferences / s.
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run (one rank per GPU, NCCL). The global batch is N x B
+samples in contiguous blocks; every rank uses one key seed (drawn on rank 0,
+broadcast) and encrypts with its global sample offset (weak scaling, no
+data-path collective but the output gather); barrier + max over ranks of the
+device time; value = all ranks' inferences / s.
 
-`--impl reference` times the CPU implementation of the same path: the
-oracle port (oracle/libckks_oracle.so, OpenMP over all host cores) running the
-identical program on a bounded sample (a prefix of one inference's op stream).
+`--impl reference` times the CPU implementation of the same path on the
+host's cores: the oracle port (oracle/libckks_oracle.so, the identical RNS-CKKS
+program, OpenMP over all host threads), each step ONE complete inference of
+one ciphertext, keys generated once before the warm-up. It also reports the
+reference package's own float simulator (`hekan.model_forward_he` on
+`CleartextBackend`, one process per core), which performs no
+cryptography.
 """
 
 from __future__ import annotations
@@ -27,6 +36,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,6 +50,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
+METRIC = "encrypted KAN inferences/sec"
 
 
 def _peaks():
@@ -48,7 +59,19 @@ def _peaks():
             d = json.load(fh)
         return float(d["hbm_gbs"]), "measured"
     except Exception:
-        return FALLBACK_HBM, "fallback"
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def _profile(name: str) -> dict:
+    """Newest committed ncu summary of that name (profiles/r2_*, else r1_*)."""
+    for rnd in ("r2", "r1"):
+        path = os.path.join(ROOT, "profiles", f"{rnd}_{name}.json")
+        if os.path.exists(path):
+            with open(path) as fh:
+                d = json.load(fh)
+            d["_path"] = os.path.relpath(path, ROOT)
+            return d
+    return {}
 
 
 # ---------------------------------------------------------------------------
@@ -106,9 +129,21 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
 # distributed plumbing
 # ---------------------------------------------------------------------------
-def dist_setup(n_gpus: int):
+def spawn_ranks(n: int) -> int:
+    """--gpus N outside torchrun: re-launch this command with one rank per GPU."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -137,51 +172,75 @@ def max_over_ranks(world, value: float, device) -> float:
     return float(t.item())
 
 
+def per_gpu_batch(args, cfg) -> int:
+    # c3's 4096-sample workload would be 220 GiB of fresh ciphertexts: the bench
+    # keeps a resident sample of 64 per GPU (the model is calibrated on all 4096)
+    return args.batch or (cfg.batch if cfg.batch <= 128 else 64)
+
+
+def workload_line(args, cfg, B, chunk, depth, params, world) -> dict:
+    return {"workload": f"{args.config}: KAN {list(cfg.dims)} G={cfg.g} k={cfg.k}, {B} ciphertexts/GPU in "
+                        f"chunks of {chunk}, RNS-CKKS N=2^{args.log_n} L={depth} dnum={params.dnum} "
+                        f"alpha={params.alpha}",
+            "global_batch": B * world, "parallelism": f"dp{world} (ciphertext sharding, output gather to rank 0)",
+            "l2": f"inputs {B * 2 * (depth + 1) * params.n * 8 / 1e9:.1f} GB/GPU >> 126 MB L2 (no flush needed)",
+            "security": (f"log2(PQ) = {params.log_pq:.0f} bits at N=2^{args.log_n}"
+                         + (" (above the ~1772-bit 128-bit-security bound for N=2^16; N=2^17 --log-n 17 "
+                            "is the 128-bit-secure ring for this depth)" if args.log_n == 16 else ""))}
+
+
 # ---------------------------------------------------------------------------
 # product arm
 # ---------------------------------------------------------------------------
 def run_product(args):
     import torch
 
-    from paper_2409_07751_b200 import configs, inference as inf
+    from paper_2409_07751_b200 import configs, distributed as D, inference as inf
     from paper_2409_07751_b200.backend import BackendConfig, make_backend
     from paper_2409_07751_b200.params import kan_params
 
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup()
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
-    cfg, model, inputs = configs.workload(args.config)
-    # c3's 4096-sample workload would be 220 GiB of fresh ciphertexts: the bench
-    # keeps a resident sample of 64 per GPU (the model is still calibrated on all 4096)
-    B = args.batch or (cfg.batch if cfg.batch <= 128 else 64)
-    inputs = inputs[:B] if B <= inputs.shape[0] else np.resize(inputs, (B, inputs.shape[1]))
+    cfg = configs.CONFIGS[args.config]
+    B = per_gpu_batch(args, cfg)
+    n_global = B * world
+    _, model, X_all = configs.workload(args.config, batch=n_global)
     pcfg = inf.PipelineConfig()
     depth = inf.plan_model(model, pcfg).total
     params = kan_params(depth, log_n=args.log_n, dnum=args.dnum)
-    be = make_backend(BackendConfig(slot_count=params.slot_count, depth_budget=depth, rng_seed=rank),
-                      params=params, device=local)
+    seed = D.shared_seed(world, rank, device)   # identical keys on every rank
+    lo, hi = D.block_range(n_global, rank, world)
+    be = make_backend(BackendConfig(slot_count=params.slot_count, depth_budget=depth), params=params,
+                      device=local, seed=seed, sample_offset=lo)
     eng = be.engine
-
+    X = X_all[lo:hi]
     chunk = min(args.chunk or B, B)
-    parts = [inputs[i:i + chunk] for i in range(0, B, chunk)]
-    cts_in = [inf.encrypt_input(x, model, be) for x in parts]
+    cts_in = [inf.encrypt_input(X[i:i + chunk], model, be) for i in range(0, B, chunk)]
 
     def step(cts):
-        outs = []
+        gathered = []
         for ct in cts:
-            o, st = inf.model_forward_he(model, ct, pcfg)
-            outs.append(o)
-        return outs, st
+            out, st = inf.model_forward_he(model, ct, pcfg)
+            gathered.append(D.gather_ciphertexts(be, out, world, rank))
+            del out
+        return gathered, st
 
-    outs, stats = step(cts_in)     # generates Galois keys + plaintext caches
-    dec = np.concatenate([be.decrypt(o) for o in outs])[:, :model.n_out]
+    outs, stats = step(cts_in)     # Galois keys + plaintext caches
+    err, n_checked = None, 0
+    if rank == 0:                  # decrypted values vs the reference (any ring degree)
+        dec = np.concatenate([be.decrypt(o) for o in outs])[:, :model.n_out]
+        gpath = os.path.join(ROOT, "tests", "golden", f"{args.config}.npz")
+        if os.path.exists(gpath):
+            gold = np.load(gpath)["mirrored"]
+            # gathered order: chunk c of rank r holds global samples r*B + c*chunk ...
+            order = np.concatenate([np.arange(r * B + c, r * B + min(c + chunk, B))
+                                    for c in range(0, B, chunk) for r in range(world)])
+            glob = np.empty_like(dec)
+            glob[order] = dec
+            n_checked = min(n_global, gold.shape[0])
+            err = float(np.max(np.abs(glob[:n_checked] - gold[:n_checked])))
     del outs
-    err = None
-    gpath = os.path.join(ROOT, "tests", "golden", f"{args.config}.npz")
-    if os.path.exists(gpath):  # decrypted values: comparable at any ring degree
-        gold = np.load(gpath)["mirrored"]
-        n = min(B, gold.shape[0])
-        err = float(np.max(np.abs(dec[:n] - gold[:n])))
     for _ in range(args.warmup):
         step(cts_in)
     torch.cuda.synchronize(device)
@@ -204,21 +263,21 @@ def run_product(args):
     ms = max_over_ranks(world, ev0.elapsed_time(ev1), device) / args.steps
     clk = clocks.stop() if clocks else None
 
-    # ---- e2e through the public API from host memory (device-resident inputs
-    # freed first; untimed warm-up steps so the allocator pool is steady-state)
+    # ---- e2e through the public API from pinned host memory (device-resident
+    # inputs freed first; one untimed warm-up so the allocator pool is steady)
     del cts_in
-    host_in = torch.from_numpy(np.ascontiguousarray(inputs)).pin_memory()
-    host_np = host_in.numpy()
+    host_np = torch.from_numpy(np.ascontiguousarray(X)).pin_memory().numpy()
 
     def e2e_step():
         for i in range(0, B, chunk):
             ct = inf.encrypt_input(host_np[i:i + chunk], model, be)
-            o, _ = inf.model_forward_he(model, ct, pcfg)
-            be.decrypt(o)
-            del ct, o
+            out, _ = inf.model_forward_he(model, ct, pcfg)
+            full = D.gather_ciphertexts(be, out, world, rank)
+            if rank == 0:
+                be.decrypt(full)
+            del ct, out, full
 
-    for _ in range(min(args.warmup, 1)):
-        e2e_step()
+    e2e_step()
     barrier(world)
     torch.cuda.synchronize(device)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -229,66 +288,55 @@ def run_product(args):
     torch.cuda.synchronize(device)
     e2e_ms = max_over_ranks(world, e0.elapsed_time(e1), device) / max(1, args.steps)
     S = params.slot_count
-    h2d = B * S * 8          # zero-padded slot rows uploaded by encrypt
-    d2h = B * S * 8          # decrypted slot vectors
+    h2d = n_global * S * 8                      # zero-padded slot rows uploaded by encrypt
+    d2h = n_global * S * 8                      # decrypted slot vectors (rank 0)
+    gather_bytes = (world - 1) * B * 2 * params.n * 8   # level-0 outputs moved to rank 0
 
-    # ---- dominant kernels: NTT and key switch, live CUDA-event timing
     torch.cuda.empty_cache()
     roof = kernel_rooflines(be, params, chunk, stream) if rank == 0 else None
-
     if rank != 0:
         return
-    total_inf = B * world
-    value = total_inf / (ms / 1e3)
+    value = n_global / (ms / 1e3)
     hbm, hbm_kind = _peaks()
     line = {
-        "metric": "encrypted KAN inferences/sec",
-        "value": round(value, 4),
-        "unit": "inferences/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": round(ms, 3),
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "u64 (RNS residues mod <=50-bit primes)",
+        "metric": METRIC, "value": round(value, 4), "unit": "inferences/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues mod <=50-bit primes)",
         "data": "synthetic (seeded PCG64, SURVEY §8d)",
-        "config": {"workload": f"{args.config}: KAN {list(cfg.dims)} G={cfg.g} k={cfg.k}, "
-                               f"{B} ciphertexts/GPU in chunks of {chunk}, RNS-CKKS N=2^{args.log_n} L={depth} "
-                               f"dnum={params.dnum} alpha={params.alpha}",
-                   "global_batch": total_inf, "parallelism": f"dp{world} (ciphertext sharding)",
-                   "l2": f"inputs {B * 2 * (depth + 1) * params.n * 8 / 1e9:.1f} GB/GPU >> 126 MB L2 "
-                         "(no flush needed)"},
-        "e2e": {"value": round(total_inf / (e2e_ms / 1e3), 4), "unit": "inferences/s",
+        "config": workload_line(args, cfg, B, chunk, depth, params, world),
+        "e2e": {"value": round(n_global / (e2e_ms / 1e3), 4), "unit": "inferences/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "encrypt_input + model_forward_he + decrypt, host slots in/out"},
+                "gather_bytes_per_step": gather_bytes,
+                "api": "encrypt_input + model_forward_he + gather to rank 0 + decrypt, host slots in/out"},
         "gpu_launches": launches,
         "clocks": clk,
         "max_abs_err_vs_reference_mirrored": err,
+        "err_samples": n_checked,
         "counts_per_inference": stats.to_json()["total"],
     }
     if roof:
-        line["roofline"] = roof["ntt"]
-        line["roofline"]["peak_kind"] = hbm_kind
+        line["roofline"] = dict(roof["ntt"], peak_kind=hbm_kind)
         line["kernels"] = roof
     if not args.no_c2:
         del be, eng
         torch.cuda.empty_cache()
         line["c2_microbench"] = c2_microbench(local)
     if world == 1 and not args.no_cpu_baseline:
-        if args.log_n > 16:
-            line["cpu_baseline"] = {"skipped": "oracle setup at N=2^17 generates every Galois key on the "
-                                               "CPU (hundreds of keys, many minutes); run c1 for the baseline"}
-        else:
-            line["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_baseline(args)
     print(json.dumps(line))
 
 
-def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
-    """CUDA-event timings of the two dominant primitives at c1 shapes."""
-    import ctypes as C
+def _binding(prof: dict) -> dict:
+    keys = ("fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "issue_active_pct", "warps_active_pct")
+    return {k: prof[k] for k in keys if k in prof} | ({"source": prof["_path"]} if prof else {})
 
+
+def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
+    """CUDA-event timings of the two dominant primitives at the bench's launch
+    shapes, against the HBM roofline on SURVEY §8(d)'s algorithmic bytes. Both
+    are compute-bound on this engine (FP64-pipe butterflies, integer-pipe
+    basis conversion), so `bound` names that pipe and `pipe` carries its ncu
+    utilisation; `frac` stays the HBM fraction."""
     import torch
     eng = be.engine
     hbm, _ = _peaks()
@@ -308,26 +356,16 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
     t = ev[0].elapsed_time(ev[1]) / reps / 1e3
     alg = 2.0 * nl * B * N * 8
     ach = alg / t / 1e9
-    traffic, tr = None, {}
-    try:  # dram__bytes_read.sum + dram__bytes_write.sum of the same launch shape (ncu --set full)
-        with open(os.path.join(ROOT, "profiles", "r1_ntt_traffic.json")) as fh:
-            tr = json.load(fh)
-        if tr.get("algorithmic_bytes") == alg:
-            traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
-    except Exception:
-        pass
-    out["ntt"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                  "frac": round(ach / hbm, 4), "traffic": traffic,
-                  "kernel": f"hk_ntt_fwd -> ntt16::fwd_kernel (one 4-CTA cluster per polynomial, FP64-pipe "
+    tr = _profile("ntt_traffic")
+    traffic = (tr["dram_read_bytes"] + tr["dram_write_bytes"]) if tr.get("algorithmic_bytes") == alg else None
+    out["ntt"] = {"bound": "fp64", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                  "frac": round(ach / hbm, 4), "traffic": traffic, "pipe": _binding(tr),
+                  "kernel": f"hk_ntt_fwd -> ntt16::fwd_kernel (4-CTA cluster per polynomial, FP64-pipe "
                             f"butterflies), {nl} limbs x {B} polys",
-                  "algorithmic_bytes": alg, "ms": round(t * 1e3, 3),
-                  "note": f"FP64-issue/latency bound: ncu fp64 pipe {tr.get('fp64_pipe_pct')}%, issue "
-                          f"{tr.get('issue_active_pct')}%; traffic above the algorithmic bytes is the "
-                          f"between-phase buffer partly reaching HBM (profiles/r1_ntt_traffic.json)"}
+                  "algorithmic_bytes": alg, "ms": round(t * 1e3, 3)}
     del buf
-    # key switch via one rotation at the top level (ModUp + IP + ModDown)
-    x = np.zeros((B, params.slot_count))
-    ct = be.encrypt(x)
+    # key switch via one rotation at the top level (ModUp + key IP + ModDown)
+    ct = be.encrypt(np.zeros((B, params.slot_count)))
     be.rotate(ct, 1)
     torch.cuda.synchronize()
     ev[0].record(stream)
@@ -337,23 +375,14 @@ def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
     torch.cuda.synchronize()
     t = ev[0].elapsed_time(ev[1]) / reps / 1e3
     l = params.depth
-    alpha, n_p = params.alpha, len(params.p)
-    nd = l // alpha + 1
-    alg = B * 4 * (l + 1) * N * 8 + 2 * nd * (l + 1 + n_p) * N * 8
+    nd = l // params.alpha + 1
+    alg = B * 4 * (l + 1) * N * 8 + 2 * nd * (l + 1 + len(params.p)) * N * 8
     ach = alg / t / 1e9
-    ks_traffic = None
-    try:  # summed dram bytes of one rotation's launches at this shape (tools/prof_rot.py)
-        with open(os.path.join(ROOT, "profiles", "r1_rotate_traffic.json")) as fh:
-            rt = json.load(fh)
-        if rt.get("algorithmic_bytes") == alg:
-            ks_traffic = rt["dram_read_bytes"] + rt["dram_write_bytes"]
-    except Exception:
-        pass
-    out["keyswitch"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                        "frac": round(ach / hbm, 4), "traffic": ks_traffic,
-                        "note": "compute bound: ~250 limb-NTTs + ~2,400 conversion MACs per coefficient; "
-                                "traffic counts the extended-basis intermediates (profiles/r1_rotate_traffic.json)",
-                        "kernel": f"hk_rotate (ModUp+KeyIP+ModDown) level {l}, {B} cts",
+    rt = _profile("rotate_traffic")
+    ks_traffic = (rt["dram_read_bytes"] + rt["dram_write_bytes"]) if rt.get("algorithmic_bytes") == alg else None
+    out["keyswitch"] = {"bound": "int+fp64", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(ach / hbm, 4), "traffic": ks_traffic, "pipe": _binding(rt),
+                        "kernel": f"hk_rotate (ModUp + key IP + ModDown) level {l}, {B} cts",
                         "algorithmic_bytes": alg, "ms": round(t * 1e3, 3)}
     return out
 
@@ -366,6 +395,7 @@ def c2_microbench(device: int, n_ct: int = 256, reps: int = 3) -> dict:
     import ctypes as C
 
     import torch
+    from paper_2409_07751_b200 import _abi
     from paper_2409_07751_b200.backend import galois_element
     from paper_2409_07751_b200.engine import GpuEngine
     from paper_2409_07751_b200.params import microbench_params
@@ -379,10 +409,10 @@ def c2_microbench(device: int, n_ct: int = 256, reps: int = 3) -> dict:
     ct = eng.alloc_u64(2 * n * n_ct * N).view(2, n, n_ct * N)
     for i, q in enumerate(p.q):  # uniform residues in [0, q_i)
         ct[:, i].random_(0, int(q))
-    eng.call("hk_keygen", C.c_uint64(7))
+    eng.call("hk_keygen", _abi.seed_words(os.urandom(32)))
     steps = [s * (1 << j) for j in range(15) for s in (1, -1)]
     gal = [galois_element(t, p.slot_count) for t in steps]
-    eng.call("hk_add_galois_keys", C.c_uint64(8), eng.u32_array(gal), len(gal))
+    eng.call("hk_add_galois_keys", _abi.seed_words(os.urandom(32)), eng.u32_array(gal), len(gal))
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 
     def timed(fn, k=reps):
@@ -395,9 +425,9 @@ def c2_microbench(device: int, n_ct: int = 256, reps: int = 3) -> dict:
         torch.cuda.synchronize(device)
         return ev[0].elapsed_time(ev[1]) / k / 1e3
 
-    def entry(alg, t, what):
+    def entry(alg, t, what, bound="int+fp64"):
         ach = alg / t / 1e9
-        return {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+        return {"bound": bound, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
                 "ms": round(t * 1e3, 3), "algorithmic_bytes": alg, "kernel": what}
 
     out = {"workload": f"c2: {n_ct} ciphertexts x 2 polys x {n} limbs (~50-bit), N=2^16, dnum=3, alpha={alpha}, "
@@ -406,9 +436,9 @@ def c2_microbench(device: int, n_ct: int = 256, reps: int = 3) -> dict:
     half = n * n_ct * N * 8
     ntt_b = 2.0 * n_ct * 2 * n * N * 8
     t = timed(lambda: [eng.call("hk_ntt_fwd", base + q * half, 0, n, n_ct) for q in (0, 1)])
-    out["ntt"] = entry(ntt_b, t, "hk_ntt_fwd, both polynomials")
+    out["ntt"] = entry(ntt_b, t, "hk_ntt_fwd, both polynomials", "fp64")
     t = timed(lambda: [eng.call("hk_ntt_inv", base + q * half, 0, n, n_ct) for q in (0, 1)])
-    out["intt"] = entry(ntt_b, t, "hk_ntt_inv, both polynomials")
+    out["intt"] = entry(ntt_b, t, "hk_ntt_inv, both polynomials", "fp64")
     dst = eng.alloc_u64(2 * n * n_ct * N)
     key_b = 2 * p.dnum * (n + alpha) * N * 8
     t = timed(lambda: eng.call("hk_mul", base, l, base, l, eng.addr(dst), n_ct))
@@ -424,227 +454,132 @@ def c2_microbench(device: int, n_ct: int = 256, reps: int = 3) -> dict:
     return out
 
 
+
+
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port on host cores
+# CPU legs: the oracle port (like-for-like HE) and the reference's float simulator
 # ---------------------------------------------------------------------------
-def cpu_baseline(args, budget_s: float = 20.0) -> dict:
-    """Oracle port, all host threads, one c1 sample at full N: runs the op
-    stream of one inference until `budget_s` is spent, then scales by the
-    fraction of the (pre-measured on GPU) program completed, counted in
-    logical ops weighted by level (limb count)."""
-    from oracle.engine import OracleEngine
-    from paper_2409_07751_b200 import configs, inference as inf
-    from paper_2409_07751_b200.backend import BackendConfig, HeBackend
-    from paper_2409_07751_b200.params import kan_params
-
-    cores = len(os.sched_getaffinity(0))
-    cfg, model, inputs = configs.workload(args.config, batch=1)
-    pcfg = inf.PipelineConfig()
-    depth = inf.plan_model(model, pcfg).total
-    params = kan_params(depth, log_n=args.log_n, dnum=args.dnum)
-    t_setup = time.perf_counter()
-    be = BudgetBackend(BackendConfig(slot_count=params.slot_count, depth_budget=depth), params,
-                       engine=OracleEngine(params))
-    be.prepare_keys_for(model, pcfg)
-    setup = time.perf_counter() - t_setup
-    ct = inf.encrypt_input(inputs, model, be)
-    be.start(budget_s)
-    t0 = time.perf_counter()
-    try:
-        inf.model_forward_he(model, ct, pcfg)
-        done = True
-    except _Budget:
-        done = False
-    el = time.perf_counter() - t0
-    frac = 1.0 if done else be.weight_done / max(be.total_weight(model, pcfg), 1e-9)
-    inf_per_s = frac / el if el > 0 else 0.0
-    return {"value": round(inf_per_s, 6), "unit": "inferences/s", "cores": cores, "kind": "port",
-            "sample": (f"oracle/libckks_oracle.so (OpenMP {cores} threads), {args.config} one ciphertext, "
-                       f"N=2^{args.log_n}; ran {'the full inference' if done else f'{frac:.1%} of one inference (level-weighted op prefix)'} "
-                       f"in {el:.1f} s; keygen/setup {setup:.1f} s untimed")}
+def _cores() -> int:
+    return len(os.sched_getaffinity(0))
 
 
-class _Budget(Exception):
-    pass
+class OracleInference:
+    """One complete inference of one ciphertext on the oracle port (the same
+    RNS-CKKS program, OpenMP over all host threads). Keys and plaintext caches
+    are made once, by an untimed first inference, before any timed step."""
+
+    def __init__(self, args):
+        from oracle.engine import OracleEngine
+        from paper_2409_07751_b200 import configs, inference as inf
+        from paper_2409_07751_b200.backend import BackendConfig, HeBackend
+        from paper_2409_07751_b200.params import kan_params
+        self.inf = inf
+        _, self.model, X = configs.workload(args.config, batch=1)
+        self.pcfg = inf.PipelineConfig()
+        depth = inf.plan_model(self.model, self.pcfg).total
+        self.params = kan_params(depth, log_n=args.log_n, dnum=args.dnum)
+        t = time.perf_counter()
+        self.be = HeBackend(BackendConfig(slot_count=self.params.slot_count, depth_budget=depth), self.params,
+                            engine=OracleEngine(self.params))
+        self.x = X
+        self.run()                       # keys + caches (untimed)
+        self.setup_s = time.perf_counter() - t
+
+    def run(self) -> float:
+        t = time.perf_counter()
+        ct = self.inf.encrypt_input(self.x, self.model, self.be)
+        out, _ = self.inf.model_forward_he(self.model, ct, self.pcfg)
+        self.be.decrypt(out)
+        return time.perf_counter() - t
 
 
-from paper_2409_07751_b200.backend import HeBackend  # noqa: E402  (torch-free import)
+def cpu_baseline(args) -> dict:
+    """Oracle port, all host threads: one measured c1 inference (after the
+    untimed key-generation inference)."""
+    o = OracleInference(args)
+    el = o.run()
+    cores = _cores()
+    return {"value": round(1.0 / el, 6), "unit": "inferences/s", "cores": cores, "kind": "port",
+            "sample": (f"oracle/libckks_oracle.so (C, Barrett/Shoup, OpenMP {cores} threads): one complete "
+                       f"{args.config} inference of one ciphertext at N=2^{args.log_n} "
+                       f"(encrypt + model_forward_he + decrypt) in {el:.1f} s; keys and plaintext caches "
+                       f"made by an untimed first inference ({o.setup_s:.1f} s)")}
 
 
-class BudgetBackend(HeBackend):
-    """HeBackend with an op-weight meter and a wall-clock budget."""
-
-    weight_done = 0.0
-    _deadline = None
-
-    def start(self, budget_s):
-        self.weight_done = 0.0
-        self._deadline = time.perf_counter() + budget_s
-
-    def _tick(self, w):
-        self.weight_done += w
-        if self._deadline is not None and time.perf_counter() > self._deadline:
-            raise _Budget()
-
-    @staticmethod
-    def op_weight(kind, level):
-        return {"mul_ct": 12.0, "rot": 10.0, "mul_pt": 2.0, "add": 0.3}[kind] * (level + 1)
-
-    def slotwise(self, op_kind, a, b):
-        kind = "mul_ct" if op_kind == "mul_ct" else ("mul_pt" if op_kind == "mul_pt" else "add")
-        out = super().slotwise(op_kind, a, b)
-        self._tick(self.op_weight(kind, a.level))
-        return out
-
-    def rotate(self, a, t):
-        out = super().rotate(a, t)
-        if t:
-            self._tick(self.op_weight("rot", a.level))
-        return out
-
-    def rotate_many(self, a, steps):
-        out = super().rotate_many(a, steps)
-        self._tick(sum(self.op_weight("rot", a.level) for t in steps if t))
-        return out
-
-    def mac_plain(self, babies, plains):
-        out = super().mac_plain(babies, plains)
-        self._tick(len(babies) * self.op_weight("mul_pt", babies[0].level))
-        return out
-
-    def mul_lin(self, a, b, x, k):
-        out = super().mul_lin(a, b, x, k)
-        self._tick(self.op_weight("mul_ct", min(a.level, b.level)))
-        return out
-
-    def mul_affine(self, a, b, mult, c):
-        out = super().mul_affine(a, b, mult, c)
-        self._tick(self.op_weight("mul_ct", min(a.level, b.level)))
-        return out
-
-    def mul2(self, a, b, a2, b2):
-        out = super().mul2(a, b, a2, b2)
-        self._tick(self.op_weight("mul_ct", min(a.level, b.level, a2.level, b2.level)))
-        return out
-
-    def prepare_keys_for(self, model, pcfg):
-        """Generate every Galois key the program needs (untimed)."""
-        from paper_2409_07751_b200 import inference as inf
-        rec = _Recorder(self.config, self.params)
-        inf.model_forward_he(model, rec.encrypt(np.zeros(model.n_in)), pcfg)
-        self.ensure_rotation_keys(sorted(rec.steps))
-        self._program = rec.ops
-
-    def total_weight(self, model, pcfg):
-        return sum(self.op_weight(k, lvl) * n for k, lvl, n in self._program)
+def _sim_worker(cfg_name, seconds, start_evt, q):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from paper_2409_07751_b200 import configs
+    from paper_2409_07751_b200._ref import hekan
+    hb, hi = hekan.backend, hekan.inference
+    _, model, X = configs.workload(cfg_name)
+    pcfg = hi.PipelineConfig()
+    depth = hi.plan_model(model, pcfg).total
+    S = 2 ** 16 if cfg_name == "c5" else 2 ** 15
+    be = hb.CleartextBackend(hb.BackendConfig(slot_count=S, depth_budget=depth))
+    hi.model_forward_he(model, hi.encrypt_input(X[0], model, be), pcfg)  # comparator fit, caches
+    start_evt.wait()
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        hi.model_forward_he(model, hi.encrypt_input(X[n % len(X)], model, be), pcfg)
+        n += 1
+    q.put((n, time.perf_counter() - t0))
 
 
-class _Recorder:
-    """Level-accurate dry run of the op program (no arithmetic)."""
-
-    def __init__(self, config, params):
-        from paper_2409_07751_b200.backend import OpCounter
-        self.config = config
-        self.params = params
-        self.counter = OpCounter()
-        self.steps = set()
-        self.ops = []
-
-    class Ct:
-        def __init__(self, be, level):
-            self.backend, self.level, self.batch, self.batched = be, level, 1, False
-
-        @property
-        def slots(self):
-            return np.zeros(self.backend.config.slot_count)
-
-    def encrypt(self, values, level=None):
-        return self.Ct(self, self.config.depth_budget if level is None else level)
-
-    def _lvl(self, a, b):
-        return min(a.level, b.level) if isinstance(b, self.Ct) else a.level
-
-    def add(self, a, b):
-        self.ops.append(("add", self._lvl(a, b), 1))
-        return self.Ct(self, self._lvl(a, b))
-
-    sub = add
-
-    def mul(self, a, b):
-        lvl = self._lvl(a, b)
-        self.ops.append(("mul_ct" if isinstance(b, self.Ct) else "mul_pt", lvl, 1))
-        return self.Ct(self, lvl - 1)
-
-    def rotate(self, a, t):
-        if t:
-            self.steps.add(t)
-            self.ops.append(("rot", a.level, 1))
-        return a if not t else self.Ct(self, a.level)
-
-    def rotate_many(self, a, steps):
-        return [self.rotate(a, t) for t in steps]
-
-    def mac_plain(self, babies, plains):
-        self.ops.append(("mul_pt", babies[0].level, len(babies)))
-        return self.Ct(self, babies[0].level - 1)
-
-    def mul_lin(self, a, b, x, k):
-        lvl = min(a.level, b.level)
-        self.ops.append(("mul_ct", lvl, 1))
-        return self.Ct(self, lvl - 1)
-
-    def mul_affine(self, a, b, mult, c):
-        lvl = min(a.level, b.level)
-        self.ops.append(("mul_ct", lvl, 1))
-        return self.Ct(self, lvl - 1)
-
-    def mul2(self, a, b, a2, b2):
-        lvl = min(a.level, b.level, a2.level, b2.level)
-        self.ops.append(("mul_ct", lvl, 1))
-        return self.Ct(self, lvl - 1)
-
-
-def reference_config(args):
-    """The product arm's workload description (same model, batch, chunking and ring),
-    so the driver compares like with like; the CPU measures a bounded sample of it."""
-    from paper_2409_07751_b200 import configs, inference as inf
-    from paper_2409_07751_b200.params import kan_params
-    cfg = configs.CONFIGS[args.config]
-    B = args.batch or (cfg.batch if cfg.batch <= 128 else 64)
-    chunk = min(args.chunk or B, B)
-    _, model, _ = configs.workload(args.config)
-    depth = inf.plan_model(model, inf.PipelineConfig()).total
-    params = kan_params(depth, log_n=args.log_n, dnum=args.dnum)
-    return {"workload": f"{args.config}: KAN {list(cfg.dims)} G={cfg.g} k={cfg.k}, "
-                        f"{B} ciphertexts/GPU in chunks of {chunk}, RNS-CKKS N=2^{args.log_n} L={depth} "
-                        f"dnum={params.dnum} alpha={params.alpha}",
-            "global_batch": B, "parallelism": "cpu (OpenMP, all host cores, one ciphertext at a time)",
-            "sample": "bounded prefix of one inference per step (cpu_baseline.sample)"}
+def float_simulator(args, seconds: float = 10.0) -> dict:
+    """the reference's own path, `hekan.model_forward_he` on
+    `CleartextBackend` (a float64 slot simulator, no cryptography), one process
+    per host core over independent inferences, OMP_NUM_THREADS=1."""
+    import multiprocessing as mp
+    cores = _cores()
+    ctx = mp.get_context("spawn")
+    q, start = ctx.Queue(), ctx.Event()
+    procs = [ctx.Process(target=_sim_worker, args=(args.config, seconds, start, q)) for _ in range(cores)]
+    for p in procs:
+        p.start()
+    time.sleep(1.0)
+    start.set()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    rate = sum(n / t for n, t in res)
+    return {"value": round(rate, 3), "unit": "inferences/s", "cores": cores, "kind": "reference float simulator",
+            "sample": f"hekan.model_forward_he on CleartextBackend (float64 slots, NO cryptography), "
+                      f"{args.config}, composite comparator, {cores} processes x {seconds:.0f} s, "
+                      f"{sum(n for n, _ in res)} inferences"}
 
 
 def run_reference(args):
-    """--impl reference: the CPU path (oracle port) on host cores, rank 0 only."""
+    """--impl reference: the CPU path on the host's cores, rank 0 only. Each step
+    is one complete inference of one ciphertext on the oracle port."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    vals = []
-    base = None
-    for i in range(args.warmup + args.steps):
-        r = cpu_baseline(args, budget_s=args.cpu_budget)
-        if i >= args.warmup:
-            vals.append(r["value"])
-            base = r
-    v = statistics.median(vals) if vals else 0.0
-    line = {"metric": "encrypted KAN inferences/sec", "value": v, "unit": "inferences/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 / v, 3) if v else None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)",
+    from paper_2409_07751_b200 import configs, inference as inf
+    o = OracleInference(args)
+    for _ in range(args.warmup):
+        o.run()
+    times = [o.run() for _ in range(args.steps)]
+    total = sum(times)
+    v = args.steps / total
+    cores = _cores()
+    cfg = configs.CONFIGS[args.config]
+    B = per_gpu_batch(args, cfg)
+    line = {"metric": METRIC, "value": round(v, 6), "unit": "inferences/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)",
             "data": "synthetic (seeded PCG64, SURVEY §8d)", "impl": "reference",
-            "config": reference_config(args),
-            "cpu_baseline": dict(base or {}, value=v),
-            "e2e": {"value": v, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "config": dict(workload_line(args, cfg, B, min(args.chunk or B, B),
+                                         o.params.depth, o.params, world),
+                           parallelism=f"cpu (OpenMP {cores} threads), one ciphertext per step"),
+            "cpu_baseline": {"value": round(v, 6), "unit": "inferences/s", "cores": cores, "kind": "port",
+                             "sample": f"oracle/libckks_oracle.so, each step one complete {args.config} inference "
+                                       f"of one ciphertext (encrypt + model_forward_he + decrypt); step times "
+                                       f"{min(times):.2f}-{max(times):.2f} s; keys made once before the warm-up "
+                                       f"({o.setup_s:.1f} s)"},
+            "e2e": {"value": round(v, 6), "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
+    if not args.no_float_sim:
+        line["float_simulator"] = float_simulator(args)
     print(json.dumps(line))
 
 
@@ -656,26 +591,27 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("product", "reference"), default="product")
     ap.add_argument("--config", default="c1")
-    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=0, help="ciphertexts per GPU")
     ap.add_argument("--dnum", type=int, default=3, help="key-switching digits over the full chain")
     ap.add_argument("--chunk", type=int, default=None,
-                    help="ciphertexts per batched launch (default 32; 8 for c5 at N=2^17)")
+                    help="ciphertexts per batched launch (default: the whole batch; 32 for c4, 8 for c5)")
     ap.add_argument("--log-n", type=int, default=None,
                     help="ring degree (default 16; 17 for c5, whose 33792 packed slots need S=2^16)")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-float-sim", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the config-2 primitive microbench")
     args = ap.parse_args()
     if args.log_n is None:
         args.log_n = 17 if args.config == "c5" else 16
     if args.chunk is None:
-        # ciphertexts per launch (the whole resident batch where it fits in HBM): c1 and
-        # c3 run their batch in one chunk; c4 / c5 hold 80 / 157 hoisted BSGS baby
-        # steps at once, which bounds them to 32 at N = 2^16 and 8 at N = 2^17
+        # c1 and c3 run their whole batch per launch; c4 / c5 hold 80 / 157 hoisted
+        # BSGS baby steps at once, which bounds them to 32 at N = 2^16 and 8 at N = 2^17
         if args.log_n > 16:
             args.chunk = 8 if args.config == "c5" else 32
         else:
             args.chunk = {"c4": 32, "c5": 8}.get(args.config, 128)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -71,15 +71,19 @@ int hk_set_stream(hk_ctx *ctx, void *cuda_stream);   /* oracle: no-op */
 int hk_sync(hk_ctx *ctx);
 
 /* ---- keys (client side; replaces nothing — the reference has no keys).
- * Secret key, relinearisation key and one Galois key per element, all from
- * the counter-based stream seeded by `seed` (identical in oracle and GPU). */
-int hk_keygen(hk_ctx *ctx, uint64_t seed);
-int hk_add_galois_keys(hk_ctx *ctx, uint64_t seed, const uint32_t *galois_elts, int32_t n);
+ * Randomness: ChaCha20 (20 rounds, 64-bit block counter + 64-bit stream as the
+ * nonce) keyed by a 256-bit `seed` (4 words, HOST memory); 64-bit output word
+ * c of stream s is words 2(c mod 8), 2(c mod 8)+1 of block c / 8. Identical in
+ * oracle and GPU. Secret key, relinearisation key and one Galois key per element
+ * come from one seed; callers draw it from the OS CSPRNG (the Python backend
+ * does unless a test seeds it explicitly). */
+int hk_keygen(hk_ctx *ctx, const uint64_t seed[4]);
+int hk_add_galois_keys(hk_ctx *ctx, const uint64_t seed[4], const uint32_t *galois_elts, int32_t n);
 /* Galois keys usable up to ciphertext `level` only: digits 0..level/alpha and the
  * rows of q_0..q_level plus the special primes (the same values as the full key's
  * rows, so results are identical). A key already present at a lower level is
  * regenerated at `level`; one at a higher level is kept. The oracle keeps full keys. */
-int hk_add_galois_keys_level(hk_ctx *ctx, uint64_t seed, const uint32_t *galois_elts, int32_t n,
+int hk_add_galois_keys_level(hk_ctx *ctx, const uint64_t seed[4], const uint32_t *galois_elts, int32_t n,
                              int32_t level);
 /* 0 if absent, else 1 + the highest ciphertext level the key serves. */
 int hk_has_galois_key(const hk_ctx *ctx, uint32_t galois_elt);
@@ -112,9 +116,12 @@ int hk_encode_diagonals(hk_ctx *ctx, const double *W, int32_t n_o, int32_t n_in,
 int hk_encode_const(hk_ctx *ctx, double c, int32_t level, double scale, uint64_t *res);
 
 /* ---- encrypt / decrypt (HeBackend.encrypt / decrypt, backend.py:160-170).
- * Secret-key RLWE encryption, randomness from (seed, batch index, limb, coeff). */
+ * Secret-key RLWE encryption; randomness from (seed, sample, limb, coeff) with
+ * sample = first_sample + batch index, so a batch sharded over ranks (rank r
+ * passing its first global sample index) encrypts exactly as the whole batch
+ * would in one call, and no (a, e) pair repeats across ranks. */
 int hk_encrypt(hk_ctx *ctx, const uint64_t *pt, int32_t level, int32_t batch,
-               uint64_t seed, uint64_t *ct);
+               const uint64_t seed[4], uint64_t first_sample, uint64_t *ct);
 int hk_decrypt(hk_ctx *ctx, const uint64_t *ct, int32_t level, int32_t batch,
                double scale, double *slots);
 

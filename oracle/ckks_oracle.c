@@ -102,14 +102,43 @@ static inline uint32_t brv(uint32_t x, int bits) {
 /* ------------------------------------------------------------------------ */
 /* counter-based randomness (identical formula in the CUDA product)          */
 /* ------------------------------------------------------------------------ */
-static inline uint64_t mix64(uint64_t z) {
-    z += 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
+/* ChaCha20 block function (RFC 8439 quarter rounds; 64-bit counter in words
+ * 12-13, the 64-bit stream id as the nonce in words 14-15) keyed by 256 bits. */
+typedef struct { uint64_t w[4]; } seed_t;
+static inline uint32_t rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+#define QR(a, b, c, d) \
+    a += b; d ^= a; d = rotl32(d, 16); c += d; b ^= c; b = rotl32(b, 12); \
+    a += b; d ^= a; d = rotl32(d, 8);  c += d; b ^= c; b = rotl32(b, 7);
+static void chacha20_block(const seed_t *key, uint64_t block, uint64_t stream, uint32_t out[16]) {
+    uint32_t s[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u};
+    for (int i = 0; i < 4; ++i) { s[4 + 2 * i] = (uint32_t)key->w[i]; s[5 + 2 * i] = (uint32_t)(key->w[i] >> 32); }
+    s[12] = (uint32_t)block; s[13] = (uint32_t)(block >> 32);
+    s[14] = (uint32_t)stream; s[15] = (uint32_t)(stream >> 32);
+    uint32_t x[16];
+    memcpy(x, s, sizeof x);
+    for (int r = 0; r < 10; ++r) {
+        QR(x[0], x[4], x[8], x[12]) QR(x[1], x[5], x[9], x[13]) QR(x[2], x[6], x[10], x[14]) QR(x[3], x[7], x[11], x[15])
+        QR(x[0], x[5], x[10], x[15]) QR(x[1], x[6], x[11], x[12]) QR(x[2], x[7], x[8], x[13]) QR(x[3], x[4], x[9], x[14])
+    }
+    for (int i = 0; i < 16; ++i) out[i] = x[i] + s[i];
 }
-static inline uint64_t rng64(uint64_t seed, uint64_t stream, uint64_t ctr) {
-    return mix64(mix64(seed ^ mix64(stream * 0xD1B54A32D192ED03ull)) + ctr);
+/* 64-bit word `ctr` of stream `stream` */
+static inline uint64_t rng64(const seed_t *key, uint64_t stream, uint64_t ctr) {
+    uint32_t o[16];
+    chacha20_block(key, ctr >> 3, stream, o);
+    const int j = (int)(ctr & 7);
+    return (uint64_t)o[2 * j] | ((uint64_t)o[2 * j + 1] << 32);
+}
+/* out[i] = rng64(key, stream, ctr0 + i), i < n: whole blocks when aligned */
+static void rng_fill(const seed_t *key, uint64_t stream, uint64_t ctr0, int n, uint64_t *out) {
+    int i = 0;
+    for (; i < n && ((ctr0 + (uint64_t)i) & 7); ++i) out[i] = rng64(key, stream, ctr0 + (uint64_t)i);
+    for (; i + 8 <= n; i += 8) {
+        uint32_t o[16];
+        chacha20_block(key, (ctr0 + (uint64_t)i) >> 3, stream, o);
+        for (int j = 0; j < 8; ++j) out[i + j] = (uint64_t)o[2 * j] | ((uint64_t)o[2 * j + 1] << 32);
+    }
+    for (; i < n; ++i) out[i] = rng64(key, stream, ctr0 + (uint64_t)i);
 }
 /* centered binomial, eta = 21: variance 10.5 (sigma 3.24) */
 static inline int64_t cbd21(uint64_t x) {
@@ -167,7 +196,7 @@ int hk_sync(hk_ctx *c) { (void)c; return HK_OK; }
 
 int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     (void)device;
-    if (!pr || !out || pr->log_n < 2 || pr->log_n > 17 || pr->n_q < 1 || pr->n_p < 1 || pr->dnum < 1 || pr->dnum > 8)
+    if (!pr || !out || pr->log_n < 3 || pr->log_n > 17 || pr->n_q < 1 || pr->n_p < 1 || pr->dnum < 1 || pr->dnum > 8)
         return HK_E_ARG;
     hk_ctx *c = (hk_ctx *)calloc(1, sizeof *c);
     c->log_n = pr->log_n;
@@ -468,14 +497,15 @@ static inline double crt_center(const hk_ctx *c, uint64_t x0, uint64_t x1, int n
 /* ------------------------------------------------------------------------ */
 /* keys                                                                       */
 /* ------------------------------------------------------------------------ */
-static void sample_uniform_ntt(const hk_ctx *c, uint64_t seed, uint64_t stream, uint64_t ctr0,
+static void sample_uniform_ntt(const hk_ctx *c, const seed_t *seed, uint64_t stream, uint64_t ctr0,
                                int m, uint64_t *dst) {
     const uint64_t q = c->mod[m];
-    for (int k = 0; k < c->n; ++k) dst[k] = rng64(seed, stream, ctr0 + (uint64_t)k) % q;
+    rng_fill(seed, stream, ctr0, c->n, dst);
+    for (int k = 0; k < c->n; ++k) dst[k] %= q;
 }
 
 /* key-switching key for target s' (NTT over all n_mod limbs), digits over q */
-static void make_ks_key(const hk_ctx *c, uint64_t seed, uint64_t stream_tag, const uint64_t *sprime,
+static void make_ks_key(const hk_ctx *c, const seed_t *seed, uint64_t stream_tag, const uint64_t *sprime,
                         uint64_t *key) {
     const int N = c->n, nm = c->n_mod;
     uint64_t P_mod[64];
@@ -489,8 +519,8 @@ static void make_ks_key(const hk_ctx *c, uint64_t seed, uint64_t stream_tag, con
         uint64_t *bj = key + ((size_t)j * 2 + 0) * nm * N;
         uint64_t *aj = key + ((size_t)j * 2 + 1) * nm * N;
         int64_t *e = malloc(sizeof(int64_t) * N);
-        for (int k = 0; k < N; ++k)
-            e[k] = cbd21(rng64(seed, ST_KEY_E + stream_tag * 64 + j, (uint64_t)k));
+        rng_fill(seed, ST_KEY_E + stream_tag * 64 + j, 0, N, (uint64_t *)e);
+        for (int k = 0; k < N; ++k) e[k] = cbd21((uint64_t)e[k]);
         #pragma omp parallel for schedule(static)
         for (int m = 0; m < nm; ++m) {
             const uint64_t q = c->mod[m];
@@ -528,12 +558,14 @@ uint64_t hk_key_words(const hk_ctx *c, int32_t which) {
     return (uint64_t)c->n_digits * 2 * nm * N;
 }
 
-int hk_keygen(hk_ctx *c, uint64_t seed) {
+int hk_keygen(hk_ctx *c, const uint64_t seed_words[4]) {
+    const seed_t sd = {{seed_words[0], seed_words[1], seed_words[2], seed_words[3]}}, *seed = &sd;
     const int N = c->n, nm = c->n_mod;
     free(c->sk); free(c->relin);
     c->sk = malloc(sizeof(uint64_t) * (size_t)nm * N);
     int64_t *s = malloc(sizeof(int64_t) * N);
-    for (int k = 0; k < N; ++k) s[k] = ternary(rng64(seed, ST_SECRET, (uint64_t)k));
+    rng_fill(seed, ST_SECRET, 0, N, (uint64_t *)s);
+    for (int k = 0; k < N; ++k) s[k] = ternary((uint64_t)s[k]);
     for (int m = 0; m < nm; ++m) {
         uint64_t *dst = c->sk + (size_t)m * N;
         for (int k = 0; k < N; ++k) dst[k] = smod(s[k], c->mod[m]);
@@ -570,7 +602,8 @@ static const uint64_t *find_gal(const hk_ctx *c, uint32_t g) {
     return NULL;
 }
 
-int hk_add_galois_keys(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n) {
+int hk_add_galois_keys(hk_ctx *c, const uint64_t seed_words[4], const uint32_t *gs, int32_t n) {
+    const seed_t sd = {{seed_words[0], seed_words[1], seed_words[2], seed_words[3]}}, *seed = &sd;
     if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
     const int N = c->n, nm = c->n_mod;
     const uint32_t M = 2u * (uint32_t)N;
@@ -593,7 +626,7 @@ int hk_add_galois_keys(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n) 
 
 /* Level-truncated keys on the GPU hold a subset of the full key's rows; the
  * oracle keeps full keys, so key-switching results are identical. */
-int hk_add_galois_keys_level(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n, int32_t level) {
+int hk_add_galois_keys_level(hk_ctx *c, const uint64_t seed[4], const uint32_t *gs, int32_t n, int32_t level) {
     if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
     if (level < 0 || level >= c->n_q) return fail(c, HK_E_ARG, "galois key level %d out of range", level);
     return hk_add_galois_keys(c, seed, gs, n);
@@ -610,7 +643,9 @@ int hk_export_key(hk_ctx *c, int32_t which, uint32_t g, uint64_t *out) {
 /* ------------------------------------------------------------------------ */
 /* encrypt / decrypt                                                          */
 /* ------------------------------------------------------------------------ */
-int hk_encrypt(hk_ctx *c, const uint64_t *pt, int32_t level, int32_t B, uint64_t seed, uint64_t *ct) {
+int hk_encrypt(hk_ctx *c, const uint64_t *pt, int32_t level, int32_t B, const uint64_t seed_words[4],
+               uint64_t first, uint64_t *ct) {
+    const seed_t sd = {{seed_words[0], seed_words[1], seed_words[2], seed_words[3]}}, *seed = &sd;
     if (!c->have_keys) return fail(c, HK_E_NOKEY, "keygen first");
     if (level < 0 || level >= c->n_q) return fail(c, HK_E_ARG, "encrypt: level out of range");
     const int N = c->n, nl = level + 1;
@@ -620,11 +655,12 @@ int hk_encrypt(hk_ctx *c, const uint64_t *pt, int32_t level, int32_t B, uint64_t
     for (int b = 0; b < B; ++b) {
         int64_t *e = malloc(sizeof(int64_t) * N);
         uint64_t *tmp = malloc(sizeof(uint64_t) * N);
-        for (int k = 0; k < N; ++k) e[k] = cbd21(rng64(seed, ST_ENC_E, (uint64_t)b * N + k));
+        rng_fill(seed, ST_ENC_E, (first + (uint64_t)b) * N, N, (uint64_t *)e);
+        for (int k = 0; k < N; ++k) e[k] = cbd21((uint64_t)e[k]);
         for (int l = 0; l < nl; ++l) {
             const uint64_t q = c->mod[l];
             const size_t o = ((size_t)l * B + b) * N;
-            sample_uniform_ntt(c, seed, ST_ENC_A, ((uint64_t)b * nl + l) * N, l, c1 + o);
+            sample_uniform_ntt(c, seed, ST_ENC_A, ((first + (uint64_t)b) * nl + l) * N, l, c1 + o);
             for (int k = 0; k < N; ++k) tmp[k] = smod(e[k], q);
             ntt_fwd_1(c, tmp, l);
             const uint64_t *s = c->sk + (size_t)l * N;

@@ -30,9 +30,9 @@ SIGNATURES = {
     "hk_last_error": (C.c_char_p, [vp]),
     "hk_set_stream": (C.c_int, [vp, vp]),
     "hk_sync": (C.c_int, [vp]),
-    "hk_keygen": (C.c_int, [vp, u64]),
-    "hk_add_galois_keys": (C.c_int, [vp, u64, vp, i32]),
-    "hk_add_galois_keys_level": (C.c_int, [vp, u64, vp, i32, i32]),
+    "hk_keygen": (C.c_int, [vp, vp]),
+    "hk_add_galois_keys": (C.c_int, [vp, vp, vp, i32]),
+    "hk_add_galois_keys_level": (C.c_int, [vp, vp, vp, i32, i32]),
     "hk_has_galois_key": (C.c_int, [vp, u32]),
     "hk_export_key": (C.c_int, [vp, i32, u32, vp]),
     "hk_key_words": (C.c_uint64, [vp, i32]),
@@ -41,7 +41,7 @@ SIGNATURES = {
     "hk_encode": (C.c_int, [vp, vp, i32, i32, dbl, vp]),
     "hk_encode_diagonals": (C.c_int, [vp, vp, i32, i32, i32, i32, i32, i32, i32, dbl, vp]),
     "hk_encode_const": (C.c_int, [vp, dbl, i32, dbl, vp]),
-    "hk_encrypt": (C.c_int, [vp, vp, i32, i32, u64, vp]),
+    "hk_encrypt": (C.c_int, [vp, vp, i32, i32, vp, u64, vp]),
     "hk_decrypt": (C.c_int, [vp, vp, i32, i32, dbl, vp]),
     "hk_add": (C.c_int, [vp, vp, i32, vp, i32, vp, i32]),
     "hk_sub": (C.c_int, [vp, vp, i32, vp, i32, vp, i32]),
@@ -86,6 +86,13 @@ def make_params_struct(params):
     st = HkParams(params.log_n, len(params.q), len(params.p), params.dnum,
                   arr(params.q), arr(params.p), arr(params.psi_q), arr(params.psi_p))
     return st, keep
+
+
+def seed_words(key: bytes) -> C.Array:
+    """A 256-bit ChaCha20 seed (32 bytes) as the uint64_t[4] the ABI takes."""
+    if len(key) != 32:
+        raise ValueError("seeds are 32 bytes")
+    return (C.c_uint64 * 4)(*[int.from_bytes(key[8 * i:8 * i + 8], "little") for i in range(4)])
 
 
 def check(lib, ctx, rc: int, what: str) -> None:

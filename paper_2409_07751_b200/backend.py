@@ -34,6 +34,7 @@ import struct
 
 import numpy as np
 
+from . import _abi
 from ._ref import hekan
 from .errors import CorruptFile, DepthExhausted, InputTooLong, LengthMismatch, SchemaMismatch
 from .params import CkksParams, kan_params
@@ -114,7 +115,7 @@ class HeBackend:
     product; tests may substitute the CPU oracle engine to check bit-exactness."""
 
     def __init__(self, config: BackendConfig, params: CkksParams | None = None,
-                 engine=None, device: int = 0, seed: int | None = None, enc_stream: int = 0):
+                 engine=None, device: int = 0, seed: int | None = None, sample_offset: int = 0):
         if params is None:
             log_n = int(math.log2(config.slot_count)) + 1
             params = kan_params(config.depth_budget, log_n=log_n)
@@ -142,21 +143,26 @@ class HeBackend:
         self._mat_cache: dict = {}
         self._pt_cache_bytes = 0
         self.pt_cache_limit = 8 << 30
-        # Key and encryption randomness: the OS CSPRNG unless a seed is passed
-        # explicitly (bit-exact oracle parity; identical keys on every rank of a
-        # sharded run, each rank with its own `enc_stream` so no two
-        # encryptions share (a, e)).
-        self._master = secrets.randbits(64) if seed is None else int(seed)
-        self._enc_stream = int(enc_stream)
-        self.engine.call("hk_keygen", C.c_uint64(self._seed("keys")))
+        # Key and encryption randomness (ChaCha20 on the device, 256-bit seeds):
+        # a master key from the OS CSPRNG unless a seed is passed explicitly
+        # (bit-exact oracle parity; one seed shared by every rank of a sharded
+        # run). `sample_offset` is this backend's first global sample index:
+        # encryption randomness is indexed by global sample, so no two
+        # encryptions of a sharded batch share (a, e), and the shards encrypt
+        # exactly as the whole batch would in one process.
+        self._master = (secrets.token_bytes(32) if seed is None
+                        else hashlib.blake2b(f"hekan-b200:{int(seed)}".encode(), digest_size=32).digest())
+        self._sample_offset = int(sample_offset)
+        self.engine.call("hk_keygen", self._seed("keys"))
 
     # ------------------------------------------------------------------
     # boundary plumbing
     # ------------------------------------------------------------------
 
-    def _seed(self, what: str, idx: int = 0) -> int:
-        h = hashlib.blake2b(f"{self._master}:{what}:{idx}".encode(), digest_size=8)
-        return int.from_bytes(h.digest(), "little")
+    def _seed(self, what: str, idx: int = 0):
+        """uint64_t[4] ChaCha20 key for one purpose, derived from the master key."""
+        return _abi.seed_words(hashlib.blake2b(f"{what}:{idx}".encode(), key=self._master,
+                                               digest_size=32).digest())
 
     def encode(self, values) -> PlainVector:
         """Zero-pad a vector (or broadcast a scalar) to the slot count (:149-158)."""
@@ -185,9 +191,8 @@ class HeBackend:
         pt = eng.alloc_u64((level + 1) * B * self.n)
         eng.call("hk_encode", eng.addr(slots), B, level, self.params.scale(level), eng.addr(pt))
         ct = eng.alloc_u64(2 * (level + 1) * B * self.n)
-        seed = self._seed("enc", next(self._enc_counter) if self._enc_stream == 0
-                          else f"{self._enc_stream}:{next(self._enc_counter)}")
-        eng.call("hk_encrypt", eng.addr(pt), level, B, C.c_uint64(seed), eng.addr(ct))
+        seed = self._seed("enc", next(self._enc_counter))
+        eng.call("hk_encrypt", eng.addr(pt), level, B, seed, C.c_uint64(self._sample_offset), eng.addr(ct))
         return self._wrap(ct, level, B, batched)
 
     def decrypt(self, a: CipherText) -> np.ndarray:
@@ -550,7 +555,7 @@ class HeBackend:
         missing = [int(g) for g in galois_elts if lib.hk_has_galois_key(ctx, C.c_uint32(int(g))) < level + 1]
         if missing:
             missing = sorted(set(missing))
-            self.engine.call("hk_add_galois_keys_level", C.c_uint64(self._seed("galois")),
+            self.engine.call("hk_add_galois_keys_level", self._seed("galois"),
                              self.engine.u32_array(missing), len(missing), level)
 
     def ensure_rotation_keys(self, steps, level: int | None = None) -> None:
@@ -587,6 +592,13 @@ class HeBackend:
         """u64 [2][level+1][B][N] host copy of the RNS limbs."""
         self.engine.sync()
         return self.engine.get_u64(a.data).reshape(2, a.level + 1, a.batch, self.n)
+
+    def adopt(self, data, level: int, batch: int, batched: bool = True) -> CipherText:
+        """Wrap an engine buffer u64 [2][level+1][batch][N] (e.g. gathered from
+        other ranks) as a ciphertext of this backend, without copying."""
+        if int(np.prod(data.shape)) != 2 * (level + 1) * batch * self.n:
+            raise LengthMismatch(f"buffer of {int(np.prod(data.shape))} words for level {level}, batch {batch}")
+        return self._wrap(data, level, batch, batched)
 
     def import_ct(self, limbs: np.ndarray, level: int, batched: bool = True) -> CipherText:
         limbs = np.asarray(limbs, dtype=np.uint64)
@@ -664,9 +676,9 @@ CkksBackend = HeBackend
 
 
 def make_backend(config: BackendConfig, params: CkksParams | None = None, engine=None,
-                 device: int = 0, seed: int | None = None, enc_stream: int = 0) -> HeBackend:
+                 device: int = 0, seed: int | None = None, sample_offset: int = 0) -> HeBackend:
     """RNS-CKKS backend on the sm_100a engine (reference factory :293-297)."""
-    return HeBackend(config, params=params, engine=engine, device=device, seed=seed, enc_stream=enc_stream)
+    return HeBackend(config, params=params, engine=engine, device=device, seed=seed, sample_offset=sample_offset)
 
 
 def slotwise(op_kind: str, a: CipherText, b) -> CipherText:

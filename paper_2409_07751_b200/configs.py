@@ -51,22 +51,30 @@ CONFIGS = {
 }
 
 
-def make_inputs(cfg: KanConfig, seed: int = 1) -> np.ndarray:
-    """(batch, n_in) synthetic inputs with the config's distribution."""
+def make_inputs(cfg: KanConfig, seed: int = 1, rows: int | None = None) -> np.ndarray:
+    """(rows, n_in) synthetic inputs with the config's distribution (default
+    rows = the config's batch). Draws are sequential, so the first cfg.batch
+    rows are the same for any rows >= cfg.batch (a multi-GPU global batch
+    extends the single-GPU one); c5 standardises with the first cfg.batch
+    rows' per-channel statistics."""
     rng = np.random.default_rng(seed)
     n = cfg.dims[0]
+    rows = cfg.batch if rows is None else max(int(rows), 1)
+    draw = max(rows, cfg.batch)
     if cfg.name == "c1":
-        return rng.uniform(-1.0, 1.0, (cfg.batch, n))
-    if cfg.name == "c3":
-        return np.clip(rng.normal(0.0, 1.0, (cfg.batch, n)), -2.0, 2.0)
-    if cfg.name == "c4":
-        return rng.uniform(0.0, 1.0, (cfg.batch, n))
-    if cfg.name == "c5":
-        x = rng.uniform(0.0, 1.0, (cfg.batch, 32, 32, 3))
-        mu = x.mean(axis=(0, 1, 2), keepdims=True)
-        sd = x.std(axis=(0, 1, 2), keepdims=True)
-        return ((x - mu) / sd).reshape(cfg.batch, n)  # HWC raster (inference.py:110-112)
-    raise KeyError(cfg.name)
+        x = rng.uniform(-1.0, 1.0, (draw, n))
+    elif cfg.name == "c3":
+        x = np.clip(rng.normal(0.0, 1.0, (draw, n)), -2.0, 2.0)
+    elif cfg.name == "c4":
+        x = rng.uniform(0.0, 1.0, (draw, n))
+    elif cfg.name == "c5":
+        img = rng.uniform(0.0, 1.0, (draw, 32, 32, 3))
+        mu = img[:cfg.batch].mean(axis=(0, 1, 2), keepdims=True)
+        sd = img[:cfg.batch].std(axis=(0, 1, 2), keepdims=True)
+        x = ((img - mu) / sd).reshape(draw, n)  # HWC raster (inference.py:110-112)
+    else:
+        raise KeyError(cfg.name)
+    return x[:rows]
 
 
 def build_model(cfg: KanConfig, calib: np.ndarray, seed: int = 0) -> KanModel:
@@ -92,8 +100,5 @@ def build_model(cfg: KanConfig, calib: np.ndarray, seed: int = 0) -> KanModel:
 def workload(name: str, batch: int | None = None):
     """(KanConfig, model, inputs[batch, n_in]) for a named config."""
     cfg = CONFIGS[name]
-    inputs = make_inputs(cfg)
-    model = build_model(cfg, inputs)
-    if batch is not None:
-        inputs = inputs[:batch]
-    return cfg, model, inputs
+    model = build_model(cfg, make_inputs(cfg))
+    return cfg, model, make_inputs(cfg, rows=batch)

@@ -132,15 +132,37 @@ __device__ __forceinline__ uint64_t mul_shoup_fast(uint64_t y, uint64_t w, uint6
 
 __device__ __forceinline__ uint32_t brev_bits(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
 
-// counter-based randomness — identical formulas to the oracle
-__host__ __device__ __forceinline__ uint64_t hk_mix64(uint64_t z) {
-    z += 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-__host__ __device__ __forceinline__ uint64_t hk_rng64(uint64_t seed, uint64_t stream, uint64_t ctr) {
-    return hk_mix64(hk_mix64(seed ^ hk_mix64(stream * 0xD1B54A32D192ED03ull)) + ctr);
+// Counter-mode randomness: ChaCha20 keyed by a 256-bit seed, 64-bit block
+// counter (words 12-13) and the 64-bit stream id as the nonce (words 14-15).
+// Word c of a stream is the 64-bit pair (2(c mod 8), 2(c mod 8)+1) of block
+// c / 8 — identical to the oracle (oracle/ckks_oracle.c: rng64).
+struct HkSeed {
+    uint64_t w[4];
+};
+__device__ __forceinline__ uint32_t hk_rotl(uint32_t x, int r) { return __funnelshift_l(x, x, r); }
+#define HK_QR(a, b, c, d)                                                              \
+    a += b; d ^= a; d = hk_rotl(d, 16); c += d; b ^= c; b = hk_rotl(b, 12);            \
+    a += b; d ^= a; d = hk_rotl(d, 8);  c += d; b ^= c; b = hk_rotl(b, 7);
+// the 8 64-bit words of block `block` of `stream`
+__device__ __forceinline__ void hk_chacha_block(const HkSeed &key, uint64_t block, uint64_t stream,
+                                                uint64_t out[8]) {
+    uint32_t s[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u,
+                      (uint32_t)key.w[0], (uint32_t)(key.w[0] >> 32), (uint32_t)key.w[1], (uint32_t)(key.w[1] >> 32),
+                      (uint32_t)key.w[2], (uint32_t)(key.w[2] >> 32), (uint32_t)key.w[3], (uint32_t)(key.w[3] >> 32),
+                      (uint32_t)block, (uint32_t)(block >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+    uint32_t x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = s[i];
+#pragma unroll 1
+    for (int r = 0; r < 10; ++r) {
+        HK_QR(x[0], x[4], x[8], x[12]) HK_QR(x[1], x[5], x[9], x[13])
+        HK_QR(x[2], x[6], x[10], x[14]) HK_QR(x[3], x[7], x[11], x[15])
+        HK_QR(x[0], x[5], x[10], x[15]) HK_QR(x[1], x[6], x[11], x[12])
+        HK_QR(x[2], x[7], x[8], x[13]) HK_QR(x[3], x[4], x[9], x[14])
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        out[j] = (uint64_t)(x[2 * j] + s[2 * j]) | ((uint64_t)(x[2 * j + 1] + s[2 * j + 1]) << 32);
 }
 __device__ __forceinline__ int64_t cbd21(uint64_t x) {
     return (int64_t)__popcll(x & 0x1FFFFFull) - (int64_t)__popcll((x >> 21) & 0x1FFFFFull);

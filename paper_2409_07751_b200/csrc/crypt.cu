@@ -1,23 +1,28 @@
 // crypt.cu — key generation, RLWE encryption and decryption on the GPU.
 //
 // Replaces HeBackend.encrypt/decrypt (hekan/backend.py:160-170), which in the
-// reference copy slots. Randomness is counter-based (hk_rng64: seed, stream,
-// counter) so the oracle reproduces every ciphertext bit for bit.
+// reference copy slots. Randomness is counter-mode ChaCha20 (common.cuh:
+// hk_chacha_block; seed, stream, counter) so the oracle reproduces every key
+// and ciphertext bit for bit. Sampling kernels give each thread 8 consecutive
+// coefficients: one ChaCha block per stream per thread (N >= 8).
 #include "common.cuh"
 
 int hk_decode_launch(hk_ctx *c, double2 *w, double2 *tmp, int B, double *slots);
 
 namespace {
 
-// residues of a ternary secret in every limb: s[m][k]
-__global__ void sample_secret(uint64_t *__restrict__ s, uint64_t seed, int log_n, int nm,
+// residues of a ternary secret in every limb: s[m][k], 8 coefficients per thread
+__global__ void sample_secret(uint64_t *__restrict__ s, HkSeed seed, int log_n, int nm,
                               const ModQ *__restrict__ mq) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int N = 1 << log_n;
-    if (gid >= (long long)nm * N) return;
-    const int m = (int)(gid >> log_n), k = (int)(gid & (N - 1));
-    const int64_t v = (int64_t)(hk_rng64(seed, ST_SECRET, (uint64_t)k) % 3) - 1;
-    s[gid] = smod_dev(v, mq[m].q);
+    if (gid >= ((long long)nm * N) >> 3) return;
+    const long long o = gid << 3;
+    const int m = (int)(o >> log_n), k0 = (int)(o & (N - 1));
+    uint64_t r[8];
+    hk_chacha_block(seed, (uint64_t)k0 >> 3, ST_SECRET, r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[o + j] = smod_dev((int64_t)(r[j] % 3) - 1, mq[m].q);
 }
 
 __global__ void square_mod(const uint64_t *__restrict__ a, uint64_t *__restrict__ out, int log_n, int nm,
@@ -50,16 +55,23 @@ __global__ void automorph_polys(const uint64_t *__restrict__ in, uint64_t *__res
 // key rows r < rows: modulus m = r <= top ? r : n_q + (r - top - 1) (top = key level)
 __device__ __forceinline__ int key_row_mod(int r, int top, int n_q) { return r <= top ? r : n_q + (r - top - 1); }
 
-__global__ void ks_sample(uint64_t *__restrict__ b, uint64_t *__restrict__ a, uint64_t seed, uint64_t stream_a,
+__global__ void ks_sample(uint64_t *__restrict__ b, uint64_t *__restrict__ a, HkSeed seed, uint64_t stream_a,
                           uint64_t stream_e, int log_n, int rows, int top, int n_q, const ModQ *__restrict__ mq) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int N = 1 << log_n;
-    if (gid >= (long long)rows * N) return;
-    const int r = (int)(gid >> log_n), k = (int)(gid & (N - 1));
+    if (gid >= ((long long)rows * N) >> 3) return;
+    const long long o = gid << 3;
+    const int r = (int)(o >> log_n), k0 = (int)(o & (N - 1));
     const int m = key_row_mod(r, top, n_q);
     const ModQ mm = mq[m];
-    a[gid] = reduce128(0, hk_rng64(seed, stream_a, (uint64_t)m * N + k), mm);  // == rng % q (exact Barrett)
-    b[gid] = smod_dev(cbd21(hk_rng64(seed, stream_e, (uint64_t)k)), mm.q);
+    uint64_t ra[8], re[8];
+    hk_chacha_block(seed, ((uint64_t)m * N + k0) >> 3, stream_a, ra);
+    hk_chacha_block(seed, (uint64_t)k0 >> 3, stream_e, re);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        a[o + j] = reduce128(0, ra[j], mm);  // == rng % q (exact Barrett)
+        b[o + j] = smod_dev(cbd21(re[j]), mm.q);
+    }
 }
 
 // b = e_ntt - a*s (+ P*s' on digit limbs); s, sp are full [n_mod][N]
@@ -78,17 +90,26 @@ __global__ void ks_finish(uint64_t *__restrict__ b, const uint64_t *__restrict__
 }
 
 // encryption: c1 = a (uniform), e (coefficient) into c0 temporarily
-__global__ void enc_sample(uint64_t *__restrict__ c0, uint64_t *__restrict__ c1, uint64_t seed, int log_n,
-                           int nl, int B, const ModQ *__restrict__ mq) {
+// sample index = first + b: a sharded batch encrypts exactly as the whole batch
+__global__ void enc_sample(uint64_t *__restrict__ c0, uint64_t *__restrict__ c1, HkSeed seed, uint64_t first,
+                           int log_n, int nl, int B, const ModQ *__restrict__ mq) {
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int N = 1 << log_n;
-    if (gid >= (long long)nl * B * N) return;
-    const int k = (int)(gid & (N - 1));
-    const long long lb = gid >> log_n;
+    if (gid >= ((long long)nl * B * N) >> 3) return;
+    const long long o = gid << 3;
+    const int k0 = (int)(o & (N - 1));
+    const long long lb = o >> log_n;
     const int l = (int)(lb / B), b = (int)(lb - (long long)l * B);
     const ModQ mm = mq[l];
-    c1[gid] = reduce128(0, hk_rng64(seed, ST_ENC_A, ((uint64_t)b * nl + l) * N + k), mm);  // == rng % q
-    c0[gid] = smod_dev(cbd21(hk_rng64(seed, ST_ENC_E, (uint64_t)b * N + k)), mm.q);
+    const uint64_t smp = first + (uint64_t)b;
+    uint64_t ra[8], re[8];
+    hk_chacha_block(seed, ((smp * nl + l) * N + k0) >> 3, ST_ENC_A, ra);
+    hk_chacha_block(seed, (smp * N + k0) >> 3, ST_ENC_E, re);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        c1[o + j] = reduce128(0, ra[j], mm);  // == rng % q
+        c0[o + j] = smod_dev(cbd21(re[j]), mm.q);
+    }
 }
 
 __global__ void enc_finish(uint64_t *__restrict__ c0, const uint64_t *__restrict__ c1,
@@ -162,7 +183,7 @@ uint64_t h_inv(uint64_t a, uint64_t q) {
 }
 
 // key-switching key for target s' (device [nm][N], NTT) into key [n_digits][2][nm][N]
-int make_ks_key(hk_ctx *c, uint64_t seed, uint64_t tag, const uint64_t *sprime, uint64_t *key, int top) {
+int make_ks_key(hk_ctx *c, const HkSeed &seed, uint64_t tag, const uint64_t *sprime, uint64_t *key, int top) {
     const int N = c->n, nm = c->n_mod, rows = top + 1 + c->n_p, nd = top / c->alpha + 1;
     std::vector<uint64_t> pmod(nm, 0);
     for (int i = 0; i < c->n_q; ++i) {
@@ -178,7 +199,7 @@ int make_ks_key(hk_ctx *c, uint64_t seed, uint64_t tag, const uint64_t *sprime, 
         const int d0 = j * c->alpha, d1 = std::min((j + 1) * c->alpha, c->n_q);
         uint64_t *bj = key + ((size_t)j * 2 + 0) * rows * N;
         uint64_t *aj = key + ((size_t)j * 2 + 1) * rows * N;
-        ks_sample<<<hk_grid(tot, 256), 256, 0, c->stream>>>(bj, aj, seed, ST_KEY_A + tag * 64 + j,
+        ks_sample<<<hk_grid(tot >> 3, 256), 256, 0, c->stream>>>(bj, aj, seed, ST_KEY_A + tag * 64 + j,
                                                               ST_KEY_E + tag * 64 + j, c->log_n, rows, top, c->n_q,
                                                               c->d_modq); ++c->launches;
         int rc = ntt_fwd_launch(c, bj, 0, top + 1, 1, 0);
@@ -210,8 +231,12 @@ uint64_t hk_key_words(const hk_ctx *c, int32_t which) {
     return (uint64_t)c->n_digits * 2 * nm * N;
 }
 
-int hk_keygen(hk_ctx *c, uint64_t seed) {
+static HkSeed to_seed(const uint64_t w[4]) { return HkSeed{{w[0], w[1], w[2], w[3]}}; }
+
+int hk_keygen(hk_ctx *c, const uint64_t seed_words[4]) {
     const int N = c->n, nm = c->n_mod;
+    if (!seed_words) return hk_fail(c, HK_E_ARG, "keygen: null seed");
+    const HkSeed seed = to_seed(seed_words);
     cudaFree(c->d_sk);
     cudaFree(c->d_relin);
     for (auto &kv : c->gal) cudaFree(kv.second.p);
@@ -220,7 +245,7 @@ int hk_keygen(hk_ctx *c, uint64_t seed) {
     HK_CUDA(c, cudaMalloc(&c->d_sk, sizeof(uint64_t) * nm * N));
     HK_CUDA(c, cudaMalloc(&c->d_relin, sizeof(uint64_t) * hk_key_words(c, 1)));
     const long long tot = (long long)nm * N;
-    sample_secret<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c->d_sk, seed, c->log_n, nm, c->d_modq); ++c->launches;
+    sample_secret<<<hk_grid(tot >> 3, 256), 256, 0, c->stream>>>(c->d_sk, seed, c->log_n, nm, c->d_modq); ++c->launches;
     int rc = ntt_fwd_launch(c, c->d_sk, 0, nm, 1, 0);
     if (rc) return rc;
     uint64_t *s2 = nullptr;
@@ -238,8 +263,11 @@ int hk_has_galois_key(const hk_ctx *c, uint32_t g) {
     return it == c->gal.end() ? 0 : it->second.level + 1;
 }
 
-int hk_add_galois_keys_level(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n, int32_t level) {
+int hk_add_galois_keys_level(hk_ctx *c, const uint64_t seed_words[4], const uint32_t *gs, int32_t n,
+                             int32_t level) {
     if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (!seed_words) return hk_fail(c, HK_E_ARG, "galois keys: null seed");
+    const HkSeed seed = to_seed(seed_words);
     if (level < 0 || level >= c->n_q) return hk_fail(c, HK_E_ARG, "galois key level %d out of range", level);
     const int N = c->n, nm = c->n_mod;
     const uint32_t M = 2u * (uint32_t)N;
@@ -265,7 +293,7 @@ int hk_add_galois_keys_level(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32
     return HK_OK;
 }
 
-int hk_add_galois_keys(hk_ctx *c, uint64_t seed, const uint32_t *gs, int32_t n) {
+int hk_add_galois_keys(hk_ctx *c, const uint64_t seed[4], const uint32_t *gs, int32_t n) {
     return hk_add_galois_keys_level(c, seed, gs, n, c->n_q - 1);
 }
 
@@ -284,14 +312,18 @@ int hk_export_key(hk_ctx *c, int32_t which, uint32_t g, uint64_t *out) {
     return HK_OK;
 }
 
-int hk_encrypt(hk_ctx *c, const uint64_t *pt, int32_t level, int32_t B, uint64_t seed, uint64_t *ct) {
+int hk_encrypt(hk_ctx *c, const uint64_t *pt, int32_t level, int32_t B, const uint64_t seed_words[4],
+               uint64_t first_sample, uint64_t *ct) {
     if (!c->have_keys) return hk_fail(c, HK_E_NOKEY, "keygen first");
+    if (!seed_words) return hk_fail(c, HK_E_ARG, "encrypt: null seed");
+    const HkSeed seed = to_seed(seed_words);
     if (level < 0 || level >= c->n_q || B < 0) return hk_fail(c, HK_E_ARG, "encrypt: level out of range");
     if (B == 0) return HK_OK;
     const int nl = level + 1;
     const long long tot = (long long)nl * B * c->n;
     uint64_t *c0 = ct, *c1 = ct + tot;
-    enc_sample<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c0, c1, seed, c->log_n, nl, B, c->d_modq); ++c->launches;
+    enc_sample<<<hk_grid(tot >> 3, 256), 256, 0, c->stream>>>(c0, c1, seed, first_sample, c->log_n, nl, B,
+                                                                   c->d_modq); ++c->launches;
     int rc = ntt_fwd_launch(c, c0, 0, nl, B, 0);
     if (rc) return rc;
     enc_finish<<<hk_grid(tot, 256), 256, 0, c->stream>>>(c0, c1, pt, c->d_sk, c->log_n, B, c->d_modq, tot); ++c->launches;

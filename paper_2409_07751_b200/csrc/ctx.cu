@@ -148,7 +148,7 @@ int hk_sync(hk_ctx *c) {
 }
 
 int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
-    if (!pr || !out || pr->log_n < 2 || pr->log_n > 17 || pr->n_q < 1 || pr->n_p < 1 || pr->dnum < 1 || pr->dnum > 8 ||
+    if (!pr || !out || pr->log_n < 3 || pr->log_n > 17 || pr->n_q < 1 || pr->n_p < 1 || pr->dnum < 1 || pr->dnum > 8 ||
         pr->n_q + pr->n_p > HK_MAX_MOD)
         return HK_E_ARG;
     if (cudaSetDevice(device) != cudaSuccess) return HK_E_CUDA;

@@ -154,6 +154,11 @@ class CkksParams:
         the rescaled product lands on the canonical scale of level - 1."""
         return self.q[level] * self.scales[level - 1] / self.scales[level]
 
+    @property
+    def log_pq(self) -> float:
+        """log2 of the whole modulus Q * P (the number security is read from)."""
+        return sum(math.log2(x) for x in list(self.q) + list(self.p))
+
     def describe(self) -> str:
         qb = [round(math.log2(x), 2) for x in self.q]
         pb = [round(math.log2(x), 2) for x in self.p]
@@ -171,8 +176,8 @@ def make_params(log_n: int, depth: int, scale_bits: int = 46, q0_bits: int = 50,
                 label: str = "") -> CkksParams:
     """Scale-stable chain: q_0 just below 2^q0_bits, rescaling primes chosen
     top-down so the canonical scale never drifts from 2^scale_bits."""
-    if not 2 <= log_n <= 17:
-        raise ValueError("log_n must be in [2, 17]")
+    if not 3 <= log_n <= 17:
+        raise ValueError("log_n must be in [3, 17]")
     if depth < 0:
         raise ValueError("depth must be >= 0")
     two_n = 2 << log_n

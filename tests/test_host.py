@@ -110,25 +110,35 @@ def test_mono_to_cheb_scaled_exact():
 
 
 def _dist_worker(rank, world, port, q):
-    import torch
+    """One CPU rank of a sharded c1 run (oracle engine, gloo): shared key seed,
+    its block of the global batch, gather of the outputs to rank 0."""
     import torch.distributed as dist
-    from paper_2409_07751_b200.distributed import gather_to_root, shard_rows, unshard_rows
+    from oracle.engine import OracleEngine
+    from paper_2409_07751_b200 import configs, distributed as D, inference as inf
+    from paper_2409_07751_b200.backend import BackendConfig, HeBackend
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    X = np.arange(10 * 3, dtype=np.float64).reshape(10, 3)
-    mine = shard_rows(X, rank, world)
-    out = torch.from_numpy(np.ascontiguousarray(mine[:5] * 2.0))  # equal shapes per rank
-    got = gather_to_root(out, world, rank)
-    t = torch.tensor([float(rank + 1)])
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    seed = D.shared_seed(world, rank)
+    _, model, X = configs.workload("c1", batch=4)
+    p = make_params(8, 36)
+    lo, _ = D.block_range(len(X), rank, world)
+    be = HeBackend(BackendConfig(slot_count=p.slot_count, depth_budget=36), p, engine=OracleEngine(p), seed=seed,
+                   sample_offset=lo)
+    out, _ = inf.model_forward_he(model, inf.encrypt_input(D.shard_rows(X, rank, world), model, be),
+                                  inf.PipelineConfig())
+    full = D.gather_ciphertexts(be, out, world, rank)
     if rank == 0:
-        full = unshard_rows([g.numpy() for g in got], 10)
-        q.put((np.array_equal(full, X * 2.0), float(t.item())))
+        q.put((seed, be.export_ct(full), be.decrypt(full)[:, :1]))
     dist.destroy_process_group()
 
 
-def test_sharding_and_gather_gloo_world2():
+def test_sharded_c1_gather_gloo_world2():
+    """Two ranks, 2 samples each: the gathered level-0 ciphertext equals, limb
+    for limb, the same 4 samples run by one process with the same seed."""
     import multiprocessing as mp
     import socket
+    from oracle.engine import OracleEngine
+    from paper_2409_07751_b200 import configs, inference as inf
+    from paper_2409_07751_b200.backend import BackendConfig, HeBackend
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -138,7 +148,13 @@ def test_sharding_and_gather_gloo_world2():
     procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    ok, mx = q.get(timeout=120)
+    seed, limbs, dec = q.get(timeout=600)
     for p in procs:
         p.join(timeout=60)
-    assert ok and mx == 2.0
+    _, model, X = configs.workload("c1", batch=4)
+    p = make_params(8, 36)
+    be = HeBackend(BackendConfig(slot_count=p.slot_count, depth_budget=36), p, engine=OracleEngine(p), seed=seed)
+    out, _ = inf.model_forward_he(model, inf.encrypt_input(X, model, be), inf.PipelineConfig())
+    assert np.array_equal(limbs, be.export_ct(out))
+    gold = np.load(os.path.join(ROOT, "tests", "golden", "c1.npz"))["mirrored"][:4]
+    assert np.abs(dec - gold).max() < 1e-4
