@@ -24,10 +24,23 @@
 #pragma once
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace ntt16 {
+
+// Two-phase epilogues: an epilogue with a nested `Pre` type splits into
+// `Pre prep(l, P, idx)` (every operand load; independent of the NTT output)
+// and `fin(l, P, idx, pre, v)` (the arithmetic and the store). The row phase
+// issues all 16 preps of a thread before its first store, so the operand
+// loads of one row block are in flight together instead of one round trip per
+// output (the functors' pointers may alias the output, so the compiler cannot
+// hoist loads above earlier stores of a single-phase epilogue).
+template <class E, class = void>
+struct HasPrep : std::false_type {};
+template <class E>
+struct HasPrep<E, std::void_t<typename E::Pre>> : std::true_type {};
 
 constexpr int kLogN = 16;
 constexpr int kN = 1 << kLogN;
@@ -207,8 +220,16 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
 #pragma unroll
     for (int v = 0; v < 16; ++v) su[pad16(16 * k + v)] = d2canon(x[v], m);
     __syncwarp();
+    if constexpr (HasPrep<Epi>::value) {
+        typename Epi::Pre pre[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) epi(l, P, r * 256 + k + 16 * u, su[pad16(k + 16 * u)]);
+        for (int u = 0; u < 16; ++u) pre[u] = epi.prep(l, P, r * 256 + k + 16 * u);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) epi.fin(l, P, r * 256 + k + 16 * u, pre[u], su[pad16(k + 16 * u)]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) epi(l, P, r * 256 + k + 16 * u, su[pad16(k + 16 * u)]);
+    }
 }
 
 // One polynomial per cluster of CPP CTAs (launch attribute; CPP = 1: a lone CTA).

@@ -534,13 +534,20 @@ struct EpiRescale {
     uint64_t *out;
     const ulonglong2 *qinv;
     int B;
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+    using Pre = uint64_t;  // X (two-phase epilogue, ntt16::HasPrep)
+    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
+        const int pb = (int)(P - (long long)l * 2 * B), p = pb >= B ? 1 : 0, b = pb - p * B;
+        return src(p, l, b, idx);
+    }
+    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre x, uint64_t v) const {
         const int pb = (int)(P - (long long)l * 2 * B), p = pb >= B ? 1 : 0, b = pb - p * B;
         const uint64_t q = src.mq[l].q;
         const ulonglong2 w = qinv[l];
-        const uint64_t x = src(p, l, b, idx);
         out[((long long)p * src.la + l) * src.BN + ((long long)b << src.log_n) + idx] =
             mul_shoup(sub_mod(x, v, q), w.x, w.y, q);
+    }
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        fin(l, P, idx, prep(l, P, idx), v);
     }
 };
 
@@ -575,16 +582,25 @@ struct EpiModDown {
     uint32_t g;
     int B, log_n;
     long long BN;
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+    struct Pre {
+        uint64_t a, add;
+    };
+    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
+        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
+        Pre r{acc[o], 0};
+        if (addend) r.add = addend[g == 1u ? o : o - idx + auto_src((uint32_t)idx, g, log_n)];
+        return r;
+    }
+    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre pr, uint64_t v) const {
         const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
         const uint64_t q = mq[l].q;
         const ulonglong2 w = pinv[l];
-        uint64_t r = mul_shoup(sub_mod(acc[o], v, q), w.x, w.y, q);
-        if (addend) {
-            const long long src = g == 1u ? o : o - idx + auto_src((uint32_t)idx, g, log_n);
-            r = add_mod(r, addend[src], q);
-        }
+        uint64_t r = mul_shoup(sub_mod(pr.a, v, q), w.x, w.y, q);
+        if (addend) r = add_mod(r, pr.add, q);
         out[o] = r;
+    }
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        fin(l, P, idx, prep(l, P, idx), v);
     }
 };
 
@@ -699,13 +715,22 @@ struct EpiMdRsT {
     long long BN;
     LinTerm lin;
     Affine aff;
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+    using Pre = uint64_t;  // y = acc + P d
+    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
         const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
         const uint64_t q = mq[l].q;
-        const ulonglong2 Pm = pmod[l], w = mqinv[l];
+        const ulonglong2 Pm = pmod[l];
         const uint64_t d = lin.apply(which, l, o, T.d(which, l, o), q);
-        const uint64_t y = add_mod(acc[o], mul_shoup(d, Pm.x, Pm.y, q), q);
+        return add_mod(acc[o], mul_shoup(d, Pm.x, Pm.y, q), q);
+    }
+    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre y, uint64_t v) const {
+        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 w = mqinv[l];
         out[o] = aff.apply(which, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
+    }
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        fin(l, P, idx, prep(l, P, idx), v);
     }
 };
 // Merged ModDown + rescale of both halves of a relinearised product: launches
@@ -750,15 +775,26 @@ struct EpiMdRsT2 {
     long long BN, pne, pout;  // offsets of half 1 in acc / out
     LinTerm lin;
     Affine aff;
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+    using Pre = uint64_t;  // y = acc_p + P d_p
+    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
         const long long pb = P - (long long)l * 2 * B;
         const int p = (int)(pb & 1);
         const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
         const uint64_t q = mq[l].q;
-        const ulonglong2 Pm = pmod[l], w = mqinv[l];
+        const ulonglong2 Pm = pmod[l];
         const uint64_t d = lin.apply(p, l, o, T.d(p, l, o), q);
-        const uint64_t y = add_mod(acc[p * pne + o], mul_shoup(d, Pm.x, Pm.y, q), q);
+        return add_mod(acc[p * pne + o], mul_shoup(d, Pm.x, Pm.y, q), q);
+    }
+    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre y, uint64_t v) const {
+        const long long pb = P - (long long)l * 2 * B;
+        const int p = (int)(pb & 1);
+        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 w = mqinv[l];
         out[p * pout + o] = aff.apply(p, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
+    }
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        fin(l, P, idx, prep(l, P, idx), v);
     }
 };
 // ModDown of both halves of a key switch (interleaved samples 2 b + p):
@@ -771,19 +807,30 @@ struct EpiModDown2 {
     uint32_t g;
     int B, log_n;
     long long BN, pne;
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+    struct Pre {
+        uint64_t a, add;
+    };
+    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
+        const long long pb = P - (long long)l * 2 * B;
+        const int p = (int)(pb & 1);
+        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
+        Pre r{acc[p * pne + o], 0};
+        const uint64_t *addend = p ? add1 : add0;
+        if (addend) r.add = addend[g == 1u ? o : o - idx + auto_src((uint32_t)idx, g, log_n)];
+        return r;
+    }
+    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre pr, uint64_t v) const {
         const long long pb = P - (long long)l * 2 * B;
         const int p = (int)(pb & 1);
         const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
         const uint64_t q = mq[l].q;
         const ulonglong2 w = pinv[l];
-        uint64_t r = mul_shoup(sub_mod(acc[p * pne + o], v, q), w.x, w.y, q);
-        const uint64_t *addend = p ? add1 : add0;
-        if (addend) {
-            const long long src = g == 1u ? o : o - idx + auto_src((uint32_t)idx, g, log_n);
-            r = add_mod(r, addend[src], q);
-        }
+        uint64_t r = mul_shoup(sub_mod(pr.a, v, q), w.x, w.y, q);
+        if (p ? add1 : add0) r = add_mod(r, pr.add, q);
         (p ? out1 : out0)[o] = r;
+    }
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        fin(l, P, idx, prep(l, P, idx), v);
     }
 };
 // iNTT prologue: y = acc_l + P d_l with d_l from (a, b)
@@ -841,12 +888,21 @@ struct EpiMdRs {
     const ModQ *mq;
     int B, log_n;
     long long BN;
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+    using Pre = uint64_t;  // y = acc + P d
+    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
         const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
         const uint64_t q = mq[l].q;
-        const ulonglong2 Pm = pmod[l], w = mqinv[l];
-        const uint64_t y = add_mod(acc[o], mul_shoup(d[o], Pm.x, Pm.y, q), q);
+        const ulonglong2 Pm = pmod[l];
+        return add_mod(acc[o], mul_shoup(d[o], Pm.x, Pm.y, q), q);
+    }
+    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre y, uint64_t v) const {
+        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 w = mqinv[l];
         out[o] = mul_shoup(sub_mod(y, v, q), w.x, w.y, q);
+    }
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        fin(l, P, idx, prep(l, P, idx), v);
     }
 };
 
