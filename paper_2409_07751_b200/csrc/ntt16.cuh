@@ -122,9 +122,25 @@ __device__ __forceinline__ double ld_inter(const double *p) {
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// The shared 256-entry twiddle table is stored bank-conflict-free for the
+// second half of each phase: stage s >= 5 reads entry 2^s + k 2^(s-4) + j in
+// lane group k (16 row/column groups, j < 2^(s-4)), which in natural order puts
+// the 16 lanes 2^(s-4) entries (>= 32 B) apart — an 8-way (s = 7) conflict per
+// LDS.128 that kept the L1 data pipe at 93% (profiles/r2_ntt_notes.md). Stored
+// at 2^s + 16 j + k instead, the 16 lanes read 16 consecutive entries.
+__device__ __forceinline__ int tw_pos(int i) {  // storage slot of table entry i
+    const int s = 31 - __clz(i | 1);
+    if (s < 5) return i;
+    const int m = i - (1 << s), sh = s - 4;
+    return (1 << s) + ((m & ((1 << sh) - 1)) << 4) + (m >> sh);
+}
+// slot read by lane group k for element v (< 16) at stage s of a phase half
+__device__ __forceinline__ int tw_idx(int s, int k, int v) {
+    return s < 5 ? (1 << s) + ((16 * k + v) >> (8 - s)) : (1 << s) + ((v >> (8 - s)) << 4) + k;
+}
 // stage the shared 256-entry twiddle table of prime mi into shared memory
 __device__ __forceinline__ void stage_table(double2 *st, const double2 *__restrict__ T) {
-    for (int i = threadIdx.x; i < 256; i += kTh) st[i] = T[i];
+    for (int i = threadIdx.x; i < 256; i += kTh) st[tw_pos(i)] = T[i];
 }
 
 // ---------------------------------------------------------------- forward
@@ -159,7 +175,7 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m);
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m);
     }
 #pragma unroll
     // no recentre for small primes: |x| < 13 q < 2^51 and the row phase starts with the
@@ -213,7 +229,7 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
         const int d = 128 >> sp;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], st[(1 << sp) + ((16 * k + v) >> (8 - sp))], m);
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m);
     }
     __syncwarp();
     uint64_t *su = reinterpret_cast<uint64_t *>(srow);
@@ -302,7 +318,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 128 >> sp;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[(1 << sp) + ((16 * k + v) >> (8 - sp))], m, !(sp & 1));
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m, !(sp & 1));
     }
     __syncwarp();
 #pragma unroll
@@ -347,7 +363,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[(1 << s) + ((16 * k + v) >> (8 - s))], m, !(s & 1));
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, !(s & 1));
     }
 #pragma unroll
     for (int v = 0; v < 16; ++v) sm[(16 * k + v) * kTc + c] = x[v];
