@@ -336,18 +336,38 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
     }
 }
 
+// Relinearisation fold: the merged ModDown + rescale divides Y_p = acc_p + P d_p
+// by P q_l, so the key inner product writes Y_p directly for the q limbs
+// (t <= l): d_p is formed here from the operands (d0 = a0 b0, d1 = a0 b1 +
+// a1 b0, plus a second product for hk_mul2 and k x_p for hk_mul_lin) on the
+// FP64 pipe, in a streaming kernel whose loads are all in flight together,
+// instead of inside the ModDown NTT's epilogue (where they were latency bound
+// at 2.3x the time of a plain NTT, profiles/r2_notes.md).
+struct FoldD {
+    const uint64_t *a, *b, *a2, *b2, *x;  // x: linear term (optional), a2 / b2: second product (optional)
+    long long pa, pb, pa2, pb2, px;       // offsets of poly 1
+    const ulonglong2 *pmod;               // [n_q] P mod q (Shoup pair; .x used)
+    Residues k;                           // linear-term constant per limb
+};
+__device__ __forceinline__ double fold_prod(const uint64_t *a, const uint64_t *b, long long oa, long long ob,
+                                            const ntt16::FpMod &M) {
+    using namespace ntt16;
+    const double y = u2d(b[ob]);
+    return f_mulmod(u2d(a[oa]), y, __dmul_rn(y, M.qinv), M.q);
+}
+
 // acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j[p][chain(t)] ; grid (BN/256, ne)
 // acc_p[t] = sum_j sigma_g(ext_j[t]) * key_j,p[t]  (p = 0, 1) on the FP64 pipe:
 // exact two-product Shoup (ntt16::f_mulmod) with w/q formed once per thread;
 // each thread owns one (coefficient k, limb t) and walks `bb` batch entries so
 // the key pair, the galois index and the address math are paid once.
 // grid (N/min(N,256) * B/bb, ne); every residue is exact, results canonical.
-template <int ND>
+template <int ND, bool FOLD>
 __global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
                                                 const uint64_t *__restrict__ dm, int alpha, int ne, int l, int n_q,
                                                 int nm, int ksp0, int log_n, int bb, const uint64_t *__restrict__ key,
                                                 uint32_t g, uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1,
-                                                const double2 *__restrict__ fmod, long long BN, int accum) {
+                                                const double2 *__restrict__ fmod, long long BN, int accum, FoldD fd) {
     using namespace ntt16;
     const int N = 1 << log_n;
     const int kblocks = N / (int)blockDim.x;
@@ -392,6 +412,25 @@ __global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext
         }
         // accum: add onto the running sum of earlier key switches (hk_rotate_sum)
         double s0 = accum ? u2d(*o0) : 0.0, s1 = accum ? u2d(*o1) : 0.0;
+        if (FOLD && t <= l) {  // Y_p = acc_p + P d_p (g = 1: ks = k)
+            const long long o = (long long)t * BN + row + (long long)b * N + k;
+            double d0 = fold_prod(fd.a, fd.b, o, o, M);
+            double d1 = __dadd_rn(fold_prod(fd.a, fd.b, o, fd.pb + o, M), fold_prod(fd.a, fd.b, fd.pa + o, o, M));
+            if (fd.a2) {
+                d0 = __dadd_rn(d0, fold_prod(fd.a2, fd.b2, o, o, M));
+                d1 = f_center(d1, M);
+                d1 = __dadd_rn(d1, __dadd_rn(fold_prod(fd.a2, fd.b2, o, fd.pb2 + o, M),
+                                             fold_prod(fd.a2, fd.b2, fd.pa2 + o, o, M)));
+            }
+            if (fd.x) {
+                const double kk = u2d(fd.k.v[t]), kq = __dmul_rn(kk, M.qinv);
+                d0 = __dadd_rn(f_center(d0, M), f_mulmod(u2d(fd.x[o]), kk, kq, M.q));
+                d1 = __dadd_rn(f_center(d1, M), f_mulmod(u2d(fd.x[fd.px + o]), kk, kq, M.q));
+            }
+            const double pm = u2d(fd.pmod[t].x), pq = __dmul_rn(pm, M.qinv);
+            s0 = f_center(__dadd_rn(s0, f_mulmod(f_center(d0, M), pm, pq, M.q)), M);
+            s1 = f_center(__dadd_rn(s1, f_mulmod(f_center(d1, M), pm, pq, M.q)), M);
+        }
 #pragma unroll
         for (int j = 0; j < ND; ++j) {  // |f_mulmod| < 2.5 q: recentre every second term
             s0 = __dadd_rn(s0, f_mulmod(x[j], w0[j], v0[j], M.q));
@@ -797,6 +836,42 @@ struct EpiMdRsT2 {
         fin(l, P, idx, prep(l, P, idx), v);
     }
 };
+// Folded relinearisation (FoldD): acc_p already holds Y_p = acc_p + P d_p on
+// the q limbs, so the q_l source of the merged ModDown + rescale is acc_p[l]
+// and its epilogue reads one operand.
+struct ProAccL2 {
+    const uint64_t *acc;
+    long long BN, pne;
+    int l, log_n;
+    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
+        return acc[(P & 1) * pne + (long long)l * BN + ((P >> 1) << log_n) + idx];
+    }
+};
+struct EpiMdRsY2 {  // out_p = aff((Y_p - v) (P q_l)^-1)
+    const uint64_t *acc;
+    uint64_t *out;
+    const ulonglong2 *mqinv;
+    const ModQ *mq;
+    int B, log_n;
+    long long BN, pne, pout;
+    Affine aff;
+    using Pre = uint64_t;
+    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
+        const long long pb = P - (long long)l * 2 * B;
+        return acc[(pb & 1) * pne + (long long)l * BN + ((pb >> 1) << log_n) + idx];
+    }
+    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre y, uint64_t v) const {
+        const long long pb = P - (long long)l * 2 * B;
+        const int p = (int)(pb & 1);
+        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
+        const uint64_t q = mq[l].q;
+        const ulonglong2 w = mqinv[l];
+        out[p * pout + o] = aff.apply(p, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
+    }
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
+        fin(l, P, idx, prep(l, P, idx), v);
+    }
+};
 // ModDown of both halves of a key switch (interleaved samples 2 b + p):
 // out_p = (acc_p - v) P^-1 (+ sigma_g(add_p))
 struct EpiModDown2 {
@@ -1061,7 +1136,10 @@ struct KeyRef {
 };
 
 static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, KeyRef key, uint32_t g,
-                 const uint64_t *dm = nullptr, int accum = 0) {
+                 const uint64_t *dm = nullptr, int accum = 0, const FoldD *fold = nullptr) {
+    FoldD fd;
+    memset(&fd, 0, sizeof fd);
+    if (fold) fd = *fold;
     const int ne = l + 1 + c->n_p, nd = l / c->alpha + 1;
     if (key.level < l) return hk_fail(c, HK_E_NOKEY, "key for element %u serves level %d < %d", g, key.level, l);
     const int krows = key.level + 1 + c->n_p;
@@ -1070,9 +1148,14 @@ static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, K
     const int ipt = std::min(256, c->n);
     const dim3 ipg((unsigned)((c->n / ipt) * (B / bb)), (unsigned)ne);
 #define HK_KEY_IP(ND)                                                                                          \
-    k_key_ip<ND><<<ipg, ipt, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, krows, key.level + 1,     \
-                                             c->log_n, bb, key.p, g, kb.acc, kb.acc + (size_t)ne * BN, c->d_fmod, BN, \
-                                             accum)
+    if (fold)                                                                                                  \
+        k_key_ip<ND, true><<<ipg, ipt, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, krows,          \
+                                                       key.level + 1, c->log_n, bb, key.p, g, kb.acc,          \
+                                                       kb.acc + (size_t)ne * BN, c->d_fmod, BN, accum, fd);    \
+    else                                                                                                       \
+        k_key_ip<ND, false><<<ipg, ipt, 0, c->stream>>>(kb.ext, d, dm, c->alpha, ne, l, c->n_q, krows,         \
+                                                        key.level + 1, c->log_n, bb, key.p, g, kb.acc,         \
+                                                        kb.acc + (size_t)ne * BN, c->d_fmod, BN, accum, fd)
     switch (nd) {
         case 1: HK_KEY_IP(1); break;
         case 2: HK_KEY_IP(2); break;
@@ -1214,15 +1297,30 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
         if (d1 < l + 1 && (rc = ntt_fwd_launch(c, ej + (size_t)d1 * BN, d1, l + 1 - d1, B, 0))) return rc;
         if ((rc = ntt_fwd_launch(c, ej + (size_t)(l + 1) * BN, c->n_q, np, B, 0))) return rc;
     }
+    // the key IP writes Y_p = acc_p + P d_p on the q limbs (d_p from the operands)
+    FoldD fold;
+    memset(&fold, 0, sizeof fold);
+    fold.a = a;
+    fold.b = b;
+    fold.pa = T.pa;
+    fold.pb = T.pb;
+    fold.a2 = T.a2;
+    fold.b2 = T.b2;
+    fold.pa2 = T.pa2;
+    fold.pb2 = T.pb2;
+    fold.x = lin.x;
+    fold.px = lin.px;
+    fold.k = lin.k;
+    fold.pmod = c->d_pmod;
     if (pair2) {
         // two products: the key IP reads the own-digit limbs of d2 = a1 b1 + a2_1 b2_1
         // from a materialised copy (limbs 0..l, NTT form)
         k_d2_sum<<<egrid(BN, l + 1, 1), 256, 0, c->stream>>>(T, d2buf, BN);
         ++c->launches;
         HK_LAUNCH_CHECK(c, "d2 of two products");
-        if ((rc = ks_ip(c, d2buf, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u))) return rc;
+        if ((rc = ks_ip(c, d2buf, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u, nullptr, 0, &fold))) return rc;
     } else if ((rc = ks_ip(c, a + (size_t)(la + 1) * BN, l, B, kb, KeyRef{c->d_relin, c->n_q - 1}, 1u,
-                           b + (size_t)(lb + 1) * BN))) {
+                           b + (size_t)(lb + 1) * BN, 0, &fold))) {
         // own-digit limbs of d2 are formed inside the key IP from a1 (.) b1
         return rc;
     }
@@ -1233,11 +1331,11 @@ static int mul_fused(hk_ctx *c, const uint64_t *a, int la, const uint64_t *b, in
     EpiScale es{kb.sp, Tm.d_inv, Tm.d_inv_sh, c->d_modq, c->n_q, c->log_n};
     if ((rc = ntt16::launch_inv(c, kb.sp, c->n_q, np, 2 * B, ProAccSp2{kb.acc, BN, pne, l, B, c->log_n}, es)))
         return rc;
-    ProMdYT2 py{kb.acc, T, BN, pne, l, c->log_n, c->d_pmod, c->d_modq, lin};
+    ProAccL2 py{kb.acc, BN, pne, l, c->log_n};
     EpiScale es2{kb.sp + (size_t)np * 2 * BN, Tm.d_inv + np, Tm.d_inv_sh + np, c->d_modq, l, c->log_n};
     if ((rc = ntt16::launch_inv(c, kb.sp + (size_t)np * 2 * BN, l, 1, 2 * B, py, es2))) return rc;
     if ((rc = conv_launch(c, Tm, kb.sp, kb.conv, 1, l, 2 * BN, l, 1))) return rc;
-    EpiMdRsT2 epi{kb.acc, T, out, c->d_pmod, mqinv, c->d_modq, B, c->log_n, BN, pne, (long long)l * BN, lin, aff};
+    EpiMdRsY2 epi{kb.acc, out, mqinv, c->d_modq, B, c->log_n, BN, pne, (long long)l * BN, aff};
     if ((rc = ntt16::launch_fwd(c, kb.conv, 0, l, 2 * B, ntt16::ProPlain{kb.conv, c->log_n}, epi))) return rc;
     return HK_OK;
 }
