@@ -13,8 +13,9 @@ Outputs
                            taken at slot_count 65536 (N = 2^17)
   tests/golden/small.npz   small multi-layer random models + inputs + outputs
   tests/golden/backend.json known-answer vectors of the backend contract
+  tests/golden/counts.json  per-layer op counts of the reference program for c3 / c4
 
-Run:  python tests/golden/make_golden.py [c5]
+Run:  python tests/golden/make_golden.py [c5|counts]
 """
 
 import json
@@ -116,10 +117,37 @@ def c5_fixture(cs):
     print("c5 plan depth", plan.total, "counts", counts)
 
 
+def counts_fixture():
+    """Per-layer logical op counts of the reference's own program for c3 and c4
+    (tests/golden/counts.json), run on CleartextBackend at a slot count that
+    holds each config's packing."""
+    out = {}
+    rng = np.random.default_rng(1)
+    X3 = np.clip(rng.normal(0.0, 1.0, (4096, 4)), -2.0, 2.0)
+    m3 = build_ref_model((4, 8, 4, 1), 10, 3, -2.0, 2.0, 0.1, 63, X3, (1, 1, 4))
+    rng = np.random.default_rng(1)
+    X4 = rng.uniform(0.0, 1.0, (64, 784))
+    m4 = build_ref_model((784, 64, 10), 5, 3, -1.0, 1.0, 0.05, 10, X4, (28, 28, 1), explicit_R=True)
+    for name, model, slots in (("c3", m3, 4096), ("c4", m4, 2 ** 15)):
+        plan = ri.plan_model(model, ri.PipelineConfig())
+        be = CleartextBackend(BackendConfig(slot_count=slots, depth_budget=plan.total))
+        _, stats = ri.model_forward_he(model, ri.encrypt_input(np.zeros(model.n_in), model, be),
+                                       ri.PipelineConfig())
+        out[name] = [{"rotations": s.rotations, "ct_mults": s.ct_mults, "pt_mults": s.pt_mults,
+                      "adds": s.adds, "depth_consumed": s.depth_consumed} for s in stats.per_layer]
+    with open(os.path.join(HERE, "counts.json"), "w") as fh:
+        json.dump({"source": "hekan.inference.model_forward_he on CleartextBackend (tests/golden/make_golden.py counts)",
+                   **out}, fh, indent=1)
+    print(out)
+
+
 def main():
     cs = comparator_json()
     if sys.argv[1:] == ["c5"]:
         c5_fixture(cs)
+        return
+    if sys.argv[1:] == ["counts"]:
+        counts_fixture()
         return
     # ---- c1
     rng = np.random.default_rng(1)

@@ -224,3 +224,22 @@ def test_c4_model_matches_reference_ranges():
     cs = build_composite_sign()
     mine = np.stack([mdl.model_forward_plain(model, x, "mirrored", cs, "lazy") for x in X[:1]])
     assert np.array_equal(mine, g["mirrored"][:1])
+
+
+def test_c3_counts_vs_reference():
+    """c3's per-layer op counts against the reference program's (golden
+    counts.json, made by running hekan). Rotations, ct-mults and depth are
+    identical; the Chebyshev evaluators add exactly: +32 adds (comparator
+    powers T_2k = 2 T_k^2 - 1, two adds each), +10 adds (degree-63 SiLU powers)
+    and +1 pt-mult / +1 add (the SiLU's affine map onto [-1, 1])."""
+    ref = json.load(open(os.path.join(GOLD, "counts.json")))["c3"]
+    _, model, X = configs.workload("c3", batch=1)
+    depth = inf.plan_model(model, inf.PipelineConfig()).total
+    be = oracle_backend(depth, log_n=9)
+    out, stats = inf.model_forward_he(model, inf.encrypt_input(X, model, be), inf.PipelineConfig())
+    assert out.level == 0
+    for mine, theirs in zip(stats.per_layer, ref):
+        assert (mine.rotations, mine.ct_mults, mine.depth_consumed) == (
+            theirs["rotations"], theirs["ct_mults"], theirs["depth_consumed"])
+        assert mine.pt_mults == theirs["pt_mults"] + 1
+        assert mine.adds == theirs["adds"] + 32 + 10 + 1
