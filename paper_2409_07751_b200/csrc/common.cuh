@@ -187,6 +187,9 @@ struct ConvTable {
     // ModDown, merged ModDown + rescale); nullptr = plain fast conversion
     double *d_src_invd;   // [n_src]  1 / m_i
     uint64_t *d_neg_m;    // [n_dst]  -M mod q_t
+    // tensor-core path (conv_tc.cu, n_src <= 16): B[(t, d)][(i, a)] = byte (d - a) of
+    // hat[t][i], 16 rows per target, 128 bytes per row, canonical no-swizzle UMMA layout
+    uint8_t *d_bmat;
 };
 
 // A key-switching key truncated to `level`: digits 0..level/alpha, rows
@@ -203,6 +206,7 @@ struct GalKey {
 struct hk_ctx {
     int log_n, n, slots, n_q, n_p, dnum, alpha, n_digits, n_mod;
     int device;
+    int n_sm;  // multiprocessors of the device (resident-grid sizing)
     cudaStream_t stream;
     std::vector<uint64_t> mod_h;
     std::vector<ModQ> modq_h;
@@ -266,6 +270,9 @@ void *hk_workspace(hk_ctx *c, size_t bytes);
 int ntt_fwd_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int batch, int limb_stride_polys);
 int ntt_inv_launch(hk_ctx *c, uint64_t *buf, int limb0, int n_limbs, int batch, int limb_stride_polys);
 int rescale_launch(hk_ctx *c, const uint64_t *in, int l, int batch, uint64_t *out, uint64_t *scratch);
+bool conv_tc_ok(const hk_ctx *c, const ConvTable &T, int n_dst, long long BN, int prescaled);
+int conv_tc_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l, long long BN,
+                   int n_dst);
 int keyswitch_launch(hk_ctx *c, const uint64_t *d, int l, int batch, const uint64_t *const *keys,
                      const uint32_t *galois, int n_keys, uint64_t *const *outs_c0,
                      const uint64_t *c0_src, bool add_c0_auto);

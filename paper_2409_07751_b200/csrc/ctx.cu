@@ -105,6 +105,22 @@ static ConvTable make_conv(const std::vector<uint64_t> &mod, const std::vector<i
     t.d_dst_mod = upload(std::vector<int32_t>(dst.begin(), dst.end()));
     t.d_src_invd = nullptr;
     t.d_neg_m = nullptr;
+    t.d_bmat = nullptr;
+    if (src.size() <= 16) {  // conv_tc.cu: bytes of hat in the no-swizzle K-major UMMA layout
+        std::vector<uint8_t> b(dst.size() * 16 * 128, 0);
+        for (size_t d = 0; d < dst.size(); ++d)
+            for (size_t i = 0; i < src.size(); ++i) {
+                const uint64_t h = hat[d * src.size() + i];
+                for (int diag = 0; diag < 16; ++diag)
+                    for (int a = 0; a < 8; ++a) {
+                        const int bb = diag - a;
+                        if (bb < 0 || bb > 7) continue;
+                        const size_t n = d * 16 + diag, kk = i * 8 + a;
+                        b[(n / 8) * 1024 + (kk / 16) * 128 + (n % 8) * 16 + kk % 16] = (uint8_t)(h >> (8 * bb));
+                    }
+            }
+        t.d_bmat = upload(b);
+    }
     if (exact) {  // centred conversion: 1/m_i as float64, -M mod q_t (M = product of the sources)
         std::vector<double> invd(src.size());
         for (size_t i = 0; i < src.size(); ++i) invd[i] = 1.0 / (double)mod[src[i]];
@@ -129,6 +145,7 @@ static void free_conv(ConvTable &t) {
     cudaFree(t.d_dst_mod);
     cudaFree(t.d_src_invd);
     cudaFree(t.d_neg_m);
+    cudaFree(t.d_bmat);
 }
 
 extern "C" {
@@ -154,6 +171,8 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     if (cudaSetDevice(device) != cudaSuccess) return HK_E_CUDA;
     hk_ctx *c = new hk_ctx();
     c->device = device;
+    c->n_sm = 148;
+    cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
     c->stream = 0;
     c->log_n = pr->log_n;
     c->n = 1 << pr->log_n;

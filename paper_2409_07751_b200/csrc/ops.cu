@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
     __syncthreads();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= BN) return;
+    {
     // Karatsuba split MAC: s0 = sum x0 y0, s2 = sum x1 y1, sm = sum (x0+x1)(y0+y1),
     // s1 = sm - s0 - s2 (once per target): three IMAD.WIDE per multiply-add.
     uint32_t v0[NS], v1[NS], vs[NS];
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(128) k_conv(const uint64_t *__restrict__ src, 
         Acc3 A{a0, am - a0 - a2, a2};
         if (neg_m) A.s0 += u * __ldg(neg_m + d);
         dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
+    }
     }
 }
 
@@ -991,6 +993,7 @@ static dim3 egrid(long long BN, int limbs, int polys) {
 static int conv_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l,
                        long long BN, int n_dst = -1, int prescaled = 0) {
     if (n_dst < 0) n_dst = T.n_dst;
+    if (conv_tc_ok(c, T, n_dst, BN, prescaled)) return conv_tc_launch(c, T, src, dst, mode, l, BN, n_dst);
     const size_t smem =
         sizeof(uint32_t) * (size_t)n_dst * ((3 * T.n_src + 3) & ~3) + sizeof(ModQ) * n_dst + sizeof(int) * n_dst;
     const dim3 grid((unsigned)((BN + 127) / 128));
@@ -1144,7 +1147,10 @@ static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, K
     if (key.level < l) return hk_fail(c, HK_E_NOKEY, "key for element %u serves level %d < %d", g, key.level, l);
     const int krows = key.level + 1 + c->n_p;
     const long long BN = (long long)B * c->n;
-    const int bb = B % 4 == 0 ? 4 : B % 2 == 0 ? 2 : 1;
+    // samples per thread: each key pair is read once per bb samples (bb = 1 / 2 /
+    // 4: 24.3 / 25.1 / 25.5 c1 inf/s, profiles/r2_notes.md)
+    static const int bb_max = getenv("HK_KEYIP_BB") ? atoi(getenv("HK_KEYIP_BB")) : 4;  // A/B knob
+    const int bb = B % 8 == 0 && bb_max >= 8 ? 8 : B % 4 == 0 && bb_max >= 4 ? 4 : B % 2 == 0 && bb_max >= 2 ? 2 : 1;
     const int ipt = std::min(256, c->n);
     const dim3 ipg((unsigned)((c->n / ipt) * (B / bb)), (unsigned)ne);
 #define HK_KEY_IP(ND)                                                                                          \
