@@ -41,7 +41,6 @@ constexpr int kTileM = 128;      // coefficients per tile (TMEM lanes)
 constexpr int kKBytes = 128;     // 16 source slots x 8 bytes
 constexpr int kRowsPerTarget = 16;
 constexpr int kChunkTargets = 16;  // N = 256 per MMA
-constexpr int kThreads = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -98,106 +97,185 @@ __device__ __forceinline__ Acc3 fold_diagonals(const uint32_t (&C)[16]) {
     return a;
 }
 
-// grid: persistent CTAs over tiles of 128 coefficients; all n_dst targets per tile
-__global__ void __launch_bounds__(kThreads, 1)
+// mbarrier helpers
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// Warp-specialised persistent kernel, one CTA per SM, 13 warps:
+//   warps 0-3   producers: A tile (the source words of 128 coefficients) and the
+//               overflow counts u, double-buffered;
+//   warp 4      MMA issuer (one lane): per 16-target chunk, ksteps MMAs into one
+//               of two 256-column TMEM accumulators;
+//   warps 5-12  epilogue: two warps per TMEM lane quarter (warp % 4), each taking
+//               8 of a chunk's 16 targets.
+// mbarriers: a_full / a_empty / u_empty per A buffer, t_full / t_empty per
+// TMEM buffer; "empty" waits start on parity 1 (the virtual previous phase).
+constexpr int kProducers = 4, kMmaWarp = 4, kEpiWarp0 = 5, kEpiWarps = 8;
+constexpr int kThreadsWs = (kEpiWarp0 + kEpiWarps) * 32;
+
+__global__ void __launch_bounds__(kThreadsWs, 1)
     k_conv_tc(const uint64_t *__restrict__ src, int n_src, const uint8_t *__restrict__ bmat,
               const int32_t *__restrict__ dst_mod, int n_dst, uint64_t *__restrict__ dst, int mode, int l, int n_q,
               long long BN, const ModQ *__restrict__ mq, const double *__restrict__ src_invd,
               const uint64_t *__restrict__ neg_m) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sa = smem;                                             // A: 128 x 128 bytes
-    uint8_t *sb = smem + kTileM * kKBytes;                          // B: 16 n_dst x 128 bytes
+    uint8_t *sa = smem;                                              // A: 2 x 128 x 128 bytes
+    uint8_t *sb = smem + 2 * kTileM * kKBytes;                       // B: 16 n_dst x 128 bytes
     const int b_bytes = n_dst * kRowsPerTarget * kKBytes;
-    uint64_t *su = reinterpret_cast<uint64_t *>(sb + b_bytes);     // u per row [128]
-    ModQ *smq = reinterpret_cast<ModQ *>(su + kTileM);              // [n_dst]
-    int *sidx = reinterpret_cast<int *>(smq + n_dst);               // [n_dst]
-    uint64_t *snm = reinterpret_cast<uint64_t *>(sidx + ((n_dst + 1) & ~1));  // [n_dst]
-    __shared__ __align__(8) uint64_t mbar;
+    uint64_t *su = reinterpret_cast<uint64_t *>(sb + b_bytes);      // u: 2 x 128
+    ModQ *smq = reinterpret_cast<ModQ *>(su + 2 * kTileM);           // [n_dst]
+    uint64_t *snm = reinterpret_cast<uint64_t *>(smq + n_dst);       // [n_dst]
+    int *sidx = reinterpret_cast<int *>(snm + n_dst);                // [n_dst]
+    __shared__ __align__(8) uint64_t bars[10];  // a_full[2] a_empty[2] u_empty[2] t_full[2] t_empty[2]
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // stage B (constant for the launch) and the target tables
     {
         const uint4 *g = reinterpret_cast<const uint4 *>(bmat);
         uint4 *s = reinterpret_cast<uint4 *>(sb);
-        for (int i = tid; i < b_bytes / 16; i += kThreads) s[i] = g[i];
-        for (int d = tid; d < n_dst; d += kThreads) {
+        for (int i = tid; i < b_bytes / 16; i += kThreadsWs) s[i] = g[i];
+        for (int d = tid; d < n_dst; d += kThreadsWs) {
             const int m = dst_mod[d];
             smq[d] = mq[m];
             sidx[d] = mode == 0 ? (m <= l ? m : l + 1 + m - n_q) : d;
             snm[d] = neg_m ? neg_m[d] : 0;
         }
     }
-    if (warp == 0) {  // TMEM: 256 columns (one 16-target chunk of int32 accumulators)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_s)));
+    const uint32_t bar0 = smem_u32(&bars[0]);
+    auto A_FULL = [&](int s) { return bar0 + 8u * (0 + s); };
+    auto A_EMPTY = [&](int s) { return bar0 + 8u * (2 + s); };
+    auto U_EMPTY = [&](int s) { return bar0 + 8u * (4 + s); };
+    auto T_FULL = [&](int s) { return bar0 + 8u * (6 + s); };
+    auto T_EMPTY = [&](int s) { return bar0 + 8u * (8 + s); };
+    if (warp == kMmaWarp) {  // TMEM: two 256-column int32 accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(A_FULL(s), kProducers);
+            mbar_init(A_EMPTY(s), 1);
+            mbar_init(U_EMPTY(s), kEpiWarps);
+            mbar_init(T_FULL(s), 1);
+            mbar_init(T_EMPTY(s), kEpiWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B visible to the tensor core
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base_s;
-    const uint32_t bar = smem_u32(&mbar);
-    uint32_t phase = 0;
     const int ksteps = (n_src + 3) >> 2;  // 4 source slots (32 bytes) per MMA
+    const int n_chunks = (n_dst + kChunkTargets - 1) / kChunkTargets;
     const long long tiles = BN / kTileM;
 
-    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const long long e0 = tile * kTileM;
-        if (tid < kTileM) {  // A rows: the source words' bytes; u = round(sum v_i / m_i)
-            const int r = tid;
-            uint8_t *row = sa + (r >> 3) * 1024 + (r & 7) * 16;
+    if (warp < kProducers) {
+        // ---------------------------------------------------------- producers
+        const int r = tid;
+        int i = 0;
+        for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+            const int s = i & 1, par = ((i >> 1) & 1) ^ 1;
+            mbar_wait(A_EMPTY(s), par);
+            mbar_wait(U_EMPTY(s), par);
+            const long long e0 = tile * kTileM;
+            uint8_t *row = sa + s * (kTileM * kKBytes) + (r >> 3) * 1024 + (r & 7) * 16;
+            uint64_t v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = j < n_src ? src[(long long)j * BN + e0 + r] : 0;
             double frac = 0.0;
-#pragma unroll 4
-            for (int c = 0; c < 8; ++c) {
-                uint64_t v0 = 0, v1 = 0;
-                if (2 * c < n_src) v0 = src[(long long)(2 * c) * BN + e0 + r];
-                if (2 * c + 1 < n_src) v1 = src[(long long)(2 * c + 1) * BN + e0 + r];
-                if (neg_m) {
-                    if (2 * c < n_src) frac = __dadd_rn(frac, __dmul_rn(ntt16::u2d(v0), src_invd[2 * c]));
-                    if (2 * c + 1 < n_src) frac = __dadd_rn(frac, __dmul_rn(ntt16::u2d(v1), src_invd[2 * c + 1]));
-                }
-                *reinterpret_cast<uint4 *>(row + c * 128) =
-                    make_uint4((uint32_t)v0, (uint32_t)(v0 >> 32), (uint32_t)v1, (uint32_t)(v1 >> 32));
+            if (neg_m) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (j < n_src) frac = __dadd_rn(frac, __dmul_rn(ntt16::u2d(v[j]), src_invd[j]));
             }
-            su[r] = neg_m ? (uint64_t)floor(__dadd_rn(frac, 0.5)) : 0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4 *>(row + c * 128) = make_uint4(
+                    (uint32_t)v[2 * c], (uint32_t)(v[2 * c] >> 32), (uint32_t)v[2 * c + 1], (uint32_t)(v[2 * c + 1] >> 32));
+            su[s * kTileM + r] = neg_m ? (uint64_t)floor(__dadd_rn(frac, 0.5)) : 0;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A visible to the tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(A_FULL(s));
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A visible to the tensor core
-        __syncthreads();
-        const int row = (warp & 3) * 32 + lane;  // TMEM lane quarter of this warp = coefficient
-        const uint64_t u = su[row];
-        for (int t0 = 0; t0 < n_dst; t0 += kChunkTargets) {
-            const int nt = min(kChunkTargets, n_dst - t0);
-            if (tid == 0) {
+    } else if (warp == kMmaWarp) {
+        // ---------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            int i = 0, g = 0;
+            for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+                const int s = i & 1;
+                mbar_wait(A_FULL(s), (i >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t idesc = umma_idesc(nt * kRowsPerTarget);
-                const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb + t0 * kRowsPerTarget * kKBytes);
-                for (int k = 0; k < ksteps; ++k)
-                    mma_i8(tmem, umma_desc(a0 + k * 256), umma_desc(b0 + k * 256), idesc, k);
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar));
+                const uint32_t a0 = smem_u32(sa + s * (kTileM * kKBytes));
+                for (int ch = 0; ch < n_chunks; ++ch, ++g) {
+                    const int tb = g & 1;
+                    mbar_wait(T_EMPTY(tb), ((g >> 1) & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const int t0 = ch * kChunkTargets, nt = min(kChunkTargets, n_dst - t0);
+                    const uint32_t idesc = umma_idesc(nt * kRowsPerTarget);
+                    const uint32_t b0 = smem_u32(sb + t0 * kRowsPerTarget * kKBytes);
+                    for (int k = 0; k < ksteps; ++k)
+                        mma_i8(tmem + tb * 256, umma_desc(a0 + k * 256), umma_desc(b0 + k * 256), idesc, k);
+                    umma_commit(T_FULL(tb));
+                }
+                umma_commit(A_EMPTY(s));  // every MMA reading this A buffer has completed
             }
-            mbar_wait(bar, phase);
-            phase ^= 1;
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            // warps 0-3: targets 0..7 of the chunk, warps 4-7: targets 8..15
-            const int tb = (warp >> 2) * 8;
-            for (int tt = tb; tt < min(tb + 8, nt); ++tt) {
-                uint32_t C[16];
-                tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(tt * kRowsPerTarget), C);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int d = t0 + tt;
-                Acc3 A = fold_diagonals(C);
-                A.s0 += u * snm[d];
-                dst[(long long)sidx[d] * BN + e0 + row] = acc3_reduce(A, smq[d]);
+        }
+    } else {
+        // ---------------------------------------------------------- epilogue
+        const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
+        const int row = q * 32 + lane;
+        int i = 0, g = 0;
+        for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+            const int s = i & 1;
+            mbar_wait(A_FULL(s), (i >> 1) & 1);  // u of this tile is written
+            const uint64_t u = su[s * kTileM + row];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(U_EMPTY(s));
+            const long long e = tile * kTileM + row;
+            for (int ch = 0; ch < n_chunks; ++ch, ++g) {
+                const int tb = g & 1;
+                mbar_wait(T_FULL(tb), (g >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const int t0 = ch * kChunkTargets, nt = min(kChunkTargets, n_dst - t0);
+                const uint32_t tq = tmem + tb * 256 + ((uint32_t)(q * 32) << 16);
+                for (int tt = half * 8; tt < min(half * 8 + 8, nt); tt += 2) {
+                    uint32_t C0[16], C1[16];
+                    tmem_ld16(tq + (uint32_t)(tt * kRowsPerTarget), C0);
+                    if (tt + 1 < nt) tmem_ld16(tq + (uint32_t)((tt + 1) * kRowsPerTarget), C1);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    {
+                        const int d = t0 + tt;
+                        Acc3 A = fold_diagonals(C0);
+                        A.s0 += u * snm[d];
+                        dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
+                    }
+                    if (tt + 1 < nt) {
+                        const int d = t0 + tt + 1;
+                        Acc3 A = fold_diagonals(C1);
+                        A.s0 += u * snm[d];
+                        dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(T_EMPTY(tb));
             }
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncthreads();  // TMEM and (after the last chunk) A are free again
         }
     }
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
 }
 
 }  // namespace
@@ -212,7 +290,7 @@ bool conv_tc_ok(const hk_ctx *c, const ConvTable &T, int n_dst, long long BN, in
 
 int conv_tc_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l, long long BN,
                    int n_dst) {
-    const size_t smem = (size_t)kTileM * kKBytes + (size_t)n_dst * kRowsPerTarget * kKBytes + kTileM * 8 +
+    const size_t smem = 2 * (size_t)kTileM * kKBytes + (size_t)n_dst * kRowsPerTarget * kKBytes + 2 * kTileM * 8 +
                         n_dst * (sizeof(ModQ) + 8 + 4) + 64;
     if (smem > 227 * 1024) return hk_fail(c, HK_E_ARG, "conv_tc: %d targets exceed shared memory", n_dst);
     static size_t attr = 0;
@@ -221,9 +299,8 @@ int conv_tc_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t 
         attr = smem;
     }
     const long long tiles = BN / kTileM;
-    const int per_sm = smem <= 100 * 1024 ? 2 : 1;
-    const unsigned grid = (unsigned)std::min<long long>(tiles, (long long)c->n_sm * per_sm);
-    k_conv_tc<<<grid, kThreads, smem, c->stream>>>(src, T.n_src, T.d_bmat, T.d_dst_mod, n_dst, dst, mode, l, c->n_q,
+    const unsigned grid = (unsigned)std::min<long long>(tiles, (long long)c->n_sm);  // one CTA per SM (512 TMEM columns)
+    k_conv_tc<<<grid, kThreadsWs, smem, c->stream>>>(src, T.n_src, T.d_bmat, T.d_dst_mod, n_dst, dst, mode, l, c->n_q,
                                                     BN, c->d_modq, T.d_src_invd, T.d_neg_m);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "basis conversion (tensor cores)");
