@@ -87,14 +87,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-// X = s0 + s1 2^25 + s2 2^50 from the 13 byte-diagonal sums C_d (X = sum C_d 2^(8d))
-__device__ __forceinline__ Acc3 fold_diagonals(const uint32_t (&C)[16]) {
-    Acc3 a;
-    a.s0 = (uint64_t)C[0] + ((uint64_t)C[1] << 8) + ((uint64_t)C[2] << 16) + ((uint64_t)C[3] << 24);
-    a.s1 = ((uint64_t)C[4] << 7) + ((uint64_t)C[5] << 15) + ((uint64_t)C[6] << 23);
-    a.s2 = ((uint64_t)C[7] << 6) + ((uint64_t)C[8] << 14) + ((uint64_t)C[9] << 22) + ((uint64_t)C[10] << 30) +
-           ((uint64_t)C[11] << 38) + ((uint64_t)C[12] << 46);
-    return a;
+// out = (sum_d C_d 2^(8d) + u negM) mod q from the 13 byte-diagonal sums (each C_d
+// < 2^23, the sum < 2^104): three 48-bit partial sums by IMAD.WIDE chains (weights
+// 2^0, 2^32, 2^64), one 128-bit combine, one Barrett step (reduce128: X < 2^(63+k)).
+// The same integer the IMAD kernel's three-limb accumulator holds, so the same result.
+__device__ __forceinline__ uint64_t fold_reduce(const uint32_t (&C)[16], uint32_t u, uint64_t nm, const ModQ &q) {
+    uint64_t lo = mad_wide(C[3], 1u << 24, mad_wide(C[2], 1u << 16, mad_wide(C[1], 1u << 8, C[0])));
+    const uint64_t mid = mad_wide(C[7], 1u << 24, mad_wide(C[6], 1u << 16, mad_wide(C[5], 1u << 8, C[4])));
+    uint64_t hi = mad_wide(C[11], 1u << 24, mad_wide(C[10], 1u << 16, mad_wide(C[9], 1u << 8, C[8]))) +
+                  ((uint64_t)C[12] << 32);
+    const uint64_t m32 = mid << 32;
+    lo += m32;
+    hi += (mid >> 32) + (lo < m32);
+    const uint64_t un = mad_wide(u, (uint32_t)nm, (uint64_t)(u * (uint32_t)(nm >> 32)) << 32);  // u nm < 2^54
+    lo += un;
+    hi += lo < un;
+    return reduce128(hi, lo, q);
 }
 
 // mbarrier helpers
@@ -117,10 +125,10 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 //               8 of a chunk's 16 targets.
 // mbarriers: a_full / a_empty / u_empty per A buffer, t_full / t_empty per
 // TMEM buffer; "empty" waits start on parity 1 (the virtual previous phase).
-constexpr int kProducers = 4, kMmaWarp = 4, kEpiWarp0 = 5, kEpiWarps = 8;
-constexpr int kThreadsWs = (kEpiWarp0 + kEpiWarps) * 32;
+constexpr int kProducers = 4, kMmaWarp = 4, kEpiWarp0 = 5;
 
-__global__ void __launch_bounds__(kThreadsWs, 1)
+template <int kEpiWarps>
+__global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
     k_conv_tc(const uint64_t *__restrict__ src, int n_src, const uint8_t *__restrict__ bmat,
               const int32_t *__restrict__ dst_mod, int n_dst, uint64_t *__restrict__ dst, int mode, int l, int n_q,
               long long BN, const ModQ *__restrict__ mq, const double *__restrict__ src_invd,
@@ -135,6 +143,8 @@ __global__ void __launch_bounds__(kThreadsWs, 1)
     int *sidx = reinterpret_cast<int *>(snm + n_dst);                // [n_dst]
     __shared__ __align__(8) uint64_t bars[10];  // a_full[2] a_empty[2] u_empty[2] t_full[2] t_empty[2]
     __shared__ uint32_t tmem_base_s;
+    constexpr int kThreadsWs = (kEpiWarp0 + kEpiWarps) * 32;
+    constexpr int kPerQuarter = kEpiWarps / 4;  // epilogue warps sharing one TMEM lane quarter
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     {
@@ -230,7 +240,7 @@ __global__ void __launch_bounds__(kThreadsWs, 1)
         }
     } else {
         // ---------------------------------------------------------- epilogue
-        const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
+        const int q = warp & 3, slot = (warp - kEpiWarp0) >> 2;
         const int row = q * 32 + lane;
         int i = 0, g = 0;
         for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
@@ -246,22 +256,20 @@ __global__ void __launch_bounds__(kThreadsWs, 1)
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const int t0 = ch * kChunkTargets, nt = min(kChunkTargets, n_dst - t0);
                 const uint32_t tq = tmem + tb * 256 + ((uint32_t)(q * 32) << 16);
-                for (int tt = half * 8; tt < min(half * 8 + 8, nt); tt += 2) {
+                // this warp's targets of the chunk: slot, slot + kPerQuarter, ... two per TMEM wait
+                for (int tt = slot; tt < nt; tt += 2 * kPerQuarter) {
+                    const bool two = tt + kPerQuarter < nt;
                     uint32_t C0[16], C1[16];
                     tmem_ld16(tq + (uint32_t)(tt * kRowsPerTarget), C0);
-                    if (tt + 1 < nt) tmem_ld16(tq + (uint32_t)((tt + 1) * kRowsPerTarget), C1);
+                    if (two) tmem_ld16(tq + (uint32_t)((tt + kPerQuarter) * kRowsPerTarget), C1);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     {
                         const int d = t0 + tt;
-                        Acc3 A = fold_diagonals(C0);
-                        A.s0 += u * snm[d];
-                        dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
+                        dst[(long long)sidx[d] * BN + e] = fold_reduce(C0, (uint32_t)u, snm[d], smq[d]);
                     }
-                    if (tt + 1 < nt) {
-                        const int d = t0 + tt + 1;
-                        Acc3 A = fold_diagonals(C1);
-                        A.s0 += u * snm[d];
-                        dst[(long long)sidx[d] * BN + e] = acc3_reduce(A, smq[d]);
+                    if (two) {
+                        const int d = t0 + tt + kPerQuarter;
+                        dst[(long long)sidx[d] * BN + e] = fold_reduce(C1, (uint32_t)u, snm[d], smq[d]);
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
@@ -293,15 +301,22 @@ int conv_tc_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t 
     const size_t smem = 2 * (size_t)kTileM * kKBytes + (size_t)n_dst * kRowsPerTarget * kKBytes + 2 * kTileM * 8 +
                         n_dst * (sizeof(ModQ) + 8 + 4) + 64;
     if (smem > 227 * 1024) return hk_fail(c, HK_E_ARG, "conv_tc: %d targets exceed shared memory", n_dst);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    static const int epi = getenv("HK_CONV_EPI") ? atoi(getenv("HK_CONV_EPI")) : 16;  // A/B: 8 / 12 / 16 warps -> 26.8 / 27.3 / 27.3 c1 inf/s
     const long long tiles = BN / kTileM;
     const unsigned grid = (unsigned)std::min<long long>(tiles, (long long)c->n_sm);  // one CTA per SM (512 TMEM columns)
-    k_conv_tc<<<grid, kThreadsWs, smem, c->stream>>>(src, T.n_src, T.d_bmat, T.d_dst_mod, n_dst, dst, mode, l, c->n_q,
-                                                    BN, c->d_modq, T.d_src_invd, T.d_neg_m);
+#define HK_CONV_TC(EW)                                                                                           \
+    {                                                                                                            \
+        static size_t attr = 0;                                                                                  \
+        if (smem > attr) {                                                                                       \
+            cudaFuncSetAttribute(k_conv_tc<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+            attr = smem;                                                                                         \
+        }                                                                                                        \
+        k_conv_tc<EW><<<grid, (kEpiWarp0 + EW) * 32, smem, c->stream>>>(src, T.n_src, T.d_bmat, T.d_dst_mod,     \
+                                                                       n_dst, dst, mode, l, c->n_q, BN,         \
+                                                                       c->d_modq, T.d_src_invd, T.d_neg_m);      \
+    }
+    if (epi == 16) HK_CONV_TC(16) else if (epi == 8) HK_CONV_TC(8) else HK_CONV_TC(12)
+#undef HK_CONV_TC
     ++c->launches;
     HK_LAUNCH_CHECK(c, "basis conversion (tensor cores)");
     return HK_OK;
