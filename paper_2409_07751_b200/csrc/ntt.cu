@@ -5,7 +5,7 @@
 // (0..logN-1) pairs (j, j + N/2^(s+1)) with twiddle psi^brv(2^s + (j >> (logN-s)));
 // inverse = Gentleman-Sande in reverse stage order with psi^-brv, then * N^-1.
 //
-// N = 2^16: the fused cluster kernels of ntt16.cuh (one 16-CTA cluster per
+// N = 2^16: the fused cluster kernels of ntt16.cuh (one 4-CTA cluster per
 // polynomial, 256 x 256 split, intermediate in L2, FP64-pipe butterflies),
 // here with plain in-place prologue/epilogue. N = 2^17: one radix-2 stage +
 // twist pass, then the 2^16 kernels on both halves (below). Other N (parity
