@@ -187,8 +187,9 @@ struct ConvTable {
     // ModDown, merged ModDown + rescale); nullptr = plain fast conversion
     double *d_src_invd;   // [n_src]  1 / m_i
     uint64_t *d_neg_m;    // [n_dst]  -M mod q_t
-    // tensor-core path (conv_tc.cu, n_src <= 16): B[(t, d)][(i, a)] = byte (d - a) of
-    // hat[t][i], 16 rows per target, 128 bytes per row, canonical no-swizzle UMMA layout
+    // tensor-core path (conv_tc.cu, <= 16 source slots): B[(t, b)][(i, a)] = byte b of
+    // hat[t][i] 2^(8a) mod q_t (slot n_src: -M mod q_t), 8 rows per target, 128 bytes per
+    // row, canonical no-swizzle UMMA layout
     uint8_t *d_bmat;
 };
 

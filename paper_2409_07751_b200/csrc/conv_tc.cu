@@ -3,34 +3,51 @@
 // The conversion of key switching (ModUp per digit, ModDown, merged ModDown +
 // rescale) is a contraction over the source limbs:
 //
-//   X[e][t] = sum_i v[i][e] * hat[t][i]      (v < 2^50, hat < 2^50, exact)
-//   out[t][e] = (X + u[e] * (-M mod q_t)) mod q_t
+//   out[t][e] = (sum_i v[i][e] * hat[t][i] + u[e] * (-M mod q_t)) mod q_t
 //
-// Split both operands into bytes, v = sum_a 2^(8a) v_a and hat = sum_b 2^(8b)
-// h_b. Then X = sum_d 2^(8d) C_d with
+// with v < 2^50 the prescaled source residues and u = round(sum_i v_i / m_i)
+// the overflow count of the centred conversion. Only the residue mod q_t
+// matters, so the constants are reduced BEFORE the product: split v into bytes,
+// v = sum_a 2^(8a) v_a, and let
 //
-//   C_d[e][t] = sum_i sum_{a+b=d} v_a[i][e] h_b[t][i],
+//   c[t][i][a] = hat[t][i] * 2^(8a) mod q_t        (< 2^50, 7 bytes c_b)
+//
+// then  out = (sum_b 2^(8b) C_b) mod q_t  with
+//
+//   C_b[e][t] = sum_i sum_a v_a[i][e] * c_b[t][i][a],
 //
 // an unsigned 8-bit GEMM: A[e][(i, a)] are the little-endian bytes of the u64
 // source words themselves (K = 8 bytes x 16 source slots = 128), and
-// B[(t, d)][(i, a)] = byte (d - a) of hat[t][i] (16 rows per target: the 13
-// byte-diagonals d = 0..12 and three zero rows). One tcgen05.mma.kind::i8
-// (M = 128 coefficients, N = 16 x 16 targets, K = 32) per 4 source slots
-// accumulates int32 C in TMEM (every C_d < 2^23); the epilogue reads a
-// coefficient's 16 diagonals of one target with a single tcgen05.ld
-// (32x32b.x16: TMEM lane = coefficient = thread), folds them into the same
-// three-limb integer s0 + s1 2^25 + s2 2^50 the IMAD kernel (ops.cu: k_conv)
-// accumulates, and reduces it with the same Barrett step — so the output is
-// bit-identical to k_conv and to the oracle. The k_conv IMAD formulation
-// spends ~13 instructions per multiply-add on the FMA/ALU pipes (profiles/
-// r2_notes.md); here the products run on the tensor pipe and the CUDA cores
-// only do the ~50-instruction fold-and-reduce per output.
+// B[(t, b)][(i, a)] = byte b of c[t][i][a] (8 rows per target: 7 bytes and a
+// zero row). The overflow term rides in the GEMM too: u is written into the
+// first free source slot and that slot's constant is -M mod q_t. One
+// tcgen05.mma.kind::i8 (M = 128 coefficients, N = 8 x up to 32 targets, K = 32)
+// per 4 source slots accumulates int32 C in TMEM (every C_b < 2^23); the
+// epilogue reads a coefficient's 8 sums of one target with one tcgen05.ld
+// (32x32b.x8: TMEM lane = coefficient = thread), folds them into
+// X = lo + 2^32 hi < 2^72 with five IMAD.WIDE, estimates X / q_t on the FP64 pipe
+// (relative error 2^-51 on a quotient < 2^28: off by at most one) and takes the
+// remainder in 64-bit wrapping arithmetic: the canonical residue, hence
+// bit-identical to the IMAD kernel (ops.cu: k_conv) and to the oracle.
+//
+// Round-2 history: the first tensor-core version multiplied by the raw bytes of
+// hat (13 byte-diagonals per target, 128-bit fold and Barrett step, ~50
+// instructions per output and 16 TMEM columns per target); reducing the
+// constants first halves the TMEM traffic and cuts the CUDA-core work per output
+// to ~20 instructions (profiles/r2_notes.md §7).
 //
 // Layouts (no swizzle, K-major canonical UMMA layout): element (row r, byte k)
 // of an operand lives at (r / 8) * 1024 + (k / 16) * 128 + (r % 8) * 16 + k % 16
 // (8-row x 16-byte core matrices; LBO = 128 B between K-adjacent core matrices,
 // SBO = 1024 B between 8-row groups). B is built on the host in exactly this
-// layout (ctx.cu: ConvTable::d_bmat) and copied linearly into shared memory.
+// layout (ctx.cu: ConvTable::d_bmat, one 1 KiB row group per target) and copied
+// linearly into shared memory.
+//
+// Data movement: the source words of a 128-coefficient tile ([slot][128] u64,
+// 1 KiB contiguous per slot in HBM) arrive by TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx) into a 4-deep ring, issued by one
+// lane several tiles ahead of the consumers; four transform warps turn a raw
+// tile into the UMMA A layout (and compute u), double-buffered against the MMA.
 #include "common.cuh"
 
 #include "ntt16.cuh"
@@ -39,8 +56,10 @@ namespace {
 
 constexpr int kTileM = 128;      // coefficients per tile (TMEM lanes)
 constexpr int kKBytes = 128;     // 16 source slots x 8 bytes
-constexpr int kRowsPerTarget = 16;
-constexpr int kChunkTargets = 16;  // N = 256 per MMA
+constexpr int kRowsPerTarget = 8;
+constexpr int kChunkTargets = 32;  // N <= 256 per MMA
+constexpr int kRawStages = 4;      // TMA ring depth (tiles)
+constexpr int kTileBytes = kTileM * kKBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -68,13 +87,10 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
         "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-        "%14, %15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
@@ -86,62 +102,81 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-
-// out = (sum_d C_d 2^(8d) + u negM) mod q from the 13 byte-diagonal sums (each C_d
-// < 2^23, the sum < 2^104): three 48-bit partial sums by IMAD.WIDE chains (weights
-// 2^0, 2^32, 2^64), one 128-bit combine, one Barrett step (reduce128: X < 2^(63+k)).
-// The same integer the IMAD kernel's three-limb accumulator holds, so the same result.
-__device__ __forceinline__ uint64_t fold_reduce(const uint32_t (&C)[16], uint32_t u, uint64_t nm, const ModQ &q) {
-    uint64_t lo = mad_wide(C[3], 1u << 24, mad_wide(C[2], 1u << 16, mad_wide(C[1], 1u << 8, C[0])));
-    const uint64_t mid = mad_wide(C[7], 1u << 24, mad_wide(C[6], 1u << 16, mad_wide(C[5], 1u << 8, C[4])));
-    uint64_t hi = mad_wide(C[11], 1u << 24, mad_wide(C[10], 1u << 16, mad_wide(C[9], 1u << 8, C[8]))) +
-                  ((uint64_t)C[12] << 32);
-    const uint64_t m32 = mid << 32;
-    lo += m32;
-    hi += (mid >> 32) + (lo < m32);
-    const uint64_t un = mad_wide(u, (uint32_t)nm, (uint64_t)(u * (uint32_t)(nm >> 32)) << 32);  // u nm < 2^54
-    lo += un;
-    hi += lo < un;
-    return reduce128(hi, lo, q);
-}
-
-// mbarrier helpers
 __device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
+// TMA bulk copy global -> shared, completion on an mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
 
-// Warp-specialised persistent kernel, one CTA per SM, 13 warps:
-//   warps 0-3   producers: A tile (the source words of 128 coefficients) and the
-//               overflow counts u, double-buffered;
-//   warp 4      MMA issuer (one lane): per 16-target chunk, ksteps MMAs into one
-//               of two 256-column TMEM accumulators;
-//   warps 5-12  epilogue: two warps per TMEM lane quarter (warp % 4), each taking
-//               8 of a chunk's 16 targets.
-// mbarriers: a_full / a_empty / u_empty per A buffer, t_full / t_empty per
-// TMEM buffer; "empty" waits start on parity 1 (the virtual previous phase).
-constexpr int kProducers = 4, kMmaWarp = 4, kEpiWarp0 = 5;
+// Power-of-two multipliers of the fold, kept opaque to ptxas (a literal is strength-
+// reduced into shift / funnel-shift / carry sequences, 2-3 instructions per term
+// instead of one IMAD.WIDE with a constant-bank operand).
+__constant__ uint32_t kPow2[3] = {1u << 8, 1u << 16, 1u << 24};
+
+struct TargetC {  // per-target constants of the epilogue (shared memory, broadcast reads)
+    uint64_t q;     // prime
+    double qi32;    // 2^32 / q
+    uint64_t *out;  // row of this target in the output
+};
+
+// out = (sum_b C_b 2^(8b)) mod q from the 7 byte sums of the reduced constants
+// (each C_b < 2^23, the sum X < 2^72). IMAD.WIDE chains build lo = C_0..C_3 (< 2^48)
+// and Xh = floor(X / 2^32) = C_4 + (lo >> 32) + 2^8 C_5 + 2^16 C_6 (< 2^41), so
+// X mod 2^64 = {lo.lo, Xh.lo}. t = round(Xh 2^32 / q) on the FP64 pipe (the integer
+// sits in the low mantissa bits after adding 1.5 * 2^52): X / q < 2^28, dropping
+// lo.lo costs < 2^-12 and the rounding of the estimate < 2^-20, so |X - t q| < q; the
+// remainder in wrapping 64-bit arithmetic, one conditional add.
+__device__ __forceinline__ uint64_t fold_reduce(const uint32_t (&C)[8], uint64_t q, double qi32) {
+    const uint32_t p8 = kPow2[0], p16 = kPow2[1], p24 = kPow2[2];
+    const uint64_t lo = mad_wide(C[3], p24, mad_wide(C[2], p16, mad_wide(C[1], p8, C[0])));
+    const uint64_t xh = mad_wide(C[6], p16, mad_wide(C[5], p8, (uint64_t)(C[4] + (uint32_t)(lo >> 32))));
+    const uint32_t t = (uint32_t)__double_as_longlong(__fma_rn(ntt16::u2d(xh), qi32, ntt16::kMagic));
+    const uint64_t x = (uint64_t)(uint32_t)lo | (xh << 32);
+    const uint64_t tq = mad_wide(t, (uint32_t)q, (uint64_t)(t * (uint32_t)(q >> 32)) << 32);
+    const int64_t r = (int64_t)(x - tq);
+    return (uint64_t)(r < 0 ? r + (int64_t)q : r);
+}
+
+// Warp-specialised persistent kernel, one CTA per SM:
+//   warp 0      TMA issuer (one lane): bulk copies of the source rows of a tile into
+//               the raw ring, kRawStages tiles ahead;
+//   warps 1-4   transform: raw tile -> UMMA A layout (+ the overflow count u in the
+//               first free source slot), double-buffered;
+//   warp 5      MMA issuer (one lane): per chunk of <= 32 targets, ksteps MMAs into
+//               one of two 256-column TMEM accumulators;
+//   warps 6-..  epilogue: kEpiWarps / 4 warps per TMEM lane quarter (warp % 4), each
+//               taking every (kEpiWarps / 4)-th target of a chunk, four per TMEM wait.
+// mbarriers: raw_full / raw_empty per ring stage, a_full / a_empty per A buffer,
+// t_full / t_empty per TMEM buffer; "empty" waits start on parity 1 (the virtual
+// previous phase).
+constexpr int kXformWarp0 = 1, kXformWarps = 4, kMmaWarp = 5, kEpiWarp0 = 6;
 
 template <int kEpiWarps>
 __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
     k_conv_tc(const uint64_t *__restrict__ src, int n_src, const uint8_t *__restrict__ bmat,
               const int32_t *__restrict__ dst_mod, int n_dst, uint64_t *__restrict__ dst, int mode, int l, int n_q,
-              long long BN, const ModQ *__restrict__ mq, const double *__restrict__ src_invd,
-              const uint64_t *__restrict__ neg_m) {
+              long long BN, const double2 *__restrict__ fmod, const double *__restrict__ src_invd, int has_u) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sa = smem;                                              // A: 2 x 128 x 128 bytes
-    uint8_t *sb = smem + 2 * kTileM * kKBytes;                       // B: 16 n_dst x 128 bytes
+    uint8_t *sa = smem;                                   // A: 2 x 16 KiB (UMMA layout)
+    uint8_t *sraw = sa + 2 * kTileBytes;                  // raw ring: kRawStages x [16][128] u64
+    uint8_t *sb = sraw + kRawStages * kTileBytes;         // B: (n_dst + 1) x 1 KiB (one pad group)
     const int b_bytes = n_dst * kRowsPerTarget * kKBytes;
-    uint64_t *su = reinterpret_cast<uint64_t *>(sb + b_bytes);      // u: 2 x 128
-    ModQ *smq = reinterpret_cast<ModQ *>(su + 2 * kTileM);           // [n_dst]
-    uint64_t *snm = reinterpret_cast<uint64_t *>(smq + n_dst);       // [n_dst]
-    int *sidx = reinterpret_cast<int *>(snm + n_dst);                // [n_dst]
-    __shared__ __align__(8) uint64_t bars[10];  // a_full[2] a_empty[2] u_empty[2] t_full[2] t_empty[2]
+    TargetC *stc = reinterpret_cast<TargetC *>(sb + b_bytes + kRowsPerTarget * kKBytes);  // [n_dst]
+    __shared__ __align__(8) uint64_t bars[2 * kRawStages + 8];
     __shared__ uint32_t tmem_base_s;
     constexpr int kThreadsWs = (kEpiWarp0 + kEpiWarps) * 32;
     constexpr int kPerQuarter = kEpiWarps / 4;  // epilogue warps sharing one TMEM lane quarter
@@ -151,28 +186,34 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
         const uint4 *g = reinterpret_cast<const uint4 *>(bmat);
         uint4 *s = reinterpret_cast<uint4 *>(sb);
         for (int i = tid; i < b_bytes / 16; i += kThreadsWs) s[i] = g[i];
+        for (int i = tid; i < kRowsPerTarget * kKBytes / 16; i += kThreadsWs)
+            s[b_bytes / 16 + i] = make_uint4(0, 0, 0, 0);
         for (int d = tid; d < n_dst; d += kThreadsWs) {
             const int m = dst_mod[d];
-            smq[d] = mq[m];
-            sidx[d] = mode == 0 ? (m <= l ? m : l + 1 + m - n_q) : d;
-            snm[d] = neg_m ? neg_m[d] : 0;
+            const double2 f = fmod[m];
+            const int row = mode == 0 ? (m <= l ? m : l + 1 + m - n_q) : d;
+            stc[d] = TargetC{(uint64_t)f.x, f.y * 4294967296.0, dst + (long long)row * BN};
         }
     }
     const uint32_t bar0 = smem_u32(&bars[0]);
-    auto A_FULL = [&](int s) { return bar0 + 8u * (0 + s); };
-    auto A_EMPTY = [&](int s) { return bar0 + 8u * (2 + s); };
-    auto U_EMPTY = [&](int s) { return bar0 + 8u * (4 + s); };
-    auto T_FULL = [&](int s) { return bar0 + 8u * (6 + s); };
-    auto T_EMPTY = [&](int s) { return bar0 + 8u * (8 + s); };
+    auto RAW_FULL = [&](int s) { return bar0 + 8u * s; };
+    auto RAW_EMPTY = [&](int s) { return bar0 + 8u * (kRawStages + s); };
+    auto A_FULL = [&](int s) { return bar0 + 8u * (2 * kRawStages + s); };
+    auto A_EMPTY = [&](int s) { return bar0 + 8u * (2 * kRawStages + 2 + s); };
+    auto T_FULL = [&](int s) { return bar0 + 8u * (2 * kRawStages + 4 + s); };
+    auto T_EMPTY = [&](int s) { return bar0 + 8u * (2 * kRawStages + 6 + s); };
     if (warp == kMmaWarp) {  // TMEM: two 256-column int32 accumulators
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
+        for (int s = 0; s < kRawStages; ++s) {
+            mbar_init(RAW_FULL(s), 1);
+            mbar_init(RAW_EMPTY(s), kXformWarps);
+        }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(A_FULL(s), kProducers);
+            mbar_init(A_FULL(s), kXformWarps);
             mbar_init(A_EMPTY(s), 1);
-            mbar_init(U_EMPTY(s), kEpiWarps);
             mbar_init(T_FULL(s), 1);
             mbar_init(T_EMPTY(s), kEpiWarps);
         }
@@ -183,34 +224,55 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base_s;
-    const int ksteps = (n_src + 3) >> 2;  // 4 source slots (32 bytes) per MMA
+    const int n_slots = n_src + (has_u ? 1 : 0);
+    const int ksteps = (n_slots + 3) >> 2;  // 4 source slots (32 bytes) per MMA
     const int n_chunks = (n_dst + kChunkTargets - 1) / kChunkTargets;
+    const int chunk = (n_dst + n_chunks - 1) / n_chunks;  // balanced: 37 targets -> 19 + 18
     const long long tiles = BN / kTileM;
 
-    if (warp < kProducers) {
-        // ---------------------------------------------------------- producers
-        const int r = tid;
+    if (warp == 0) {
+        // ---------------------------------------------------------- TMA issuer
+        if (lane == 0) {
+            int i = 0;
+            for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+                const int s = i % kRawStages, par = ((i / kRawStages) & 1) ^ 1;
+                mbar_wait(RAW_EMPTY(s), par);
+                mbar_expect_tx(RAW_FULL(s), (uint32_t)n_src * 1024u);
+                const uint64_t *g = src + tile * kTileM;
+                const uint32_t d0 = smem_u32(sraw + s * kTileBytes);
+                for (int j = 0; j < n_src; ++j) bulk_g2s(d0 + j * 1024, g + (long long)j * BN, 1024, RAW_FULL(s));
+            }
+        }
+    } else if (warp < kMmaWarp) {
+        // ---------------------------------------------------------- transform
+        const int r = tid - kXformWarp0 * 32;
         int i = 0;
         for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
-            const int s = i & 1, par = ((i >> 1) & 1) ^ 1;
-            mbar_wait(A_EMPTY(s), par);
-            mbar_wait(U_EMPTY(s), par);
-            const long long e0 = tile * kTileM;
-            uint8_t *row = sa + s * (kTileM * kKBytes) + (r >> 3) * 1024 + (r & 7) * 16;
+            const int rs = i % kRawStages;
+            mbar_wait(RAW_FULL(rs), (i / kRawStages) & 1);
+            const uint64_t *raw = reinterpret_cast<const uint64_t *>(sraw + rs * kTileBytes) + r;
             uint64_t v[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = j < n_src ? src[(long long)j * BN + e0 + r] : 0;
-            double frac = 0.0;
-            if (neg_m) {
+            for (int j = 0; j < 16; ++j) v[j] = j < n_src ? raw[j * kTileM] : 0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(RAW_EMPTY(rs));
+            uint64_t u = 0;
+            if (has_u) {
+                double frac = 0.0;  // sum_i v_i / m_i, fixed order, no contraction (as k_conv and the oracle)
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
                     if (j < n_src) frac = __dadd_rn(frac, __dmul_rn(ntt16::u2d(v[j]), src_invd[j]));
+                u = (uint64_t)floor(__dadd_rn(frac, 0.5));
             }
+            const int s = i & 1;
+            mbar_wait(A_EMPTY(s), ((i >> 1) & 1) ^ 1);
+            uint8_t *row = sa + s * kTileBytes + (r >> 3) * 1024 + (r & 7) * 16;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
                 *reinterpret_cast<uint4 *>(row + c * 128) = make_uint4(
                     (uint32_t)v[2 * c], (uint32_t)(v[2 * c] >> 32), (uint32_t)v[2 * c + 1], (uint32_t)(v[2 * c + 1] >> 32));
-            su[s * kTileM + r] = neg_m ? (uint64_t)floor(__dadd_rn(frac, 0.5)) : 0;
+            // the overflow count takes source slot n_src (zero so far)
+            if (has_u) *reinterpret_cast<uint64_t *>(row + (n_src >> 1) * 128 + (n_src & 1) * 8) = u;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A visible to the tensor core
             __syncwarp();
             if (lane == 0) mbar_arrive(A_FULL(s));
@@ -223,13 +285,15 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
                 const int s = i & 1;
                 mbar_wait(A_FULL(s), (i >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t a0 = smem_u32(sa + s * (kTileM * kKBytes));
+                const uint32_t a0 = smem_u32(sa + s * kTileBytes);
                 for (int ch = 0; ch < n_chunks; ++ch, ++g) {
                     const int tb = g & 1;
                     mbar_wait(T_EMPTY(tb), ((g >> 1) & 1) ^ 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
-                    const int t0 = ch * kChunkTargets, nt = min(kChunkTargets, n_dst - t0);
-                    const uint32_t idesc = umma_idesc(nt * kRowsPerTarget);
+                    const int t0 = ch * chunk, nt = min(chunk, n_dst - t0);
+                    // N is a multiple of 16: an odd target count also multiplies the next row
+                    // group (the next target or the zero pad group), whose columns nobody reads
+                    const uint32_t idesc = umma_idesc((nt * kRowsPerTarget + 15) & ~15);
                     const uint32_t b0 = smem_u32(sb + t0 * kRowsPerTarget * kKBytes);
                     for (int k = 0; k < ksteps; ++k)
                         mma_i8(tmem + tb * 256, umma_desc(a0 + k * 256), umma_desc(b0 + k * 256), idesc, k);
@@ -242,35 +306,29 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
         // ---------------------------------------------------------- epilogue
         const int q = warp & 3, slot = (warp - kEpiWarp0) >> 2;
         const int row = q * 32 + lane;
-        int i = 0, g = 0;
-        for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
-            const int s = i & 1;
-            mbar_wait(A_FULL(s), (i >> 1) & 1);  // u of this tile is written
-            const uint64_t u = su[s * kTileM + row];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(U_EMPTY(s));
+        int g = 0;
+        for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             const long long e = tile * kTileM + row;
             for (int ch = 0; ch < n_chunks; ++ch, ++g) {
                 const int tb = g & 1;
                 mbar_wait(T_FULL(tb), (g >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const int t0 = ch * kChunkTargets, nt = min(kChunkTargets, n_dst - t0);
+                const int t0 = ch * chunk, nt = min(chunk, n_dst - t0);
                 const uint32_t tq = tmem + tb * 256 + ((uint32_t)(q * 32) << 16);
-                // this warp's targets of the chunk: slot, slot + kPerQuarter, ... two per TMEM wait
-                for (int tt = slot; tt < nt; tt += 2 * kPerQuarter) {
-                    const bool two = tt + kPerQuarter < nt;
-                    uint32_t C0[16], C1[16];
-                    tmem_ld16(tq + (uint32_t)(tt * kRowsPerTarget), C0);
-                    if (two) tmem_ld16(tq + (uint32_t)((tt + kPerQuarter) * kRowsPerTarget), C1);
+                // this warp's targets of the chunk: slot, slot + kPerQuarter, ... four per TMEM wait
+                for (int tt = slot; tt < nt; tt += 4 * kPerQuarter) {
+                    uint32_t C[4][8];
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+                        if (tt + w * kPerQuarter < nt)
+                            tmem_ld8(tq + (uint32_t)((tt + w * kPerQuarter) * kRowsPerTarget), C[w]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    {
-                        const int d = t0 + tt;
-                        dst[(long long)sidx[d] * BN + e] = fold_reduce(C0, (uint32_t)u, snm[d], smq[d]);
-                    }
-                    if (two) {
-                        const int d = t0 + tt + kPerQuarter;
-                        dst[(long long)sidx[d] * BN + e] = fold_reduce(C1, (uint32_t)u, snm[d], smq[d]);
-                    }
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+                        if (tt + w * kPerQuarter < nt) {
+                            const TargetC tc = stc[t0 + tt + w * kPerQuarter];
+                            tc.out[e] = fold_reduce(C[w], tc.q, tc.qi32);
+                        }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();
@@ -288,20 +346,21 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
 
 }  // namespace
 
-// Usable for this table and launch: prescaled sources, at most 16 of them, a
-// built B matrix, whole 128-coefficient tiles.
+// Usable for this table and launch: prescaled sources, at most 16 source slots
+// (the overflow count of a centred conversion takes one), a built B matrix, whole
+// 128-coefficient tiles.
 bool conv_tc_ok(const hk_ctx *c, const ConvTable &T, int n_dst, long long BN, int prescaled) {
     static const bool off = getenv("HK_CONV_TC") && atoi(getenv("HK_CONV_TC")) == 0;  // A/B knob
-    return !off && prescaled && T.d_bmat && T.n_src <= 16 && n_dst <= T.n_dst && BN % kTileM == 0 &&
-           c->log_n >= 7;
+    return !off && prescaled && T.d_bmat && T.n_src + (T.d_neg_m ? 1 : 0) <= 16 && n_dst <= T.n_dst &&
+           BN % kTileM == 0 && c->log_n >= 7;
 }
 
 int conv_tc_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l, long long BN,
                    int n_dst) {
-    const size_t smem = 2 * (size_t)kTileM * kKBytes + (size_t)n_dst * kRowsPerTarget * kKBytes + 2 * kTileM * 8 +
-                        n_dst * (sizeof(ModQ) + 8 + 4) + 64;
+    const size_t smem = (size_t)(2 + kRawStages) * kTileBytes + (size_t)(n_dst + 1) * kRowsPerTarget * kKBytes +
+                        n_dst * 24 + 64;
     if (smem > 227 * 1024) return hk_fail(c, HK_E_ARG, "conv_tc: %d targets exceed shared memory", n_dst);
-    static const int epi = getenv("HK_CONV_EPI") ? atoi(getenv("HK_CONV_EPI")) : 16;  // A/B: 8 / 12 / 16 warps -> 26.8 / 27.3 / 27.3 c1 inf/s
+    static const int epi = getenv("HK_CONV_EPI") ? atoi(getenv("HK_CONV_EPI")) : 16;  // A/B knob: 8 / 12 / 16 warps
     const long long tiles = BN / kTileM;
     const unsigned grid = (unsigned)std::min<long long>(tiles, (long long)c->n_sm);  // one CTA per SM (512 TMEM columns)
 #define HK_CONV_TC(EW)                                                                                           \
@@ -313,7 +372,8 @@ int conv_tc_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t 
         }                                                                                                        \
         k_conv_tc<EW><<<grid, (kEpiWarp0 + EW) * 32, smem, c->stream>>>(src, T.n_src, T.d_bmat, T.d_dst_mod,     \
                                                                        n_dst, dst, mode, l, c->n_q, BN,         \
-                                                                       c->d_modq, T.d_src_invd, T.d_neg_m);      \
+                                                                       c->d_fmod, T.d_src_invd,                 \
+                                                                       T.d_neg_m ? 1 : 0);                      \
     }
     if (epi == 16) HK_CONV_TC(16) else if (epi == 8) HK_CONV_TC(8) else HK_CONV_TC(12)
 #undef HK_CONV_TC

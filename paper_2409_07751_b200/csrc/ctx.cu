@@ -106,25 +106,11 @@ static ConvTable make_conv(const std::vector<uint64_t> &mod, const std::vector<i
     t.d_src_invd = nullptr;
     t.d_neg_m = nullptr;
     t.d_bmat = nullptr;
-    if (src.size() <= 16) {  // conv_tc.cu: bytes of hat in the no-swizzle K-major UMMA layout
-        std::vector<uint8_t> b(dst.size() * 16 * 128, 0);
-        for (size_t d = 0; d < dst.size(); ++d)
-            for (size_t i = 0; i < src.size(); ++i) {
-                const uint64_t h = hat[d * src.size() + i];
-                for (int diag = 0; diag < 16; ++diag)
-                    for (int a = 0; a < 8; ++a) {
-                        const int bb = diag - a;
-                        if (bb < 0 || bb > 7) continue;
-                        const size_t n = d * 16 + diag, kk = i * 8 + a;
-                        b[(n / 8) * 1024 + (kk / 16) * 128 + (n % 8) * 16 + kk % 16] = (uint8_t)(h >> (8 * bb));
-                    }
-            }
-        t.d_bmat = upload(b);
-    }
+    std::vector<uint64_t> negm;
     if (exact) {  // centred conversion: 1/m_i as float64, -M mod q_t (M = product of the sources)
         std::vector<double> invd(src.size());
         for (size_t i = 0; i < src.size(); ++i) invd[i] = 1.0 / (double)mod[src[i]];
-        std::vector<uint64_t> negm(dst.size());
+        negm.resize(dst.size());
         for (size_t d = 0; d < dst.size(); ++d) {
             const uint64_t qt = mod[dst[d]];
             uint64_t M = 1;
@@ -133,6 +119,30 @@ static ConvTable make_conv(const std::vector<uint64_t> &mod, const std::vector<i
         }
         t.d_src_invd = upload(invd);
         t.d_neg_m = upload(negm);
+    }
+    // conv_tc.cu: B[(t, b)][(i, a)] = byte b of (hat[t][i] 2^(8a) mod q_t), one 8-row group
+    // (7 bytes + a zero row) x 128 bytes per target in the no-swizzle K-major UMMA layout; a
+    // centred conversion carries -M mod q_t as the constant of source slot n_src (the
+    // overflow count u rides in the GEMM)
+    bool below50 = true;  // 7-byte residues and constants (every generated prime is < 2^50)
+    for (int m : src) below50 = below50 && mod[m] < (1ull << 50);
+    for (int m : dst) below50 = below50 && mod[m] < (1ull << 50);
+    if (below50 && src.size() + (exact ? 1 : 0) <= 16) {
+        std::vector<uint8_t> b(dst.size() * 8 * 128, 0);
+        for (size_t d = 0; d < dst.size(); ++d) {
+            const uint64_t qt = mod[dst[d]];
+            for (size_t i = 0; i < src.size() + (exact ? 1 : 0); ++i) {
+                uint64_t cst = i < src.size() ? hat[d * src.size() + i] : negm[d];
+                for (int a = 0; a < 8; ++a) {
+                    for (int bb = 0; bb < 8; ++bb) {
+                        const size_t n = d * 8 + bb, kk = i * 8 + a;
+                        b[(n / 8) * 1024 + (kk / 16) * 128 + (n % 8) * 16 + kk % 16] = (uint8_t)(cst >> (8 * bb));
+                    }
+                    cst = h_mulmod(cst, 256, qt);
+                }
+            }
+        }
+        t.d_bmat = upload(b);
     }
     return t;
 }

@@ -42,6 +42,16 @@ struct HasPrep : std::false_type {};
 template <class E>
 struct HasPrep<E, std::void_t<typename E::Pre>> : std::true_type {};
 
+// Epilogues whose output is NOT the between-phase buffer declare
+// `static constexpr bool kDiscardInter = true`: the row phase then drops each
+// between-phase line from L2 once it has been read (discard.global.L2), so the dirty
+// line is never written back to HBM. With an in-place epilogue the output
+// overwrites the line instead and nothing is discarded.
+template <class E, class = void>
+struct DiscardInter : std::false_type {};
+template <class E>
+struct DiscardInter<E, std::enable_if_t<E::kDiscardInter>> : std::true_type {};
+
 constexpr int kLogN = 16;
 constexpr int kN = 1 << kLogN;
 constexpr int kCl = 16;                      // column tiles / row blocks of 16 per polynomial
@@ -222,6 +232,9 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
 #pragma unroll
     for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = x[u];
     __syncwarp();
+    // every lane's loads of this row have been consumed: drop its 16 lines (one per lane)
+    if constexpr (DiscardInter<Epi>::value)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(rd + 16 * k) : "memory");
 #pragma unroll
     for (int v = 0; v < 16; ++v) x[v] = srow[pad16(16 * k + v)];
 #pragma unroll
@@ -459,6 +472,7 @@ constexpr int kH17 = 1 << 16;
 
 template <class Epi>
 struct EpiHalf {  // sub-polynomial P2 = l * 2B + 2b + h, idx < 2^16 -> (l * B + b, h * H + idx)
+    static constexpr bool kDiscardInter = DiscardInter<Epi>::value;
     Epi epi;
     int B;
     __device__ __forceinline__ void operator()(int l, long long P2, int idx, uint64_t v) const {
@@ -552,9 +566,21 @@ inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int 
     const long long n = (long long)n_limbs * B;
     const double2 *tw = (const double2 *)c->d_twf, *twist = (const double2 *)c->d_twist;
     const FpMod *fm = (const FpMod *)c->d_fmod;
-    const cudaError_t e =
-        launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi,
-                         sample_major ? n_limbs : 0);
+    cudaError_t e;
+    if constexpr (DiscardInter<Epi>::value) {
+        // epilogues that stream operands and outputs past the between-phase buffer: fewer
+        // polynomials in flight (8 CTAs each) keep that buffer in L2 (profiles/r2_notes.md §8)
+        static const int cpp = getenv("HK_CPP_EPI") ? atoi(getenv("HK_CPP_EPI")) : 8;  // A/B knob: 4 -> 29.66, 8 -> 29.76 c1 inf/s
+        if (cpp == 8)
+            e = launch_clustered(fwd_kernel<Pro, Epi, 8>, 8, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi,
+                                 sample_major ? n_limbs : 0);
+        else
+            e = launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, fm, pro,
+                                 epi, sample_major ? n_limbs : 0);
+    } else {
+        e = launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi,
+                             sample_major ? n_limbs : 0);
+    }
     ++c->launches;
     if (e != cudaSuccess) return hk_fail(c, HK_E_CUDA, "ntt16 fwd launch: %s", cudaGetErrorString(e));
     HK_LAUNCH_CHECK(c, "ntt16 fwd");

@@ -571,6 +571,7 @@ struct ProRsBcast {
 // NTT epilogue: out[p][l][b] = (X - v) * q_la^-1
 template <int KIND>
 struct EpiRescale {
+    static constexpr bool kDiscardInter = true;  // output != between-phase buffer (ntt16.cuh)
     RsSrc<KIND> src;
     uint64_t *out;
     const ulonglong2 *qinv;
@@ -584,8 +585,8 @@ struct EpiRescale {
         const int pb = (int)(P - (long long)l * 2 * B), p = pb >= B ? 1 : 0, b = pb - p * B;
         const uint64_t q = src.mq[l].q;
         const ulonglong2 w = qinv[l];
-        out[((long long)p * src.la + l) * src.BN + ((long long)b << src.log_n) + idx] =
-            mul_shoup(sub_mod(x, v, q), w.x, w.y, q);
+        __stcs(out + ((long long)p * src.la + l) * src.BN + ((long long)b << src.log_n) + idx,
+               mul_shoup(sub_mod(x, v, q), w.x, w.y, q));
     }
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         fin(l, P, idx, prep(l, P, idx), v);
@@ -616,6 +617,7 @@ struct EpiScaleDigits {
 
 // NTT epilogue: ModDown finish (acc - v) * P^-1 (+ sigma_g(addend))
 struct EpiModDown {
+    static constexpr bool kDiscardInter = true;  // output != between-phase buffer (ntt16.cuh)
     const uint64_t *acc, *addend;
     uint64_t *out;
     const ulonglong2 *pinv;
@@ -744,36 +746,6 @@ struct ProD2 {
         return T.d(2, l, (long long)l * BN + ((P - (long long)l * B) << log_n) + idx);
     }
 };
-// NTT epilogue, merged ModDown + rescale with d_p formed from (a, b)
-struct EpiMdRsT {
-    const uint64_t *acc;
-    Tensor T;
-    int which;
-    uint64_t *out;
-    const ulonglong2 *pmod, *mqinv;
-    const ModQ *mq;
-    int B, log_n;
-    long long BN;
-    LinTerm lin;
-    Affine aff;
-    using Pre = uint64_t;  // y = acc + P d
-    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
-        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
-        const uint64_t q = mq[l].q;
-        const ulonglong2 Pm = pmod[l];
-        const uint64_t d = lin.apply(which, l, o, T.d(which, l, o), q);
-        return add_mod(acc[o], mul_shoup(d, Pm.x, Pm.y, q), q);
-    }
-    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre y, uint64_t v) const {
-        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
-        const uint64_t q = mq[l].q;
-        const ulonglong2 w = mqinv[l];
-        out[o] = aff.apply(which, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
-    }
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
-        fin(l, P, idx, prep(l, P, idx), v);
-    }
-};
 // Merged ModDown + rescale of both halves of a relinearised product: launches
 // run over 2B "samples" pb = 2 b + p, so the two halves of one sample sit in
 // adjacent clusters and the tensor operands a0 / b0 both read are shared in L2.
@@ -785,57 +757,6 @@ struct ProAccSp2 {
     __device__ __forceinline__ uint64_t operator()(int j, long long P, int idx) const {
         const long long pb = P - (long long)j * 2 * B;
         return acc[(pb & 1) * pne + (long long)(l + 1 + j) * BN + ((pb >> 1) << log_n) + idx];
-    }
-};
-// iNTT prologue of limb l: y = acc_p,l + P d_p,l
-struct ProMdYT2 {
-    const uint64_t *acc;
-    Tensor T;
-    long long BN, pne;
-    int l, log_n;
-    const ulonglong2 *pmod;
-    const ModQ *mq;
-    LinTerm lin;
-    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
-        const int p = (int)(P & 1);
-        const long long o = (long long)l * BN + ((P >> 1) << log_n) + idx;
-        const uint64_t q = mq[l].q;
-        const ulonglong2 Pm = pmod[l];
-        const uint64_t d = lin.apply(p, l, o, T.d(p, l, o), q);
-        return add_mod(acc[p * pne + o], mul_shoup(d, Pm.x, Pm.y, q), q);
-    }
-};
-// forward NTT epilogue: out_p = (acc_p + P d_p - v) (P q_l)^-1 (+ affine)
-struct EpiMdRsT2 {
-    const uint64_t *acc;
-    Tensor T;
-    uint64_t *out;
-    const ulonglong2 *pmod, *mqinv;
-    const ModQ *mq;
-    int B, log_n;
-    long long BN, pne, pout;  // offsets of half 1 in acc / out
-    LinTerm lin;
-    Affine aff;
-    using Pre = uint64_t;  // y = acc_p + P d_p
-    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
-        const long long pb = P - (long long)l * 2 * B;
-        const int p = (int)(pb & 1);
-        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
-        const uint64_t q = mq[l].q;
-        const ulonglong2 Pm = pmod[l];
-        const uint64_t d = lin.apply(p, l, o, T.d(p, l, o), q);
-        return add_mod(acc[p * pne + o], mul_shoup(d, Pm.x, Pm.y, q), q);
-    }
-    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre y, uint64_t v) const {
-        const long long pb = P - (long long)l * 2 * B;
-        const int p = (int)(pb & 1);
-        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
-        const uint64_t q = mq[l].q;
-        const ulonglong2 w = mqinv[l];
-        out[p * pout + o] = aff.apply(p, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
-    }
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
-        fin(l, P, idx, prep(l, P, idx), v);
     }
 };
 // Folded relinearisation (FoldD): acc_p already holds Y_p = acc_p + P d_p on
@@ -850,6 +771,7 @@ struct ProAccL2 {
     }
 };
 struct EpiMdRsY2 {  // out_p = aff((Y_p - v) (P q_l)^-1)
+    static constexpr bool kDiscardInter = true;  // output != between-phase buffer (ntt16.cuh)
     const uint64_t *acc;
     uint64_t *out;
     const ulonglong2 *mqinv;
@@ -860,7 +782,7 @@ struct EpiMdRsY2 {  // out_p = aff((Y_p - v) (P q_l)^-1)
     using Pre = uint64_t;
     __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
         const long long pb = P - (long long)l * 2 * B;
-        return acc[(pb & 1) * pne + (long long)l * BN + ((pb >> 1) << log_n) + idx];
+        return __ldcs(acc + (pb & 1) * pne + (long long)l * BN + ((pb >> 1) << log_n) + idx);
     }
     __device__ __forceinline__ void fin(int l, long long P, int idx, Pre y, uint64_t v) const {
         const long long pb = P - (long long)l * 2 * B;
@@ -868,7 +790,7 @@ struct EpiMdRsY2 {  // out_p = aff((Y_p - v) (P q_l)^-1)
         const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
         const uint64_t q = mq[l].q;
         const ulonglong2 w = mqinv[l];
-        out[p * pout + o] = aff.apply(p, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q);
+        __stcs(out + p * pout + o, aff.apply(p, l, mul_shoup(sub_mod(y, v, q), w.x, w.y, q), q));
     }
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         fin(l, P, idx, prep(l, P, idx), v);
@@ -877,6 +799,7 @@ struct EpiMdRsY2 {  // out_p = aff((Y_p - v) (P q_l)^-1)
 // ModDown of both halves of a key switch (interleaved samples 2 b + p):
 // out_p = (acc_p - v) P^-1 (+ sigma_g(add_p))
 struct EpiModDown2 {
+    static constexpr bool kDiscardInter = true;  // output != between-phase buffer (ntt16.cuh)
     const uint64_t *acc, *add0, *add1;
     uint64_t *out0, *out1;
     const ulonglong2 *pinv;
@@ -891,7 +814,7 @@ struct EpiModDown2 {
         const long long pb = P - (long long)l * 2 * B;
         const int p = (int)(pb & 1);
         const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
-        Pre r{acc[p * pne + o], 0};
+        Pre r{__ldcs(acc + p * pne + o), 0};
         const uint64_t *addend = p ? add1 : add0;
         if (addend) r.add = addend[g == 1u ? o : o - idx + auto_src((uint32_t)idx, g, log_n)];
         return r;
@@ -904,28 +827,10 @@ struct EpiModDown2 {
         const ulonglong2 w = pinv[l];
         uint64_t r = mul_shoup(sub_mod(pr.a, v, q), w.x, w.y, q);
         if (p ? add1 : add0) r = add_mod(r, pr.add, q);
-        (p ? out1 : out0)[o] = r;
+        __stcs((p ? out1 : out0) + o, r);
     }
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         fin(l, P, idx, prep(l, P, idx), v);
-    }
-};
-// iNTT prologue: y = acc_l + P d_l with d_l from (a, b)
-struct ProMdYT {
-    const uint64_t *acc;
-    Tensor T;
-    int which, l;
-    long long BN;
-    const ulonglong2 *pmod;
-    const ModQ *mq;
-    int log_n;
-    LinTerm lin;
-    __device__ __forceinline__ uint64_t operator()(int, long long P, int idx) const {
-        const long long o = (long long)l * BN + (P << log_n) + idx;
-        const uint64_t q = mq[l].q;
-        const ulonglong2 Pm = pmod[l];
-        const uint64_t d = lin.apply(which, l, o, T.d(which, l, o), q);
-        return add_mod(acc[o], mul_shoup(d, Pm.x, Pm.y, q), q);
     }
 };
 
@@ -959,6 +864,7 @@ struct ProMdY {
 };
 // NTT epilogue: out_t = (acc_t + P d_t - v) * (P q_l)^-1
 struct EpiMdRs {
+    static constexpr bool kDiscardInter = true;  // output != between-phase buffer (ntt16.cuh)
     const uint64_t *acc, *d;
     uint64_t *out;
     const ulonglong2 *pmod, *mqinv;
