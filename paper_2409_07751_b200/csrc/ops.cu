@@ -46,6 +46,28 @@ __global__ void k_addsub(const uint64_t *__restrict__ a, int la, const uint64_t 
     out[((long long)p * (lo + 1) + l) * BN + e] = neg ? sub_mod(x, y, q) : add_mod(x, y, q);
 }
 
+// same, four elements per thread as two 16-byte accesses (BN % 1024 == 0): the scalar
+// kernel reaches 4.4 TB/s of DRAM traffic on 37 x 128 limbs, this one see profiles/r2_notes.md §9
+__global__ void __launch_bounds__(256) k_addsub4(const ulonglong2 *__restrict__ a, int la,
+                                                 const ulonglong2 *__restrict__ b, int lb,
+                                                 ulonglong2 *__restrict__ out, int lo, long long BN2, int neg,
+                                                 const ModQ *__restrict__ mq) {
+    const long long e = (long long)blockIdx.x * 512 + threadIdx.x;  // in 16-byte units
+    const int l = blockIdx.y, p = blockIdx.z;
+    const uint64_t q = mq[l].q;
+    const ulonglong2 *pa = a + ((long long)p * (la + 1) + l) * BN2 + e;
+    const ulonglong2 *pb = b + ((long long)p * (lb + 1) + l) * BN2 + e;
+    ulonglong2 *po = out + ((long long)p * (lo + 1) + l) * BN2 + e;
+    const ulonglong2 x0 = pa[0], x1 = pa[256], y0 = pb[0], y1 = pb[256];
+    ulonglong2 r0, r1;
+    r0.x = neg ? sub_mod(x0.x, y0.x, q) : add_mod(x0.x, y0.x, q);
+    r0.y = neg ? sub_mod(x0.y, y0.y, q) : add_mod(x0.y, y0.y, q);
+    r1.x = neg ? sub_mod(x1.x, y1.x, q) : add_mod(x1.x, y1.x, q);
+    r1.y = neg ? sub_mod(x1.y, y1.y, q) : add_mod(x1.y, y1.y, q);
+    po[0] = r0;
+    po[256] = r1;
+}
+
 // c0 +/- pt (pt_batch 1 or B), c1 copied
 __global__ void k_add_plain(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ pt, int pb,
                             int neg, uint64_t *__restrict__ out, long long BN, int log_n,
@@ -365,7 +387,7 @@ __device__ __forceinline__ double fold_prod(const uint64_t *a, const uint64_t *b
 // the key pair, the galois index and the address math are paid once.
 // grid (N/min(N,256) * B/bb, ne); every residue is exact, results canonical.
 template <int ND, bool FOLD>
-__global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
+__global__ void __launch_bounds__(256, 3) k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
                                                 const uint64_t *__restrict__ dm, int alpha, int ne, int l, int n_q,
                                                 int nm, int ksp0, int log_n, int bb, const uint64_t *__restrict__ key,
                                                 uint32_t g, uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1,
@@ -398,57 +420,93 @@ __global__ void __launch_bounds__(256) k_key_ip(const uint64_t *__restrict__ ext
     const uint64_t *xm = dm ? dm + (long long)t * BN + row + ks : nullptr;
     uint64_t *o0 = acc0 + (long long)t * BN + row + k;
     uint64_t *o1 = acc1 + (long long)t * BN + row + k;
-    for (int b = 0; b < bb; ++b) {
-        double x[ND];
+    const bool fold = FOLD && t <= l;
+    // two samples per step: every load of both is issued before the arithmetic of the
+    // first (the operand pointers of the fold are not restrict-qualified, so the compiler
+    // would not hoist them above the previous sample's stores): 6.18 -> see profiles/r2_notes.md §9
+    for (int b = 0; b < bb; b += 2) {
+        const int nu = min(2, bb - b);
+        uint64_t rx[2][ND], ry[2] = {0, 0}, rm[2] = {0, 0}, rs0[2] = {0, 0}, rs1[2] = {0, 0};
+        uint64_t fa0[2] = {0, 0}, fa1[2] = {0, 0}, fb0[2] = {0, 0}, fb1[2] = {0, 0};
 #pragma unroll
-        for (int j = 0; j < ND; ++j) x[j] = j == own_j ? 0.0 : u2d(xe[j * dstride]);
-        if (own_j >= 0) {
-            double y = u2d(*xd);
-            if (xm) {  // relinearisation: d = a1 (.) b1 on the fly
-                const double w = u2d(*xm);
-                y = f_center(f_mulmod(y, w, __dmul_rn(w, M.qinv), M.q), M);
-            }
+        for (int u = 0; u < 2; ++u) {
+            if (u < nu) {
 #pragma unroll
-            for (int j = 0; j < ND; ++j)
-                if (j == own_j) x[j] = y;
-        }
-        // accum: add onto the running sum of earlier key switches (hk_rotate_sum)
-        double s0 = accum ? u2d(*o0) : 0.0, s1 = accum ? u2d(*o1) : 0.0;
-        if (FOLD && t <= l) {  // Y_p = acc_p + P d_p (g = 1: ks = k)
-            const long long o = (long long)t * BN + row + (long long)b * N + k;
-            double d0 = fold_prod(fd.a, fd.b, o, o, M);
-            double d1 = __dadd_rn(fold_prod(fd.a, fd.b, o, fd.pb + o, M), fold_prod(fd.a, fd.b, fd.pa + o, o, M));
-            if (fd.a2) {
-                d0 = __dadd_rn(d0, fold_prod(fd.a2, fd.b2, o, o, M));
-                d1 = f_center(d1, M);
-                d1 = __dadd_rn(d1, __dadd_rn(fold_prod(fd.a2, fd.b2, o, fd.pb2 + o, M),
-                                             fold_prod(fd.a2, fd.b2, fd.pa2 + o, o, M)));
+                for (int j = 0; j < ND; ++j) rx[u][j] = j == own_j ? 0 : xe[u * N + j * dstride];
+                if (own_j >= 0) {
+                    ry[u] = xd[u * N];
+                    if (xm) rm[u] = xm[u * N];
+                }
+                if (accum) {
+                    rs0[u] = o0[u * N];
+                    rs1[u] = o1[u * N];
+                }
+                if (fold) {  // g = 1: ks = k
+                    const long long o = (long long)t * BN + row + (long long)(b + u) * N + k;
+                    fa0[u] = fd.a[o];
+                    fa1[u] = fd.a[fd.pa + o];
+                    fb0[u] = fd.b[o];
+                    fb1[u] = fd.b[fd.pb + o];
+                }
             }
-            if (fd.x) {
-                const double kk = u2d(fd.k.v[t]), kq = __dmul_rn(kk, M.qinv);
-                d0 = __dadd_rn(f_center(d0, M), f_mulmod(u2d(fd.x[o]), kk, kq, M.q));
-                d1 = __dadd_rn(f_center(d1, M), f_mulmod(u2d(fd.x[fd.px + o]), kk, kq, M.q));
-            }
-            const double pm = u2d(fd.pmod[t].x), pq = __dmul_rn(pm, M.qinv);
-            s0 = f_center(__dadd_rn(s0, f_mulmod(f_center(d0, M), pm, pq, M.q)), M);
-            s1 = f_center(__dadd_rn(s1, f_mulmod(f_center(d1, M), pm, pq, M.q)), M);
         }
 #pragma unroll
-        for (int j = 0; j < ND; ++j) {  // |f_mulmod| < 2.5 q: recentre every second term
-            s0 = __dadd_rn(s0, f_mulmod(x[j], w0[j], v0[j], M.q));
-            s1 = __dadd_rn(s1, f_mulmod(x[j], w1[j], v1[j], M.q));
-            if (j & 1) {
-                s0 = f_center(s0, M);
-                s1 = f_center(s1, M);
+        for (int u = 0; u < 2; ++u) {
+            if (u < nu) {
+                double x[ND];
+#pragma unroll
+                for (int j = 0; j < ND; ++j) x[j] = u2d(rx[u][j]);
+                if (own_j >= 0) {
+                    double y = u2d(ry[u]);
+                    if (xm) {  // relinearisation: d = a1 (.) b1 on the fly
+                        const double w = u2d(rm[u]);
+                        y = f_center(f_mulmod(y, w, __dmul_rn(w, M.qinv), M.q), M);
+                    }
+#pragma unroll
+                    for (int j = 0; j < ND; ++j)
+                        if (j == own_j) x[j] = y;
+                }
+                // accum: add onto the running sum of earlier key switches (hk_rotate_sum)
+                double s0 = accum ? u2d(rs0[u]) : 0.0, s1 = accum ? u2d(rs1[u]) : 0.0;
+                if (fold) {  // Y_p = acc_p + P d_p
+                    const long long o = (long long)t * BN + row + (long long)(b + u) * N + k;
+                    const double a0 = u2d(fa0[u]), a1 = u2d(fa1[u]), b0 = u2d(fb0[u]), b1 = u2d(fb1[u]);
+                    const double b0q = __dmul_rn(b0, M.qinv), b1q = __dmul_rn(b1, M.qinv);
+                    double d0 = f_mulmod(a0, b0, b0q, M.q);
+                    double d1 = __dadd_rn(f_mulmod(a0, b1, b1q, M.q), f_mulmod(a1, b0, b0q, M.q));
+                    if (fd.a2) {
+                        d0 = __dadd_rn(d0, fold_prod(fd.a2, fd.b2, o, o, M));
+                        d1 = f_center(d1, M);
+                        d1 = __dadd_rn(d1, __dadd_rn(fold_prod(fd.a2, fd.b2, o, fd.pb2 + o, M),
+                                                     fold_prod(fd.a2, fd.b2, fd.pa2 + o, o, M)));
+                    }
+                    if (fd.x) {
+                        const double kk = u2d(fd.k.v[t]), kq = __dmul_rn(kk, M.qinv);
+                        d0 = __dadd_rn(f_center(d0, M), f_mulmod(u2d(fd.x[o]), kk, kq, M.q));
+                        d1 = __dadd_rn(f_center(d1, M), f_mulmod(u2d(fd.x[fd.px + o]), kk, kq, M.q));
+                    }
+                    const double pm = u2d(fd.pmod[t].x), pq = __dmul_rn(pm, M.qinv);
+                    s0 = f_center(__dadd_rn(s0, f_mulmod(f_center(d0, M), pm, pq, M.q)), M);
+                    s1 = f_center(__dadd_rn(s1, f_mulmod(f_center(d1, M), pm, pq, M.q)), M);
+                }
+#pragma unroll
+                for (int j = 0; j < ND; ++j) {  // |f_mulmod| < 2.5 q: recentre every second term
+                    s0 = __dadd_rn(s0, f_mulmod(x[j], w0[j], v0[j], M.q));
+                    s1 = __dadd_rn(s1, f_mulmod(x[j], w1[j], v1[j], M.q));
+                    if (j & 1) {
+                        s0 = f_center(s0, M);
+                        s1 = f_center(s1, M);
+                    }
+                }
+                o0[u * N] = d2canon(s0, M);
+                o1[u * N] = d2canon(s1, M);
             }
         }
-        *o0 = d2canon(s0, M);
-        *o1 = d2canon(s1, M);
-        xe += N;
-        xd += N;
-        if (xm) xm += N;
-        o0 += N;
-        o1 += N;
+        xe += 2 * N;
+        xd += 2 * N;
+        if (xm) xm += 2 * N;
+        o0 += 2 * N;
+        o1 += 2 * N;
     }
 }
 
@@ -1275,7 +1333,12 @@ int hk_add(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "add: level out of range");
     const int lo = std::min(la, lb);
     const long long BN = (long long)B * c->n;
-    k_addsub<<<egrid(BN, lo + 1, 2), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 0, c->d_modq); ++c->launches;
+    if (BN % 1024 == 0)
+        k_addsub4<<<dim3((unsigned)(BN / 1024), (unsigned)(lo + 1), 2), 256, 0, c->stream>>>(
+            (const ulonglong2 *)a, la, (const ulonglong2 *)b, lb, (ulonglong2 *)o, lo, BN / 2, 0, c->d_modq);
+    else
+        k_addsub<<<egrid(BN, lo + 1, 2), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 0, c->d_modq);
+    ++c->launches;
     HK_LAUNCH_CHECK(c, "add");
     return HK_OK;
 }
@@ -1284,7 +1347,12 @@ int hk_sub(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *b, int32_t 
     if (la < 0 || lb < 0 || la >= c->n_q || lb >= c->n_q) return hk_fail(c, HK_E_ARG, "sub: level out of range");
     const int lo = std::min(la, lb);
     const long long BN = (long long)B * c->n;
-    k_addsub<<<egrid(BN, lo + 1, 2), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 1, c->d_modq); ++c->launches;
+    if (BN % 1024 == 0)
+        k_addsub4<<<dim3((unsigned)(BN / 1024), (unsigned)(lo + 1), 2), 256, 0, c->stream>>>(
+            (const ulonglong2 *)a, la, (const ulonglong2 *)b, lb, (ulonglong2 *)o, lo, BN / 2, 1, c->d_modq);
+    else
+        k_addsub<<<egrid(BN, lo + 1, 2), 256, 0, c->stream>>>(a, la, b, lb, o, lo, BN, 1, c->d_modq);
+    ++c->launches;
     HK_LAUNCH_CHECK(c, "sub");
     return HK_OK;
 }

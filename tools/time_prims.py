@@ -21,6 +21,7 @@ eng = be.engine
 B, nl, N = args.batch, args.level + 1, p.n
 x = np.random.default_rng(0).uniform(-1, 1, (B, p.slot_count))
 ct = be.encrypt(x, level=args.level)
+ct2 = be.encrypt(-x, level=args.level)
 be.ensure_rotation_keys([1])
 buf = eng.alloc_u64(nl * B * N)
 buf.zero_()
@@ -42,7 +43,7 @@ def timeit(name, fn, algbytes):
 limb = B * N * 8
 timeit("ntt_fwd", lambda: eng.call("hk_ntt_fwd", eng.addr(buf), 0, nl, B), 2 * nl * limb)
 timeit("ntt_inv", lambda: eng.call("hk_ntt_inv", eng.addr(buf), 0, nl, B), 2 * nl * limb)
-timeit("add", lambda: be.add(ct, ct), 6 * nl * limb)
+timeit("add", lambda: be.add(ct, ct2), 6 * nl * limb)
 timeit("mul_plain", lambda: be.mul(ct, x[0]), 4 * nl * limb)
 timeit("mul_ct(relin)", lambda: be.mul(ct, ct), 6 * nl * limb)
 timeit("rotate", lambda: be.rotate(ct, 1), 4 * nl * limb)
