@@ -89,6 +89,52 @@ __global__ void k_add_const(const uint64_t *__restrict__ a, int la, Residues r, 
     out[o] = p == 1 ? a[o] : add_mod(a[o], r.v[l], mq[l].q);
 }
 
+// add_plain / add_const with 16-byte accesses, four elements per thread (BN % 1024 == 0;
+// grid (BN / 1024, limbs, 2)), as k_addsub4
+__global__ void __launch_bounds__(256) k_add_plain4(const ulonglong2 *__restrict__ a, int la,
+                                                    const ulonglong2 *__restrict__ pt, int pb, int neg,
+                                                    ulonglong2 *__restrict__ out, long long BN2, int log_n,
+                                                    const ModQ *__restrict__ mq) {
+    const long long e = (long long)blockIdx.x * 512 + threadIdx.x;  // in 16-byte units
+    const int l = blockIdx.y, p = blockIdx.z;
+    const long long o = ((long long)p * (la + 1) + l) * BN2 + e;
+    const ulonglong2 x0 = a[o], x1 = a[o + 256];
+    if (p == 1) {
+        out[o] = x0;
+        out[o + 256] = x1;
+        return;
+    }
+    const int N2 = 1 << (log_n - 1);
+    const long long e1 = e + 256;
+    const ulonglong2 y0 = pt[((long long)l * pb + (pb == 1 ? 0 : e >> (log_n - 1))) * N2 + (e & (N2 - 1))];
+    const ulonglong2 y1 = pt[((long long)l * pb + (pb == 1 ? 0 : e1 >> (log_n - 1))) * N2 + (e1 & (N2 - 1))];
+    const uint64_t q = mq[l].q;
+    ulonglong2 r0, r1;
+    r0.x = neg ? sub_mod(x0.x, y0.x, q) : add_mod(x0.x, y0.x, q);
+    r0.y = neg ? sub_mod(x0.y, y0.y, q) : add_mod(x0.y, y0.y, q);
+    r1.x = neg ? sub_mod(x1.x, y1.x, q) : add_mod(x1.x, y1.x, q);
+    r1.y = neg ? sub_mod(x1.y, y1.y, q) : add_mod(x1.y, y1.y, q);
+    out[o] = r0;
+    out[o + 256] = r1;
+}
+__global__ void __launch_bounds__(256) k_add_const4(const ulonglong2 *__restrict__ a, int la, Residues r,
+                                                    ulonglong2 *__restrict__ out, long long BN2,
+                                                    const ModQ *__restrict__ mq) {
+    const long long e = (long long)blockIdx.x * 512 + threadIdx.x;
+    const int l = blockIdx.y, p = blockIdx.z;
+    const long long o = ((long long)p * (la + 1) + l) * BN2 + e;
+    ulonglong2 x0 = a[o], x1 = a[o + 256];
+    if (p == 0) {
+        const uint64_t c = r.v[l], q = mq[l].q;
+        x0.x = add_mod(x0.x, c, q);
+        x0.y = add_mod(x0.y, c, q);
+        x1.x = add_mod(x1.x, c, q);
+        x1.y = add_mod(x1.y, c, q);
+    }
+    out[o] = x0;
+    out[o + 256] = x1;
+}
+
 // tmp = a (.) pt for both polys (limbs 0..la)
 __global__ void k_mul_plain(const uint64_t *__restrict__ a, int la, const uint64_t *__restrict__ pt, int pb,
                             uint64_t *__restrict__ out, long long BN, int log_n, const ModQ *__restrict__ mq) {
@@ -1362,7 +1408,12 @@ int hk_add_plain(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *pt, i
     if (la < 0 || la >= c->n_q || lp < la) return hk_fail(c, HK_E_ARG, "add_plain: level mismatch");
     if (pb != 1 && pb != B) return hk_fail(c, HK_E_LENGTH, "add_plain: plaintext batch");
     const long long BN = (long long)B * c->n;
-    k_add_plain<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, pt, pb, negate, out, BN, c->log_n, c->d_modq);
+    if (BN % 1024 == 0)
+        k_add_plain4<<<dim3((unsigned)(BN / 1024), (unsigned)(la + 1), 2), 256, 0, c->stream>>>(
+            (const ulonglong2 *)a, la, (const ulonglong2 *)pt, pb, negate, (ulonglong2 *)out, BN / 2, c->log_n,
+            c->d_modq);
+    else
+        k_add_plain<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, pt, pb, negate, out, BN, c->log_n, c->d_modq);
     ++c->launches;
     HK_LAUNCH_CHECK(c, "add_plain");
     return HK_OK;
@@ -1373,7 +1424,12 @@ int hk_add_const(hk_ctx *c, const uint64_t *a, int32_t la, const uint64_t *res, 
     Residues r;
     for (int l = 0; l <= la; ++l) r.v[l] = res[l];
     const long long BN = (long long)B * c->n;
-    k_add_const<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, r, out, BN, c->d_modq); ++c->launches;
+    if (BN % 1024 == 0)
+        k_add_const4<<<dim3((unsigned)(BN / 1024), (unsigned)(la + 1), 2), 256, 0, c->stream>>>(
+            (const ulonglong2 *)a, la, r, (ulonglong2 *)out, BN / 2, c->d_modq);
+    else
+        k_add_const<<<egrid(BN, la + 1, 2), 256, 0, c->stream>>>(a, la, r, out, BN, c->d_modq);
+    ++c->launches;
     HK_LAUNCH_CHECK(c, "add_const");
     return HK_OK;
 }

@@ -167,3 +167,32 @@ def test_c5_ring_2e17(gpu_lib):
         assert ours.pt_mults == theirs["pt_mults"]
         assert ours.adds == theirs["adds"] + 32
         assert ours.depth_consumed == theirs["depth_consumed"]
+
+
+def test_c5_tiled_2e16(gpu_lib):
+    """c5 [3072,128,10] at N = 2^16 as BASELINE config 5 states it: 33792
+    repeat-packed slots exceed the 32768 available (the reference raises
+    PackingOverflow), so layer 1's B-spline branch runs as two tiles of 1536
+    features (inference.spline_tiles). Decrypted outputs within 1e-4 of the
+    reference's mirrored forward (golden, produced at 65536 slots) and of the
+    plaintext twin; depth equals the reference plan; layer 1 spends the
+    second tile's products and rotations on top of the reference counts."""
+    g_ = np.load(os.path.join(GOLD, "c5.npz"))
+    _, model, X = configs.workload("c5", batch=2)
+    depth = int(g_["plan_total"])
+    p = kan_params(depth)
+    assert p.slot_count == 32768
+    assert inf.spline_tiles(model.layers[0], p.slot_count) == 2
+    assert inf.spline_tiles(model.layers[1], p.slot_count) == 1
+    be = _gpu(p, depth)
+    out, stats = inf.model_forward_he(model, inf.encrypt_input(X[:2], model, be), inf.PipelineConfig())
+    dec = be.decrypt(out)[:, :10]
+    err_twin = np.abs(dec - _twin(model, X[:2])).max()
+    err_ref = np.abs(dec - g_["mirrored"][:2]).max()
+    print(f"c5 tiled at N=2^16: |dec - twin| = {err_twin:.3g}, |dec - reference mirrored| = {err_ref:.3g}")
+    assert err_twin < 1e-4 and err_ref < 1e-4
+    ref = json.loads(str(g_["counts"]))
+    assert [s.depth_consumed for s in stats.per_layer] == [r["depth_consumed"] for r in ref]
+    assert stats.per_layer[0].ct_mults > ref[0]["ct_mults"]          # the second tile
+    assert stats.per_layer[1].ct_mults == ref[1]["ct_mults"]          # layer 2 is untiled
+    assert stats.per_layer[1].rotations == ref[1]["rotations"]

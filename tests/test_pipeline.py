@@ -67,7 +67,6 @@ def test_mirrored_plaintext_is_reference_bit_exact():
     cs = build_composite_sign()
     mine = np.stack([mdl.model_forward_plain(model, x, "mirrored", cs, "lazy") for x in X])
     assert np.array_equal(mine, g["mirrored"])
-    exact = np.stack([mdl.model_forward_plain(model, x, "exact") for x in X])
     assert np.array_equal(exact, g["exact"])
 
 
@@ -243,3 +242,43 @@ def test_c3_counts_vs_reference():
             theirs["rotations"], theirs["ct_mults"], theirs["depth_consumed"])
         assert mine.pt_mults == theirs["pt_mults"] + 1
         assert mine.adds == theirs["adds"] + 32 + 10 + 1
+
+
+def _one_layer_model(n_i, n_o, seed=3):
+    rng = np.random.default_rng(seed)
+    grid = GridMatrix.uniform(n_i, 5, 3, -1.0, 1.0)
+    silu = Polynomial((0.0, 0.5, 0.2, 0.0, -0.01))  # a fixed well-conditioned activation polynomial
+    layer = mdl.KanLayer(W_b=rng.normal(0, 0.3, (n_o, n_i)), S=rng.normal(0, 0.3, (n_o, n_i, grid.n_basis)),
+                         grid=grid, silu_poly=silu)
+    return mdl.KanModel(layers=[layer], input_shape=(1, 1, n_i))
+
+
+def test_spline_branch_tiles_when_packing_overflows():
+    """Beyond the reference (PackingOverflow, bspline.py:151-154): a layer whose
+    repeat packing exceeds the slot vector runs its B-spline branch tiled over
+    several ciphertexts. n_i = 6 at 64 slots needs two tiles of 3 features
+    (3 * 16 <= 64 < 6 * 16); the decrypted output equals the same model run
+    untiled at 128 slots and the plaintext twin of the engine's schedule, with
+    the untiled depth."""
+    model = _one_layer_model(6, 2)
+    layer = model.layers[0]
+    pcfg = inf.PipelineConfig()
+    depth = inf.plan_model(model, pcfg).total
+    assert inf.spline_tiles(layer, 64) == 2 and inf.spline_tiles(layer, 128) == 1
+    X = np.random.default_rng(5).uniform(-0.9, 0.9, (2, 6))
+    small, big = oracle_backend(depth, log_n=7), oracle_backend(depth, log_n=8)
+    o_small, st_small = inf.model_forward_he(model, inf.encrypt_input(X, model, small), pcfg)
+    o_big, st_big = inf.model_forward_he(model, inf.encrypt_input(X, model, big), pcfg)
+    d_small, d_big = small.decrypt(o_small)[:, :2], big.decrypt(o_big)[:, :2]
+    cs = build_composite_sign()
+    twin = np.stack([mdl.model_forward_plain(model, x, "mirrored", cs, "lazy", schedule="cheb") for x in X])
+    assert np.abs(d_small - d_big).max() < TOL
+    assert np.abs(d_small - twin).max() < TOL
+    assert st_small.total.depth_consumed == st_big.total.depth_consumed == depth
+    # two tiles: twice the spline-branch products, one extra rotation to bring tile 1 forward
+    assert st_small.total.ct_mults > st_big.total.ct_mults
+    # the reference's own packing refuses this shape
+    from paper_2409_07751_b200.errors import PackingOverflow
+    from paper_2409_07751_b200.bspline import repeat_pack
+    with pytest.raises(PackingOverflow):
+        repeat_pack(inf.encrypt_input(X, model, small), layer.g, layer.k, layer.n_i)
