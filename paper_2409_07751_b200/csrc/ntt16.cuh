@@ -82,20 +82,30 @@ __device__ __forceinline__ double f_center(double x, const FpMod &m) {
 __device__ __forceinline__ double u2d(uint64_t x) {  // exact for x < 2^52
     return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), kTwo52);
 }
+// Canonical residue of the exact integer x (|x| < 2^51). The centred remainder c lies in
+// [-q/2 - 1, q/2 + 1], so c + q is a positive integer below 2^52: adding 2^52 + q (exact:
+// q < 2^51) leaves it in the low mantissa bits, and the final conditional subtraction
+// runs on the integer pipe — four FP64-pipe operations instead of the eight of a
+// compare-and-add chain in doubles (the FP64 pipe is what bounds the NTT).
 __device__ __forceinline__ uint64_t d2canon(double x, const FpMod &m) {
-    double c = f_center(x, m);
-    c = c < 0.0 ? __dadd_rn(c, m.q) : c;
-    c = c >= m.q ? __dsub_rn(c, m.q) : c;
-    return (uint64_t)__double_as_longlong(__dadd_rn(c, kTwo52)) & 0xFFFFFFFFFFFFFull;
+    const double c = f_center(x, m);
+    const uint64_t v =
+        (uint64_t)__double_as_longlong(__dadd_rn(c, __dadd_rn(kTwo52, m.q))) & 0xFFFFFFFFFFFFFull;
+    const uint64_t q = (uint64_t)__double_as_longlong(__dadd_rn(m.q, kTwo52)) & 0xFFFFFFFFFFFFFull;
+    return v >= q ? v - q : v;
 }
 
+// Cooley-Tukey butterfly. Large primes (2^47 <= q < 2^50) recentre after every SECOND
+// stage (`cen`): |f_mulmod(y)| <= (1/2 + |y| 2^-53) q, so from |x| <= q/2 one stage gives
+// |x| <= 1.07 q and the next |x| <= 1.7 q — still an exact integer in a double and, as
+// the multiplicand of the following stage, below the 2^51 that keeps f_mulmod exact.
 template <bool kBig>
-__device__ __forceinline__ void ct_f(double &x, double &y, double2 w, const FpMod &m) {
+__device__ __forceinline__ void ct_f(double &x, double &y, double2 w, const FpMod &m, bool cen = true) {
     const double r = f_mulmod(y, w.x, w.y, m.q);
     const double U = x;
     x = __dadd_rn(U, r);
     y = __dsub_rn(U, r);
-    if (kBig) {
+    if (kBig && cen) {
         x = f_center(x, m);
         y = f_center(y, m);
     }
@@ -103,13 +113,17 @@ __device__ __forceinline__ void ct_f(double &x, double &y, double2 w, const FpMo
 // Gentleman-Sande butterfly. The sum is recentred only when `center` (small primes
 // recentre at stages 6, 4 and 2 only: |x| stays below 6q < 2^50, inside the exact
 // range of f_mulmod and f_center); the large prime recentres every stage.
+// The large prime recentres sum and product after every second stage (`cen_big`, the
+// odd stages): from |x| <= q/2 an uncentred stage leaves |x| <= q, so the next stage's
+// difference stays below 2 q < 2^51.
 template <bool kBig>
-__device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMod &m, bool center = true) {
+__device__ __forceinline__ void gs_f(double &x, double &y, double2 w, const FpMod &m, bool center = true,
+                                     bool cen_big = true) {
     const double U = x, V = y;
     const double sum = __dadd_rn(U, V);
-    x = (kBig || center) ? f_center(sum, m) : sum;
+    x = (kBig ? cen_big : center) ? f_center(sum, m) : sum;
     y = f_mulmod(__dsub_rn(U, V), w.x, w.y, m.q);
-    if (kBig) y = f_center(y, m);
+    if (kBig && cen_big) y = f_center(y, m);
 }
 
 // The between-phase buffer is written once and read once by the cluster: its
@@ -173,7 +187,7 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m);
+            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m, s & 1);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) sm[(k + 16 * u) * kTc + c] = x[u];
@@ -185,11 +199,12 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m);
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, (s & 1) && s != 7);
     }
 #pragma unroll
     // no recentre for small primes: |x| < 13 q < 2^51 and the row phase starts with the
-    // twist multiply (f_mulmod, exact for |x| < 2^51); the large prime is centred already
+    // twist multiply (f_mulmod, exact for |x| < 2^51); the large prime leaves stage 7 with
+    // |x| <= 1.7 q < 2^51 as well
     for (int v = 0; v < 16; ++v) st_inter(inter + (16 * k + v) * 256 + col, x[v]);
 }
 
@@ -215,19 +230,15 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
     for (int u = 0; u < 8; ++u) {
         const double2 ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
         const double a = f_mulmod(x[u], ta.x, ta.y, m.q), b = f_mulmod(x[u + 8], tb.x, tb.y, m.q);
-        x[u] = __dadd_rn(a, b);
+        x[u] = __dadd_rn(a, b);  // |a|, |b| <= 0.72 q: an uncentred stage for the large prime too
         x[u + 8] = __dsub_rn(a, b);
-        if (kBig) {
-            x[u] = f_center(x[u], m);
-            x[u + 8] = f_center(x[u + 8], m);
-        }
     }
 #pragma unroll
     for (int sp = 1; sp < 4; ++sp) {
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m);
+            if (!(u & d)) ct_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m, sp & 1);
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = x[u];
@@ -242,7 +253,7 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
         const int d = 128 >> sp;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m);
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m, (sp & 1) && sp != 7);  // d2canon centres
     }
     __syncwarp();
     uint64_t *su = reinterpret_cast<uint64_t *>(srow);
@@ -331,7 +342,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 128 >> sp;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m, !(sp & 1));
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m, !(sp & 1), sp & 1);
     }
     __syncwarp();
 #pragma unroll
@@ -344,7 +355,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m, !(sp & 1));
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m, !(sp & 1), sp & 1);
     }
     // stage 0 (pairs c, c+128, twiddle Ti[1]) fused with the untwist: the table holds
     // tau^-1(r, c) for c < 128 and tau^-1(r, c) * Ti[1] for c >= 128
@@ -376,7 +387,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, !(s & 1));
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, !(s & 1), s & 1);
     }
 #pragma unroll
     for (int v = 0; v < 16; ++v) sm[(16 * k + v) * kTc + c] = x[v];
@@ -388,7 +399,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m, !(s & 1));
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m, !(s & 1), s & 1);
     }
     // stage 0 (twiddle Ti[1]) fused with the N^-1 scaling: niw = N^-1 * Ti[1]
 #pragma unroll

@@ -208,3 +208,41 @@ def test_ragged_batches_bitexact(gpu_lib, B):
     _same(g, o, g.mul(ga, 0.75), o.mul(oa, 0.75), f"mul_const B={B}")
     for cg, co in zip(g.rotate_many(ga, [1, 2, 7]), o.rotate_many(oa, [1, 2, 7])):
         _same(g, o, cg, co, f"hoisted B={B}")
+
+
+def test_ntt_large_primes_extreme_inputs(gpu_lib):
+    """Forward / inverse NTT at the config-2 primes (all just below 2^50: the
+    kernels' large-prime path, which recentres every second stage) on inputs
+    that push the lazy bounds: all q - 1, alternating 0 / q - 1 at several
+    strides, (q - 1) / 2, and uniform draws. GPU == oracle exactly, and the
+    inverse returns the input."""
+    from oracle.engine import OracleEngine
+    from paper_2409_07751_b200.engine import GpuEngine
+    p = microbench_params()
+    ge, oe = GpuEngine(p), OracleEngine(p)
+    mods = np.array(list(p.q) + list(p.p), dtype=np.uint64)
+    assert mods.min() >= (1 << 47) and mods.max() < (1 << 50)
+    nl, N = len(mods), p.n
+    rng = np.random.default_rng(11)
+    pats = [np.broadcast_to(mods[:, None] - 1, (nl, N)).copy()]
+    idx = np.arange(N)
+    for stride in (1, 2, 256, 257, 32768):
+        pats.append(np.where(((idx // stride) & 1)[None, :] == 1, mods[:, None] - 1, 0).astype(np.uint64))
+    pats.append(np.broadcast_to((mods[:, None] - 1) // 2, (nl, N)).copy())
+    pats.append((rng.integers(0, 1 << 62, size=(nl, N), dtype=np.uint64) % mods[:, None]).astype(np.uint64))
+    x = np.ascontiguousarray(np.stack(pats, axis=1).astype(np.uint64))  # [nl][B][N]
+    B = x.shape[1]
+    gb, ob = ge.put_u64(x), oe.put_u64(x)
+    ge.call("hk_ntt_fwd", ge.addr(gb), 0, nl, B)
+    oe.call("hk_ntt_fwd", oe.addr(ob), 0, nl, B)
+    ge.sync()
+    assert np.array_equal(ge.get_u64(gb), oe.get_u64(ob))
+    ge.call("hk_ntt_inv", ge.addr(gb), 0, nl, B)
+    ge.sync()
+    assert np.array_equal(ge.get_u64(gb), x.ravel())
+    # the inverse on its own extreme inputs
+    gb, ob = ge.put_u64(x), oe.put_u64(x)
+    ge.call("hk_ntt_inv", ge.addr(gb), 0, nl, B)
+    oe.call("hk_ntt_inv", oe.addr(ob), 0, nl, B)
+    ge.sync()
+    assert np.array_equal(ge.get_u64(gb), oe.get_u64(ob))
