@@ -432,12 +432,13 @@ __device__ __forceinline__ double fold_prod(const uint64_t *a, const uint64_t *b
 // each thread owns one (coefficient k, limb t) and walks `bb` batch entries so
 // the key pair, the galois index and the address math are paid once.
 // grid (N/min(N,256) * B/bb, ne); every residue is exact, results canonical.
-template <int ND, bool FOLD>
-__global__ void __launch_bounds__(256, 3) k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
-                                                const uint64_t *__restrict__ dm, int alpha, int ne, int l, int n_q,
-                                                int nm, int ksp0, int log_n, int bb, const uint64_t *__restrict__ key,
-                                                uint32_t g, uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1,
-                                                const double2 *__restrict__ fmod, long long BN, int accum, FoldD fd) {
+template <int ND, bool FOLD, bool kBig>
+__device__ __forceinline__ void key_ip_body(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
+                                            const uint64_t *__restrict__ dm, int alpha, int ne, int l, int n_q,
+                                            int nm, int ksp0, int log_n, int bb, const uint64_t *__restrict__ key,
+                                            uint32_t g, uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1,
+                                            const double2 *__restrict__ fmod, long long BN, int accum,
+                                            const FoldD &fd) {
     using namespace ntt16;
     const int N = 1 << log_n;
     const int kblocks = N / (int)blockDim.x;
@@ -448,6 +449,10 @@ __global__ void __launch_bounds__(256, 3) k_key_ip(const uint64_t *__restrict__ 
     const int kr = t <= l ? t : ksp0 + (t - l - 1);  // key row: nm rows, specials from ksp0
     const double2 fm = fmod[m];
     const FpMod M{fm.x, fm.y};
+    // Small primes (q < 2^47, every prime but q_0) never recentre: each product is below
+    // 0.75 q and at most 8 + 5 of them add up, far inside the 2^51 > 16 q that keeps
+    // f_mulmod and d2canon exact; the large prime keeps the centring steps.
+    auto cen = [&](double v) { return kBig ? f_center(v, M) : v; };
     const int ks = g == 1u ? k : (int)auto_src((uint32_t)k, g, log_n);
     double w0[ND], v0[ND], w1[ND], v1[ND];
 #pragma unroll
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(256, 3) k_key_ip(const uint64_t *__restrict__ 
                     double y = u2d(ry[u]);
                     if (xm) {  // relinearisation: d = a1 (.) b1 on the fly
                         const double w = u2d(rm[u]);
-                        y = f_center(f_mulmod(y, w, __dmul_rn(w, M.qinv), M.q), M);
+                        y = cen(f_mulmod(y, w, __dmul_rn(w, M.qinv), M.q));
                     }
 #pragma unroll
                     for (int j = 0; j < ND; ++j)
@@ -522,26 +527,26 @@ __global__ void __launch_bounds__(256, 3) k_key_ip(const uint64_t *__restrict__ 
                     double d1 = __dadd_rn(f_mulmod(a0, b1, b1q, M.q), f_mulmod(a1, b0, b0q, M.q));
                     if (fd.a2) {
                         d0 = __dadd_rn(d0, fold_prod(fd.a2, fd.b2, o, o, M));
-                        d1 = f_center(d1, M);
+                        d1 = cen(d1);
                         d1 = __dadd_rn(d1, __dadd_rn(fold_prod(fd.a2, fd.b2, o, fd.pb2 + o, M),
                                                      fold_prod(fd.a2, fd.b2, fd.pa2 + o, o, M)));
                     }
                     if (fd.x) {
                         const double kk = u2d(fd.k.v[t]), kq = __dmul_rn(kk, M.qinv);
-                        d0 = __dadd_rn(f_center(d0, M), f_mulmod(u2d(fd.x[o]), kk, kq, M.q));
-                        d1 = __dadd_rn(f_center(d1, M), f_mulmod(u2d(fd.x[fd.px + o]), kk, kq, M.q));
+                        d0 = __dadd_rn(cen(d0), f_mulmod(u2d(fd.x[o]), kk, kq, M.q));
+                        d1 = __dadd_rn(cen(d1), f_mulmod(u2d(fd.x[fd.px + o]), kk, kq, M.q));
                     }
                     const double pm = u2d(fd.pmod[t].x), pq = __dmul_rn(pm, M.qinv);
-                    s0 = f_center(__dadd_rn(s0, f_mulmod(f_center(d0, M), pm, pq, M.q)), M);
-                    s1 = f_center(__dadd_rn(s1, f_mulmod(f_center(d1, M), pm, pq, M.q)), M);
+                    s0 = cen(__dadd_rn(s0, f_mulmod(cen(d0), pm, pq, M.q)));
+                    s1 = cen(__dadd_rn(s1, f_mulmod(cen(d1), pm, pq, M.q)));
                 }
 #pragma unroll
                 for (int j = 0; j < ND; ++j) {  // |f_mulmod| < 2.5 q: recentre every second term
                     s0 = __dadd_rn(s0, f_mulmod(x[j], w0[j], v0[j], M.q));
                     s1 = __dadd_rn(s1, f_mulmod(x[j], w1[j], v1[j], M.q));
                     if (j & 1) {
-                        s0 = f_center(s0, M);
-                        s1 = f_center(s1, M);
+                        s0 = cen(s0);
+                        s1 = cen(s1);
                     }
                 }
                 o0[u * N] = d2canon(s0, M);
@@ -554,6 +559,21 @@ __global__ void __launch_bounds__(256, 3) k_key_ip(const uint64_t *__restrict__ 
         o0 += 2 * N;
         o1 += 2 * N;
     }
+}
+
+template <int ND, bool FOLD>
+__global__ void __launch_bounds__(256, 3) k_key_ip(const uint64_t *__restrict__ ext, const uint64_t *__restrict__ d,
+                                                const uint64_t *__restrict__ dm, int alpha, int ne, int l, int n_q,
+                                                int nm, int ksp0, int log_n, int bb, const uint64_t *__restrict__ key,
+                                                uint32_t g, uint64_t *__restrict__ acc0, uint64_t *__restrict__ acc1,
+                                                const double2 *__restrict__ fmod, long long BN, int accum, FoldD fd) {
+    const int t = blockIdx.y;
+    if (fmod[t <= l ? t : n_q + (t - l - 1)].x < (double)ntt16::kSmallPrime)
+        key_ip_body<ND, FOLD, false>(ext, d, dm, alpha, ne, l, n_q, nm, ksp0, log_n, bb, key, g, acc0, acc1, fmod, BN,
+                                     accum, fd);
+    else
+        key_ip_body<ND, FOLD, true>(ext, d, dm, alpha, ne, l, n_q, nm, ksp0, log_n, bb, key, g, acc0, acc1, fmod, BN,
+                                    accum, fd);
 }
 
 // out (+)= sigma_g(in) over [l+1][B][N] ; grid (BN/256, l+1)
