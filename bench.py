@@ -594,22 +594,23 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="ciphertexts per GPU")
     ap.add_argument("--dnum", type=int, default=3, help="key-switching digits over the full chain")
     ap.add_argument("--chunk", type=int, default=None,
-                    help="ciphertexts per batched launch (default: the whole batch; 32 for c4, 8 for c5)")
+                    help="ciphertexts per batched launch (default: the whole batch; 32 for c4, 16 for c5)")
     ap.add_argument("--log-n", type=int, default=None,
-                    help="ring degree (default 16; 17 for c5, whose 33792 packed slots need S=2^16)")
+                    help="ring degree (default 16: c5's 33792 packed slots run as two feature tiles; "
+                         "17 runs it untiled and is the 128-bit-secure ring for depth 36)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-float-sim", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the config-2 primitive microbench")
     args = ap.parse_args()
     if args.log_n is None:
-        args.log_n = 17 if args.config == "c5" else 16
+        args.log_n = 16
     if args.chunk is None:
         # c1 and c3 run their whole batch per launch; c4 / c5 hold 80 / 157 hoisted
         # BSGS baby steps at once, which bounds them to 32 at N = 2^16 and 8 at N = 2^17
         if args.log_n > 16:
             args.chunk = 8 if args.config == "c5" else 32
         else:
-            args.chunk = {"c4": 32, "c5": 8}.get(args.config, 128)
+            args.chunk = {"c4": 32, "c5": 16}.get(args.config, 128)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":

@@ -52,6 +52,14 @@ struct DiscardInter : std::false_type {};
 template <class E>
 struct DiscardInter<E, std::enable_if_t<E::kDiscardInter>> : std::true_type {};
 
+// Prologues may produce their value on the FP64 pipe: `dval(l, P, idx, m, big)` returns
+// the input as an exact integer in a double, |x| <= 1.5 q for small primes and centred
+// (|x| <= q/2) for the large one, instead of a canonical u64 that the kernel converts.
+template <class Pr, class = void>
+struct HasDval : std::false_type {};
+template <class Pr>
+struct HasDval<Pr, std::void_t<decltype(&Pr::dval)>> : std::true_type {};
+
 constexpr int kLogN = 16;
 constexpr int kN = 1 << kLogN;
 constexpr int kCl = 16;                      // column tiles / row blocks of 16 per polynomial
@@ -93,6 +101,12 @@ __device__ __forceinline__ uint64_t d2canon(double x, const FpMod &m) {
         (uint64_t)__double_as_longlong(__dadd_rn(c, __dadd_rn(kTwo52, m.q))) & 0xFFFFFFFFFFFFFull;
     const uint64_t q = (uint64_t)__double_as_longlong(__dadd_rn(m.q, kTwo52)) & 0xFFFFFFFFFFFFFull;
     return v >= q ? v - q : v;
+}
+
+template <bool kBig, class Pr>
+__device__ __forceinline__ double pro_value(const Pr &pro, int l, long long P, int idx, const FpMod &m) {
+    if constexpr (HasDval<Pr>::value) return pro.dval(l, P, idx, m, kBig);
+    else return u2d(pro(l, P, idx));
 }
 
 // Cooley-Tukey butterfly. Large primes (2^47 <= q < 2^50) recentre after every SECOND
@@ -333,7 +347,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
     const int k = threadIdx.x & 15;
     double x[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = u2d(pro(l, P, r * 256 + k + 16 * u));
+    for (int u = 0; u < 16; ++u) srow[pad16(k + 16 * u)] = pro_value<kBig>(pro, l, P, r * 256 + k + 16 * u, m);
     __syncwarp();
 #pragma unroll
     for (int v = 0; v < 16; ++v) x[v] = srow[pad16(16 * k + v)];

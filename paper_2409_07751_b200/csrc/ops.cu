@@ -869,6 +869,19 @@ struct ProD2 {
     __device__ __forceinline__ uint64_t operator()(int l, long long P, int idx) const {
         return T.d(2, l, (long long)l * BN + ((P - (long long)l * B) << log_n) + idx);
     }
+    // the same product on the FP64 pipe (ntt16::HasDval): exact two-product Shoup step on
+    // the operands instead of a 128-bit Barrett product on the integer pipe
+    __device__ __forceinline__ double dval(int l, long long P, int idx, const ntt16::FpMod &m, bool big) const {
+        using namespace ntt16;
+        const long long o = (long long)l * BN + ((P - (long long)l * B) << log_n) + idx;
+        const double b = u2d(T.b[T.pb + o]);
+        double r = f_mulmod(u2d(T.a[T.pa + o]), b, __dmul_rn(b, m.qinv), m.q);
+        if (T.a2) {
+            const double b2 = u2d(T.b2[T.pb2 + o]);
+            r = __dadd_rn(r, f_mulmod(u2d(T.a2[T.pa2 + o]), b2, __dmul_rn(b2, m.qinv), m.q));
+        }
+        return big ? f_center(r, m) : r;
+    }
 };
 // Merged ModDown + rescale of both halves of a relinearised product: launches
 // run over 2B "samples" pb = 2 b + p, so the two halves of one sample sit in
