@@ -103,6 +103,35 @@ __device__ __forceinline__ uint64_t d2canon(double x, const FpMod &m) {
     return v >= q ? v - q : v;
 }
 
+// Epilogues of the form out = (operand - v) * w (ModDown, rescale and their merged form)
+// may finish on the FP64 pipe: with a nested `Pre`, `prep` as above and
+//   uint64_t operand(const Pre &)        the canonical operand the output is subtracted from
+//     (or double operand_d(const Pre &, int l, const FpMod &, bool big): the operand as an
+//      exact integer in a double, |.| <= 2 q, centred when `big`)
+//   double2 factor(int l)                {w, unused} as an exact integer in a double
+//   void store(l, P, idx, pre, uint64_t) consume the canonical product
+// the row phase forms (operand - x) * w from the UNCANONICALISED transform output x with
+// one exact two-product Shoup step and canonicalises once — instead of canonicalising x
+// and then spending ~25 integer instructions on a modular subtraction and a 64-bit Shoup
+// multiply (profiles/r2_notes.md §13).
+template <class E, class = void>
+struct HasFactor : std::false_type {};
+template <class E>
+struct HasFactor<E, std::void_t<decltype(&E::factor)>> : std::true_type {};
+template <class E, class = void>
+struct HasOperandD : std::false_type {};
+template <class E>
+struct HasOperandD<E, std::void_t<decltype(&E::operand_d)>> : std::true_type {};
+
+// Inverse-NTT epilogues that only multiply by a per-limb constant (the basis-conversion
+// prescale) offer `uint64_t scale(int l)` and `store(l, P, idx, v)`: the kernel folds the
+// constant into the N^-1 factors of its last stage, so the scaling costs nothing per
+// element (it was a 64-bit integer Shoup multiply per output).
+template <class E, class = void>
+struct HasScale : std::false_type {};
+template <class E>
+struct HasScale<E, std::void_t<decltype(&E::scale)>> : std::true_type {};
+
 template <bool kBig, class Pr>
 __device__ __forceinline__ double pro_value(const Pr &pro, int l, long long P, int idx, const FpMod &m) {
     if constexpr (HasDval<Pr>::value) return pro.dval(l, P, idx, m, kBig);
@@ -191,7 +220,7 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
     const int c = threadIdx.x % kTc, k = threadIdx.x / kTc, col = tile * kTc + c;
     double x[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) x[u] = u2d(pro(l, P, (k + 16 * u) * 256 + col));
+    for (int u = 0; u < 16; ++u) x[u] = pro_value<kBig>(pro, l, P, (k + 16 * u) * 256 + col, m);
     if (stage) {
         stage_table(T, Tg);
         __syncthreads();
@@ -270,19 +299,45 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
             if (!(v & d)) ct_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m, (sp & 1) && sp != 7);  // d2canon centres
     }
     __syncwarp();
-    uint64_t *su = reinterpret_cast<uint64_t *>(srow);
+    if constexpr (HasFactor<Epi>::value) {
+        // |x| <= 13 q (small primes) or 1.7 q (the large prime, recentred here): the
+        // difference from a canonical operand stays below 2^51
 #pragma unroll
-    for (int v = 0; v < 16; ++v) su[pad16(16 * k + v)] = d2canon(x[v], m);
-    __syncwarp();
-    if constexpr (HasPrep<Epi>::value) {
-        typename Epi::Pre pre[16];
+        for (int v = 0; v < 16; ++v) srow[pad16(16 * k + v)] = kBig ? f_center(x[v], m) : x[v];
+        __syncwarp();
+        const double w = epi.factor(l).x, wq = __dmul_rn(w, m.qinv);
+        // operand loads in flight together: all 16 of the thread, or two groups of 8 when an
+        // operand record is wider than one word (register budget: 64 per thread)
+        constexpr int kG = sizeof(typename Epi::Pre) > 8 ? 8 : 16;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) pre[u] = epi.prep(l, P, r * 256 + k + 16 * u);
+        for (int u0 = 0; u0 < 16; u0 += kG) {
+            typename Epi::Pre pre[kG];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) epi.fin(l, P, r * 256 + k + 16 * u, pre[u], su[pad16(k + 16 * u)]);
+            for (int u = 0; u < kG; ++u) pre[u] = epi.prep(l, P, r * 256 + k + 16 * (u0 + u));
+#pragma unroll
+            for (int u = 0; u < kG; ++u) {
+                double od;
+                if constexpr (HasOperandD<Epi>::value) od = epi.operand_d(pre[u], l, m, kBig);
+                else od = u2d(epi.operand(pre[u]));
+                const double t = __dsub_rn(od, srow[pad16(k + 16 * (u0 + u))]);
+                epi.store(l, P, r * 256 + k + 16 * (u0 + u), pre[u], d2canon(f_mulmod(t, w, wq, m.q), m));
+            }
+        }
     } else {
+        uint64_t *su = reinterpret_cast<uint64_t *>(srow);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) epi(l, P, r * 256 + k + 16 * u, su[pad16(k + 16 * u)]);
+        for (int v = 0; v < 16; ++v) su[pad16(16 * k + v)] = d2canon(x[v], m);
+        __syncwarp();
+        if constexpr (HasPrep<Epi>::value) {
+            typename Epi::Pre pre[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) pre[u] = epi.prep(l, P, r * 256 + k + 16 * u);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) epi.fin(l, P, r * 256 + k + 16 * u, pre[u], su[pad16(k + 16 * u)]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) epi(l, P, r * 256 + k + 16 * u, su[pad16(k + 16 * u)]);
+        }
     }
 }
 
@@ -423,7 +478,10 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
         x[u + 8] = f_mulmod(__dsub_rn(U, V), niw.x, niw.y, m.q);
     }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) epi(l, P, (k + 16 * u) * 256 + col, d2canon(x[u], m));
+    for (int u = 0; u < 16; ++u) {
+        if constexpr (HasScale<Epi>::value) epi.store(l, P, (k + 16 * u) * 256 + col, d2canon(x[u], m));
+        else epi(l, P, (k + 16 * u) * 256 + col, d2canon(x[u], m));
+    }
 }
 
 template <class Pro, class Epi, int CPP>
@@ -444,6 +502,14 @@ __global__ void __launch_bounds__(kTh, 4)
     __syncthreads();
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
     const int rs = threadIdx.x >> 4;
+    double2 ni = ninv[2 * mi], niw = ninv[2 * mi + 1];
+    if constexpr (HasScale<Epi>::value) {  // N^-1 s and N^-1 Ti[1] s (|.| <= 0.75 q) with their /q companions
+        const double sd = u2d(epi.scale(l)), sq = __dmul_rn(sd, m.qinv);
+        ni.x = f_mulmod(ni.x, sd, sq, m.q);
+        ni.y = __dmul_rn(ni.x, m.qinv);
+        niw.x = f_mulmod(niw.x, sd, sq, m.q);
+        niw.y = __dmul_rn(niw.x, m.qinv);
+    }
     if (m.q < (double)kSmallPrime) {
         for (int t = 0; t < kT; ++t) {
             if (t) __syncwarp();
@@ -453,7 +519,7 @@ __global__ void __launch_bounds__(kTh, 4)
         else __syncthreads();
         for (int t = 0; t < kT; ++t) {
             if (t) __syncthreads();
-            inv_cols<false>(epi, l, P, inter, c * kT + t, st, ninv[2 * mi], ninv[2 * mi + 1], m, smd);
+            inv_cols<false>(epi, l, P, inter, c * kT + t, st, ni, niw, m, smd);
         }
     } else {
         for (int t = 0; t < kT; ++t) {
@@ -464,7 +530,7 @@ __global__ void __launch_bounds__(kTh, 4)
         else __syncthreads();
         for (int t = 0; t < kT; ++t) {
             if (t) __syncthreads();
-            inv_cols<true>(epi, l, P, inter, c * kT + t, st, ninv[2 * mi], ninv[2 * mi + 1], m, smd);
+            inv_cols<true>(epi, l, P, inter, c * kT + t, st, ni, niw, m, smd);
         }
     }
 }

@@ -690,6 +690,18 @@ struct ProRsBcast {
         }
         return neg ? (r ? q - r : 0) : r;
     }
+    // ntt16::HasDval: the centred remainder itself as a signed double. `fast` (set on the
+    // host) says |remainder| <= q_l / 2 <= 4 q_t for every target prime, which the forward
+    // NTT's lazy range absorbs (8 stages from 4 q stay below 10 q < 2^51 for q < 2^47; for
+    // the large prime q_0 the remainder is already below q_0 / 2).
+    int fast = 0;
+    __device__ __forceinline__ double dval(int l, long long P, int idx, const ntt16::FpMod &, bool) const {
+        if (!fast) return ntt16::u2d((*this)(l, P, idx));
+        const long long pb = P - (long long)l * B2;
+        const uint64_t x = L[(pb << log_n) + idx];
+        const double xd = ntt16::u2d(x);
+        return x > (ql >> 1) ? __dsub_rn(xd, ntt16::u2d(ql)) : xd;
+    }
 };
 
 // NTT epilogue: out[p][l][b] = (X - v) * q_la^-1
@@ -700,20 +712,54 @@ struct EpiRescale {
     uint64_t *out;
     const ulonglong2 *qinv;
     int B;
-    using Pre = uint64_t;  // X (two-phase epilogue, ntt16::HasPrep)
-    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
-        const int pb = (int)(P - (long long)l * 2 * B), p = pb >= B ? 1 : 0, b = pb - p * B;
-        return src(p, l, b, idx);
-    }
-    __device__ __forceinline__ void fin(int l, long long P, int idx, Pre x, uint64_t v) const {
+    // integer path (generic rings, N = 2^17 halves)
+    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         const int pb = (int)(P - (long long)l * 2 * B), p = pb >= B ? 1 : 0, b = pb - p * B;
         const uint64_t q = src.mq[l].q;
         const ulonglong2 w = qinv[l];
         __stcs(out + ((long long)p * src.la + l) * src.BN + ((long long)b << src.log_n) + idx,
-               mul_shoup(sub_mod(x, v, q), w.x, w.y, q));
+               mul_shoup(sub_mod(src(p, l, b, idx), v, q), w.x, w.y, q));
     }
-    __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
-        fin(l, P, idx, prep(l, P, idx), v);
+    // FP64 finish (ntt16::HasFactor / HasOperandD): the raw operands are loaded in `prep`
+    // (all 16 of a thread before its first store) and X is formed as a double
+    struct Pre2 {
+        uint64_t a, b;
+    };
+    static constexpr bool kTwo = KIND == SRC_MULPT || KIND == SRC_SUM2;  // two raw operands per output
+    using Pre = std::conditional_t<kTwo, Pre2, uint64_t>;
+    __device__ __forceinline__ Pre prep(int l, long long P, int idx) const {
+        const int pb = (int)(P - (long long)l * 2 * B), p = pb >= B ? 1 : 0, b = pb - p * B;
+        const long long o = ((long long)p * (src.la + 1) + l) * src.BN + ((long long)b << src.log_n) + idx;
+        if constexpr (kTwo) {
+            if (KIND == SRC_SUM2) return Pre2{src.a[o], src.a2[o]};
+            return Pre2{src.a[o], src.pt[(((long long)l * src.pb + (src.pb == 1 ? 0 : b)) << src.log_n) + idx]};
+        } else {
+            if (KIND == SRC_MAC) return src(p, l, b, idx);
+            return src.a[o];
+        }
+    }
+    __device__ __forceinline__ double operand_d(const Pre &pr, int l, const ntt16::FpMod &m, bool big) const {
+        using namespace ntt16;
+        if constexpr (kTwo) {
+            const double a = u2d(pr.a), y = u2d(pr.b);
+            if (KIND == SRC_SUM2) {
+                const double s2 = __dadd_rn(a, y);
+                return big ? f_center(s2, m) : s2;
+            }
+            return f_mulmod(a, y, __dmul_rn(y, m.qinv), m.q);
+        } else {
+            const double a = u2d(pr);
+            if (KIND == SRC_MULCONST) {
+                const double y = u2d(src.k.v[l]);
+                return f_mulmod(a, y, __dmul_rn(y, m.qinv), m.q);
+            }
+            return a;
+        }
+    }
+    __device__ __forceinline__ double2 factor(int l) const { return make_double2(ntt16::u2d(qinv[l].x), 0.0); }
+    __device__ __forceinline__ void store(int l, long long P, int idx, const Pre &, uint64_t r) const {
+        const int pb = (int)(P - (long long)l * 2 * B), p = pb >= B ? 1 : 0, b = pb - p * B;
+        __stcs(out + ((long long)p * src.la + l) * src.BN + ((long long)b << src.log_n) + idx, r);
     }
 };
 
@@ -726,6 +772,9 @@ struct EpiScale {
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         out[(P << log_n) + idx] = mul_shoup(v, inv[l], inv_sh[l], mq[mi0 + l].q);
     }
+    // ntt16::HasScale: the kernel folds inv[l] into its N^-1 stage
+    __device__ __forceinline__ uint64_t scale(int l) const { return inv[l]; }
+    __device__ __forceinline__ void store(int, long long P, int idx, uint64_t v) const { out[(P << log_n) + idx] = v; }
 };
 // same, per-digit tables (ModUp sources at one level)
 struct EpiScaleDigits {
@@ -737,6 +786,12 @@ struct EpiScaleDigits {
         const int j = l / alpha, i = l - j * alpha;
         out[(P << log_n) + idx] = mul_shoup(v, inv[j][i], inv_sh[j][i], mq[l].q);
     }
+    // ntt16::HasScale
+    __device__ __forceinline__ uint64_t scale(int l) const {
+        const int j = l / alpha;
+        return inv[j][l - j * alpha];
+    }
+    __device__ __forceinline__ void store(int, long long P, int idx, uint64_t v) const { out[(P << log_n) + idx] = v; }
 };
 
 // NTT epilogue: ModDown finish (acc - v) * P^-1 (+ sigma_g(addend))
@@ -932,6 +987,15 @@ struct EpiMdRsY2 {  // out_p = aff((Y_p - v) (P q_l)^-1)
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         fin(l, P, idx, prep(l, P, idx), v);
     }
+    // FP64 finish (ntt16::HasFactor): out_p = aff((Y_p - v) (P q_l)^-1)
+    __device__ __forceinline__ uint64_t operand(const Pre &y) const { return y; }
+    __device__ __forceinline__ double2 factor(int l) const { return make_double2(ntt16::u2d(mqinv[l].x), 0.0); }
+    __device__ __forceinline__ void store(int l, long long P, int idx, const Pre &, uint64_t r) const {
+        const long long pb = P - (long long)l * 2 * B;
+        const int p = (int)(pb & 1);
+        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
+        __stcs(out + p * pout + o, aff.apply(p, l, r, mq[l].q));
+    }
 };
 // ModDown of both halves of a key switch (interleaved samples 2 b + p):
 // out_p = (acc_p - v) P^-1 (+ sigma_g(add_p))
@@ -968,6 +1032,16 @@ struct EpiModDown2 {
     }
     __device__ __forceinline__ void operator()(int l, long long P, int idx, uint64_t v) const {
         fin(l, P, idx, prep(l, P, idx), v);
+    }
+    // FP64 finish (ntt16::HasFactor): out_p = (acc_p - v) P^-1 (+ sigma_g(add_p))
+    __device__ __forceinline__ uint64_t operand(const Pre &pr) const { return pr.a; }
+    __device__ __forceinline__ double2 factor(int l) const { return make_double2(ntt16::u2d(pinv[l].x), 0.0); }
+    __device__ __forceinline__ void store(int l, long long P, int idx, const Pre &pr, uint64_t r) const {
+        const long long pb = P - (long long)l * 2 * B;
+        const int p = (int)(pb & 1);
+        const long long o = (long long)l * BN + ((pb >> 1) << log_n) + idx;
+        if (p ? add1 : add0) r = add_mod(r, pr.add, mq[l].q);
+        __stcs((p ? out1 : out0) + o, r);
     }
 };
 
@@ -1095,6 +1169,12 @@ static int rescale_fused(hk_ctx *c, const RsSrc<KIND> &src, int l, int B, uint64
     int rc = ntt16::launch_inv(c, L, l, 1, 2 * B, ProLast<KIND>{src, B}, ntt16::EpiPlain{L, c->log_n});
     if (rc) return rc;
     ProRsBcast pro{L, c->mod_h[l], 2 * B, c->log_n, c->d_modq};
+    static const int rs_fast = getenv("HK_RS_FAST") ? atoi(getenv("HK_RS_FAST")) : 1;  // A/B knob
+    pro.fast = rs_fast;
+    for (int t = 0; t < l; ++t)  // |remainder| <= q_l / 2 must stay within 4 q_t (below q_t for a large prime)
+        if ((c->mod_h[t] < ntt16::kSmallPrime && c->mod_h[l] / 2 > 4 * c->mod_h[t]) ||
+            (c->mod_h[t] >= ntt16::kSmallPrime && c->mod_h[l] / 2 >= c->mod_h[t]))
+            pro.fast = 0;
     EpiRescale<KIND> epi{src, out, c->d_rs_qinv + (size_t)l * c->n_q, B};
     return ntt16::launch_fwd(c, inter, 0, l, 2 * B, pro, epi, true);
 }
