@@ -97,7 +97,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred done;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, 0x4000;\n\t"  // suspend-time hint: idle roles sleep instead of spinning
         "@!done bra WAIT_%=;\n\t}\n" ::"r"(bar),
         "r"(parity)
         : "memory");
