@@ -67,6 +67,7 @@ def test_mirrored_plaintext_is_reference_bit_exact():
     cs = build_composite_sign()
     mine = np.stack([mdl.model_forward_plain(model, x, "mirrored", cs, "lazy") for x in X])
     assert np.array_equal(mine, g["mirrored"])
+    exact = np.stack([mdl.model_forward_plain(model, x, "exact") for x in X])
     assert np.array_equal(exact, g["exact"])
 
 
