@@ -221,8 +221,8 @@ struct hk_ctx {
     double2 *d_itwf;       // [n_mod][2^16] inverse twiddles, float64
     double2 *d_ninvf;      // [n_mod][2] {2^-16, 2^-16/q}, {2^-16 Ti[1], .../q} (inverse stage 0 fused)
     double2 *d_fmod;       // [n_mod] {q, 1/q} (every N)
-    double2 *d_twist;      // [n_mod][256][256] w^(c (2 brv8(r) + 1 - 256)), float64 {w, w/q} (rows)
-    double2 *d_itwist;     // [n_mod][256][256] inverse twist
+    double *d_twist;       // [n_mod][256][256] w^(c (2 brv8(r) + 1 - 256)) as float64 (rows; w/q formed in-register)
+    double *d_itwist;      // [n_mod][256][256] inverse twist
     ulonglong2 *d_n17;     // N = 2^17: [n_mod][4][2^16] radix-2 pre/post twists (ntt.cu)
     ulonglong2 *d_n17w;    // N = 2^17: [n_mod][2] {psi^(2^16), inverse}
     double2 *d_zeta;       // [2N]

@@ -242,13 +242,14 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     // Tables of the fused 2^16 kernels (ntt16.cuh), float64 {w, w/q}, stride 2^16 per prime:
     // N = 2^16 uses root psi; N = 2^17 runs each half through the 2^16 kernel with root
     // psi^2 after one radix-2 stage and a pre-twist by psi^-+i (ntt.cu, ntt17_*).
-    c->d_twf = c->d_itwf = c->d_ninvf = c->d_twist = c->d_itwist = nullptr;
+    c->d_twf = c->d_itwf = c->d_ninvf = nullptr;
+    c->d_twist = c->d_itwist = nullptr;
     c->d_n17 = nullptr;
     c->d_n17w = nullptr;
     if (c->log_n == 16 || c->log_n == 17) {
         const int H = 1 << 16;
         std::vector<double2> twf((size_t)nm * H), itwf((size_t)nm * H), ninvf(2 * (size_t)nm);
-        std::vector<double2> tws((size_t)nm * H), itws((size_t)nm * H);
+        std::vector<double> tws((size_t)nm * H), itws((size_t)nm * H);
         const uint64_t M2 = 2ull * H;
         for (int m = 0; m < nm; ++m) {
             const uint64_t q = c->mod_h[m];
@@ -278,8 +279,8 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
                     const size_t o = (size_t)m * H + (size_t)r * 256 + col;
                     const uint64_t tv = col < 128 ? t : h_mulmod(t, t1, q);
                     const uint64_t itv = col < 128 ? it : h_mulmod(it, ti1, q);
-                    tws[o] = make_double2((double)tv, (double)tv / qd);
-                    itws[o] = make_double2((double)itv, (double)itv / qd);
+                    tws[o] = (double)tv;
+                    itws[o] = (double)itv;
                     t = h_mulmod(t, base, q);
                     it = h_mulmod(it, ibase, q);
                 }

@@ -242,12 +242,12 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, (s & 1) && s != 7);
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, s & 1);
     }
 #pragma unroll
     // no recentre for small primes: |x| < 13 q < 2^51 and the row phase starts with the
-    // twist multiply (f_mulmod, exact for |x| < 2^51); the large prime leaves stage 7 with
-    // |x| <= 1.7 q < 2^51 as well
+    // twist multiply (f_mulmod, exact for |x| < 2^51); the large prime is centred (the twist's
+    // w / q is formed in-register, a 1.5 ulp estimate: |product| <= (1/2 + 1.5 |x| 2^-52) q)
     for (int v = 0; v < 16; ++v) st_inter(inter + (16 * k + v) * 256 + col, x[v]);
 }
 
@@ -259,11 +259,11 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
 // twiddles per row by one coalesced table element per coefficient.
 template <bool kBig, class Epi>
 __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, const double *inter, int r,
-                                        const double2 *__restrict__ tau, const double2 *st, const FpMod &m,
+                                        const double *__restrict__ tau, const double2 *st, const FpMod &m,
                                         double *srow) {
     const int k = threadIdx.x & 15;
     const double *rd = inter + r * 256;
-    const double2 *tr = tau + r * 256;
+    const double *tr = tau + r * 256;
     double x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = ld_inter(rd + k + 16 * u);
@@ -271,9 +271,12 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
     // tau(r, c) for c < 128 and tau(r, c) * T[1] for c >= 128
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-        const double2 ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
-        const double a = f_mulmod(x[u], ta.x, ta.y, m.q), b = f_mulmod(x[u + 8], tb.x, tb.y, m.q);
-        x[u] = __dadd_rn(a, b);  // |a|, |b| <= 0.72 q: an uncentred stage for the large prime too
+        // 8-byte table entries: w / q is one DMUL here instead of 8 more bytes per coefficient
+        // through L1 (the L1 / LSU path ran at 77 % beside an FP64 pipe at 70 %)
+        const double ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
+        const double a = f_mulmod(x[u], ta, __dmul_rn(ta, m.qinv), m.q);
+        const double b = f_mulmod(x[u + 8], tb, __dmul_rn(tb, m.qinv), m.q);
+        x[u] = __dadd_rn(a, b);  // |a|, |b| <= 1.1 q (0.7 q for the large prime): an uncentred stage
         x[u + 8] = __dsub_rn(a, b);
     }
 #pragma unroll
@@ -350,7 +353,7 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
 template <class Pro, class Epi, int CPP>
 __global__ void __launch_bounds__(kTh, 4)
     fwd_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ tw,
-               const double2 *__restrict__ twist, const FpMod *__restrict__ fm, Pro pro, Epi epi, int smaj) {
+               const double *__restrict__ twist, const FpMod *__restrict__ fm, Pro pro, Epi epi, int smaj) {
     constexpr int kT = kCl / CPP;
     extern __shared__ double smd[];
     double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(kTh, 4)
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = tw + (size_t)mi * kN;
-    const double2 *tau = twist + (size_t)mi * kN;
+    const double *tau = twist + (size_t)mi * kN;
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
     const int rs = threadIdx.x >> 4;
     if (m.q < (double)kSmallPrime) {
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(kTh, 4)
 // multiplication with tau^-1(r, c).
 template <bool kBig, class Pro>
 __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, double *inter, int r,
-                                        const double2 *__restrict__ itau, const double2 *st, const FpMod &m,
+                                        const double *__restrict__ itau, const double2 *st, const FpMod &m,
                                         double *srow) {
     const int k = threadIdx.x & 15;
     double x[16];
@@ -428,16 +431,16 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
     }
     // stage 0 (pairs c, c+128, twiddle Ti[1]) fused with the untwist: the table holds
     // tau^-1(r, c) for c < 128 and tau^-1(r, c) * Ti[1] for c >= 128
-    const double2 *tr = itau + r * 256;
+    const double *tr = itau + r * 256;
     double *rd = inter + r * 256;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-        const double2 ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
+        const double ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
         const double U = x[u], V = x[u + 8];
         // |f_mulmod| < 1.5 q: small primes skip the recentre (the column phase's first GS
         // stages keep |x| < 6 q); the large prime needs it for the next f_mulmod's range
-        const double a = f_mulmod(__dadd_rn(U, V), ta.x, ta.y, m.q);
-        const double b = f_mulmod(__dsub_rn(U, V), tb.x, tb.y, m.q);
+        const double a = f_mulmod(__dadd_rn(U, V), ta, __dmul_rn(ta, m.qinv), m.q);
+        const double b = f_mulmod(__dsub_rn(U, V), tb, __dmul_rn(tb, m.qinv), m.q);
         st_inter(rd + k + 16 * u, kBig ? f_center(a, m) : a);
         st_inter(rd + k + 16 * (u + 8), kBig ? f_center(b, m) : b);
     }
@@ -487,7 +490,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
 template <class Pro, class Epi, int CPP>
 __global__ void __launch_bounds__(kTh, 4)
     inv_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ itw,
-               const double2 *__restrict__ itwist, const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
+               const double *__restrict__ itwist, const double2 *__restrict__ ninv, const FpMod *__restrict__ fm,
                Pro pro, Epi epi) {
     constexpr int kT = kCl / CPP;
     extern __shared__ double smd[];
@@ -497,7 +500,7 @@ __global__ void __launch_bounds__(kTh, 4)
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = itw + (size_t)mi * kN;
-    const double2 *itau = itwist + (size_t)mi * kN;
+    const double *itau = itwist + (size_t)mi * kN;
     stage_table(st, T);
     __syncthreads();
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
@@ -655,7 +658,8 @@ template <class Pro, class Epi>
 inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi,
                         bool sample_major = false) {
     const long long n = (long long)n_limbs * B;
-    const double2 *tw = (const double2 *)c->d_twf, *twist = (const double2 *)c->d_twist;
+    const double2 *tw = (const double2 *)c->d_twf;
+    const double *twist = c->d_twist;
     const FpMod *fm = (const FpMod *)c->d_fmod;
     cudaError_t e;
     if constexpr (DiscardInter<Epi>::value) {
@@ -681,7 +685,8 @@ inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int 
 template <class Pro, class Epi>
 inline int launch16_inv(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int B, const Pro &pro, const Epi &epi) {
     const long long n = (long long)n_limbs * B;
-    const double2 *itw = (const double2 *)c->d_itwf, *itwist = (const double2 *)c->d_itwist;
+    const double2 *itw = (const double2 *)c->d_itwf;
+    const double *itwist = c->d_itwist;
     const double2 *ninv = (const double2 *)c->d_ninvf;
     const FpMod *fm = (const FpMod *)c->d_fmod;
     const cudaError_t e = launch_clustered(inv_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, itw, itwist,
