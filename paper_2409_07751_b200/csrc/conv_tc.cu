@@ -140,8 +140,8 @@ struct TargetC {  // per-target constants of the epilogue (shared memory, broadc
 // sits in the low mantissa bits after adding 1.5 * 2^52): X / q < 2^28, dropping
 // lo.lo costs < 2^-12 and the rounding of the estimate < 2^-20, so |X - t q| < q; the
 // remainder in wrapping 64-bit arithmetic, one conditional add.
-__device__ __forceinline__ uint64_t fold_reduce(const uint32_t (&C)[8], uint64_t q, double qi32) {
-    const uint32_t p8 = kPow2[0], p16 = kPow2[1], p24 = kPow2[2];
+__device__ __forceinline__ uint64_t fold_reduce(const uint32_t (&C)[8], uint64_t q, double qi32, uint32_t p8,
+                                                uint32_t p16, uint32_t p24) {
     const uint64_t lo = mad_wide(C[3], p24, mad_wide(C[2], p16, mad_wide(C[1], p8, C[0])));
     const uint64_t xh = mad_wide(C[6], p16, mad_wide(C[5], p8, (uint64_t)(C[4] + (uint32_t)(lo >> 32))));
     const uint32_t t = (uint32_t)__double_as_longlong(__fma_rn(ntt16::u2d(xh), qi32, ntt16::kMagic));
@@ -306,6 +306,8 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
         // ---------------------------------------------------------- epilogue
         const int q = warp & 3, slot = (warp - kEpiWarp0) >> 2;
         const int row = q * 32 + lane;
+        // read once: the "memory" clobbers of the TMEM waits would reload them per target
+        const uint32_t p8 = kPow2[0], p16 = kPow2[1], p24 = kPow2[2];
         int g = 0;
         for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             const long long e = tile * kTileM + row;
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
                     for (int w = 0; w < 4; ++w)
                         if (tt + w * kPerQuarter < nt) {
                             const TargetC tc = stc[t0 + tt + w * kPerQuarter];
-                            tc.out[e] = fold_reduce(C[w], tc.q, tc.qi32);
+                            tc.out[e] = fold_reduce(C[w], tc.q, tc.qi32, p8, p16, p24);
                         }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;");
