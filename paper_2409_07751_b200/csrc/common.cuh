@@ -222,6 +222,7 @@ struct hk_ctx {
     double2 *d_ninvf;      // [n_mod][2] {2^-16, 2^-16/q}, {2^-16 Ti[1], .../q} (inverse stage 0 fused)
     double2 *d_fmod;       // [n_mod] {q, 1/q} (every N)
     double *d_twist;       // [n_mod][256][256] w^(c (2 brv8(r) + 1 - 256)) as float64 (rows; w/q formed in-register)
+    double *d_twistq;      // [n_mod][256][256] the correctly rounded w / q of d_twist (read for large primes only)
     double *d_itwist;      // [n_mod][256][256] inverse twist
     ulonglong2 *d_n17;     // N = 2^17: [n_mod][4][2^16] radix-2 pre/post twists (ntt.cu)
     ulonglong2 *d_n17w;    // N = 2^17: [n_mod][2] {psi^(2^16), inverse}

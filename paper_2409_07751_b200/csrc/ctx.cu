@@ -243,13 +243,13 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
     // N = 2^16 uses root psi; N = 2^17 runs each half through the 2^16 kernel with root
     // psi^2 after one radix-2 stage and a pre-twist by psi^-+i (ntt.cu, ntt17_*).
     c->d_twf = c->d_itwf = c->d_ninvf = nullptr;
-    c->d_twist = c->d_itwist = nullptr;
+    c->d_twist = c->d_twistq = c->d_itwist = nullptr;
     c->d_n17 = nullptr;
     c->d_n17w = nullptr;
     if (c->log_n == 16 || c->log_n == 17) {
         const int H = 1 << 16;
         std::vector<double2> twf((size_t)nm * H), itwf((size_t)nm * H), ninvf(2 * (size_t)nm);
-        std::vector<double> tws((size_t)nm * H), itws((size_t)nm * H);
+        std::vector<double> tws((size_t)nm * H), twsq((size_t)nm * H), itws((size_t)nm * H);
         const uint64_t M2 = 2ull * H;
         for (int m = 0; m < nm; ++m) {
             const uint64_t q = c->mod_h[m];
@@ -280,6 +280,7 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
                     const uint64_t tv = col < 128 ? t : h_mulmod(t, t1, q);
                     const uint64_t itv = col < 128 ? it : h_mulmod(it, ti1, q);
                     tws[o] = (double)tv;
+                    twsq[o] = (double)tv / qd;
                     itws[o] = (double)itv;
                     t = h_mulmod(t, base, q);
                     it = h_mulmod(it, ibase, q);
@@ -290,6 +291,7 @@ int hk_ctx_create(const hk_params *pr, int32_t device, hk_ctx **out) {
         c->d_itwf = upload(itwf);
         c->d_ninvf = upload(ninvf);
         c->d_twist = upload(tws);
+        c->d_twistq = upload(twsq);
         c->d_itwist = upload(itws);
         if (c->log_n == 17) {
             // [m][4][2^16] Shoup pairs: psi^-i, psi^i (forward pre-twist of halves 0 / 1),
@@ -411,6 +413,7 @@ void hk_ctx_destroy(hk_ctx *c) {
     cudaFree(c->d_ninvf);
     cudaFree(c->d_fmod);
     cudaFree(c->d_twist);
+    cudaFree(c->d_twistq);
     cudaFree(c->d_itwist);
     cudaFree(c->d_n17);
     cudaFree(c->d_n17w);

@@ -242,12 +242,12 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, s & 1);
+            if (!(v & d)) ct_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, (s & 1) && s != 7);
     }
 #pragma unroll
     // no recentre for small primes: |x| < 13 q < 2^51 and the row phase starts with the
-    // twist multiply (f_mulmod, exact for |x| < 2^51); the large prime is centred (the twist's
-    // w / q is formed in-register, a 1.5 ulp estimate: |product| <= (1/2 + 1.5 |x| 2^-52) q)
+    // twist multiply (f_mulmod, exact for |x| < 2^51); the large prime leaves stage 7 with
+    // |x| <= 1.7 q < 2^51 as well (its twist reads the correctly rounded w / q companion)
     for (int v = 0; v < 16; ++v) st_inter(inter + (16 * k + v) * 256 + col, x[v]);
 }
 
@@ -259,11 +259,11 @@ __device__ __forceinline__ void fwd_cols(const Pro &pro, int l, long long P, dou
 // twiddles per row by one coalesced table element per coefficient.
 template <bool kBig, class Epi>
 __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, const double *inter, int r,
-                                        const double *__restrict__ tau, const double2 *st, const FpMod &m,
-                                        double *srow) {
+                                        const double *__restrict__ tau, const double *__restrict__ tauq,
+                                        const double2 *st, const FpMod &m, double *srow) {
     const int k = threadIdx.x & 15;
     const double *rd = inter + r * 256;
-    const double *tr = tau + r * 256;
+    const double *tr = tau + r * 256, *tq = tauq + r * 256;
     double x[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) x[u] = ld_inter(rd + k + 16 * u);
@@ -273,10 +273,14 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
     for (int u = 0; u < 8; ++u) {
         // 8-byte table entries: w / q is one DMUL here instead of 8 more bytes per coefficient
         // through L1 (the L1 / LSU path ran at 77 % beside an FP64 pipe at 70 %)
+        // (the large prime keeps the correctly rounded companion: its |x| <= 1.7 q multiplicand
+        // leaves no room for the 1.5-ulp in-register estimate)
         const double ta = __ldg(tr + k + 16 * u), tb = __ldg(tr + k + 16 * (u + 8));
-        const double a = f_mulmod(x[u], ta, __dmul_rn(ta, m.qinv), m.q);
-        const double b = f_mulmod(x[u + 8], tb, __dmul_rn(tb, m.qinv), m.q);
-        x[u] = __dadd_rn(a, b);  // |a|, |b| <= 1.1 q (0.7 q for the large prime): an uncentred stage
+        const double aq = kBig ? __ldg(tq + k + 16 * u) : __dmul_rn(ta, m.qinv);
+        const double bq = kBig ? __ldg(tq + k + 16 * (u + 8)) : __dmul_rn(tb, m.qinv);
+        const double a = f_mulmod(x[u], ta, aq, m.q);
+        const double b = f_mulmod(x[u + 8], tb, bq, m.q);
+        x[u] = __dadd_rn(a, b);  // |a|, |b| <= 1.1 q (0.72 q for the large prime): an uncentred stage
         x[u + 8] = __dsub_rn(a, b);
     }
 #pragma unroll
@@ -353,7 +357,8 @@ __device__ __forceinline__ void fwd_row(const Epi &epi, int l, long long P, cons
 template <class Pro, class Epi, int CPP>
 __global__ void __launch_bounds__(kTh, 4)
     fwd_kernel(uint64_t *__restrict__ inter_base, int limb0, int B, const double2 *__restrict__ tw,
-               const double *__restrict__ twist, const FpMod *__restrict__ fm, Pro pro, Epi epi, int smaj) {
+               const double *__restrict__ twist, const double *__restrict__ twistq, const FpMod *__restrict__ fm,
+               Pro pro, Epi epi, int smaj) {
     constexpr int kT = kCl / CPP;
     extern __shared__ double smd[];
     double2 *st = reinterpret_cast<double2 *>(smd + kTc * kRowPad);
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(kTh, 4)
     const int l = (int)(P / B), mi = limb0 + l;
     const FpMod m = fm[mi];
     const double2 *T = tw + (size_t)mi * kN;
-    const double *tau = twist + (size_t)mi * kN;
+    const double *tau = twist + (size_t)mi * kN, *tauq = twistq + (size_t)mi * kN;
     double *inter = reinterpret_cast<double *>(inter_base) + P * kN;
     const int rs = threadIdx.x >> 4;
     if (m.q < (double)kSmallPrime) {
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(kTh, 4)
         else __syncthreads();
         for (int t = 0; t < kT; ++t) {
             if (t) __syncwarp();
-            fwd_row<false>(epi, l, P, inter, (c * kT + t) * kTc + rs, tau, st, m, smd + rs * kRowPad);
+            fwd_row<false>(epi, l, P, inter, (c * kT + t) * kTc + rs, tau, tauq, st, m, smd + rs * kRowPad);
         }
     } else {
         for (int t = 0; t < kT; ++t) {
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(kTh, 4)
         else __syncthreads();
         for (int t = 0; t < kT; ++t) {
             if (t) __syncwarp();
-            fwd_row<true>(epi, l, P, inter, (c * kT + t) * kTc + rs, tau, st, m, smd + rs * kRowPad);
+            fwd_row<true>(epi, l, P, inter, (c * kT + t) * kTc + rs, tau, tauq, st, m, smd + rs * kRowPad);
         }
     }
 }
@@ -659,7 +664,7 @@ inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int 
                         bool sample_major = false) {
     const long long n = (long long)n_limbs * B;
     const double2 *tw = (const double2 *)c->d_twf;
-    const double *twist = c->d_twist;
+    const double *twist = c->d_twist, *twistq = c->d_twistq;
     const FpMod *fm = (const FpMod *)c->d_fmod;
     cudaError_t e;
     if constexpr (DiscardInter<Epi>::value) {
@@ -667,13 +672,13 @@ inline int launch16_fwd(hk_ctx *c, uint64_t *inter, int limb0, int n_limbs, int 
         // polynomials in flight (8 CTAs each) keep that buffer in L2 (profiles/r2_notes.md §8)
         static const int cpp = getenv("HK_CPP_EPI") ? atoi(getenv("HK_CPP_EPI")) : 8;  // A/B knob: 4 -> 29.66, 8 -> 29.76 c1 inf/s
         if (cpp == 8)
-            e = launch_clustered(fwd_kernel<Pro, Epi, 8>, 8, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi,
+            e = launch_clustered(fwd_kernel<Pro, Epi, 8>, 8, n, c->stream, inter, limb0, B, tw, twist, twistq, fm, pro, epi,
                                  sample_major ? n_limbs : 0);
         else
-            e = launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, fm, pro,
+            e = launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, twistq, fm, pro,
                                  epi, sample_major ? n_limbs : 0);
     } else {
-        e = launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, fm, pro, epi,
+        e = launch_clustered(fwd_kernel<Pro, Epi, kCpp>, kCpp, n, c->stream, inter, limb0, B, tw, twist, twistq, fm, pro, epi,
                              sample_major ? n_limbs : 0);
     }
     ++c->launches;
