@@ -327,15 +327,16 @@ def run_product(args):
 
 
 def _binding(prof: dict) -> dict:
-    keys = ("fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "issue_active_pct", "warps_active_pct")
+    keys = ("fp64_pipe_pct", "alu_pipe_pct", "fma_pipe_pct", "l1tex_throughput_pct", "issue_active_pct", "warps_active_pct",
+            "traffic_over_algorithmic")
     return {k: prof[k] for k in keys if k in prof} | ({"source": prof["_path"]} if prof else {})
 
 
 def kernel_rooflines(be, params, B, stream, reps: int = 5) -> dict:
     """CUDA-event timings of the two dominant primitives at the bench's launch
     shapes, against the HBM roofline on SURVEY §8(d)'s algorithmic bytes. Both
-    are compute-bound on this engine (FP64-pipe butterflies, integer-pipe
-    basis conversion), so `bound` names that pipe and `pipe` carries its ncu
+    are compute-bound on this engine (FP64-pipe butterflies, tensor-core basis
+    conversion with a CUDA-core epilogue), so `bound` names that pipe and `pipe` carries its ncu
     utilisation; `frac` stays the HBM fraction."""
     import torch
     eng = be.engine
