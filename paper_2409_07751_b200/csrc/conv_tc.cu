@@ -43,6 +43,11 @@
 // layout (ctx.cu: ConvTable::d_bmat, one 1 KiB row group per target) and copied
 // linearly into shared memory.
 //
+// Two instantiations: 16 source slots (K = 128 bytes per row, 4-deep TMA ring) and 32 slots
+// (K = 256 bytes, 2-deep ring) for digits of up to 31 primes (c3's alpha = 19: 9.85 -> 11.67
+// inferences/s against the IMAD kernel). When the B matrix of all targets does not fit the
+// shared memory left, the launcher splits the targets into groups (one launch each).
+//
 // Data movement: the source words of a 128-coefficient tile ([slot][128] u64,
 // 1 KiB contiguous per slot in HBM) arrive by TMA bulk copies
 // (cp.async.bulk + mbarrier complete_tx) into a 4-deep ring, issued by one
@@ -55,19 +60,17 @@
 namespace {
 
 constexpr int kTileM = 128;      // coefficients per tile (TMEM lanes)
-constexpr int kKBytes = 128;     // 16 source slots x 8 bytes
+constexpr int kKBytes = 128;     // 16 source slots x 8 bytes (kSlots = 16; 256 for kSlots = 32: c3's 19-prime digits)
 constexpr int kRowsPerTarget = 8;
 constexpr int kChunkTargets = 32;  // N <= 256 per MMA
-constexpr int kRawStages = 4;      // TMA ring depth (tiles)
-constexpr int kTileBytes = kTileM * kKBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
 // shared-memory matrix descriptor: no swizzle, K-major
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-    const uint64_t lbo = 128 >> 4, sbo = 1024 >> 4;
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo_bytes) {
+    const uint64_t lbo = 128 >> 4, sbo = sbo_bytes >> 4;
     return (uint64_t)((saddr >> 4) & 0x3FFF) | (lbo << 16) | (sbo << 32) | (1ull << 46);
 }
 
@@ -165,15 +168,24 @@ __device__ __forceinline__ uint64_t fold_reduce(const uint32_t (&C)[8], uint64_t
 // previous phase).
 constexpr int kXformWarp0 = 1, kXformWarps = 4, kMmaWarp = 5, kEpiWarp0 = 6;
 
-template <int kEpiWarps>
+// kSlots = 16 (K = 128 bytes per row, 4-deep raw ring) or 32 (K = 256 bytes, 2-deep ring: digits
+// of up to 31 primes, e.g. c3's alpha = 19); d_off: position of target 0 of this launch in
+// the conversion's target list (the launcher splits a conversion whose B matrix does not fit
+// shared memory into target groups).
+template <int kEpiWarps, int kSlots>
 __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
     k_conv_tc(const uint64_t *__restrict__ src, int n_src, const uint8_t *__restrict__ bmat,
               const int32_t *__restrict__ dst_mod, int n_dst, uint64_t *__restrict__ dst, int mode, int l, int n_q,
-              long long BN, const double2 *__restrict__ fmod, const double *__restrict__ src_invd, int has_u) {
+              long long BN, const double2 *__restrict__ fmod, const double *__restrict__ src_invd, int has_u,
+              int d_off) {
+    constexpr int kKBytes = kSlots * 8;                   // bytes per operand row
+    constexpr int kTileBytes = kTileM * kKBytes;          // one A tile / one raw tile
+    constexpr int kRawStages = kSlots == 16 ? 4 : 2;      // TMA ring depth (tiles)
+    constexpr uint32_t kSbo = 8 * kKBytes;                // bytes between 8-row groups
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sa = smem;                                   // A: 2 x 16 KiB (UMMA layout)
-    uint8_t *sraw = sa + 2 * kTileBytes;                  // raw ring: kRawStages x [16][128] u64
-    uint8_t *sb = sraw + kRawStages * kTileBytes;         // B: (n_dst + 1) x 1 KiB (one pad group)
+    uint8_t *sa = smem;                                   // A: 2 tiles (UMMA layout)
+    uint8_t *sraw = sa + 2 * kTileBytes;                  // raw ring: kRawStages x [kSlots][128] u64
+    uint8_t *sb = sraw + kRawStages * kTileBytes;         // B: (n_dst + 1) row groups (one pad group)
     const int b_bytes = n_dst * kRowsPerTarget * kKBytes;
     TargetC *stc = reinterpret_cast<TargetC *>(sb + b_bytes + kRowsPerTarget * kKBytes);  // [n_dst]
     __shared__ __align__(8) uint64_t bars[2 * kRawStages + 8];
@@ -191,7 +203,7 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
         for (int d = tid; d < n_dst; d += kThreadsWs) {
             const int m = dst_mod[d];
             const double2 f = fmod[m];
-            const int row = mode == 0 ? (m <= l ? m : l + 1 + m - n_q) : d;
+            const int row = mode == 0 ? (m <= l ? m : l + 1 + m - n_q) : d_off + d;
             stc[d] = TargetC{(uint64_t)f.x, f.y * 4294967296.0, dst + (long long)row * BN};
         }
     }
@@ -251,28 +263,34 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
             const int rs = i % kRawStages;
             mbar_wait(RAW_FULL(rs), (i / kRawStages) & 1);
             const uint64_t *raw = reinterpret_cast<const uint64_t *>(sraw + rs * kTileBytes) + r;
-            uint64_t v[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = j < n_src ? raw[j * kTileM] : 0;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(RAW_EMPTY(rs));
-            uint64_t u = 0;
-            if (has_u) {
-                double frac = 0.0;  // sum_i v_i / m_i, fixed order, no contraction (as k_conv and the oracle)
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (j < n_src) frac = __dadd_rn(frac, __dmul_rn(ntt16::u2d(v[j]), src_invd[j]));
-                u = (uint64_t)floor(__dadd_rn(frac, 0.5));
-            }
             const int s = i & 1;
-            mbar_wait(A_EMPTY(s), ((i >> 1) & 1) ^ 1);
-            uint8_t *row = sa + s * kTileBytes + (r >> 3) * 1024 + (r & 7) * 16;
+            uint8_t *row = sa + s * kTileBytes + (r >> 3) * kSbo + (r & 7) * 16;
+            double frac = 0.0;  // sum_i v_i / m_i, fixed order, no contraction (as k_conv and the oracle)
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<uint4 *>(row + c * 128) = make_uint4(
-                    (uint32_t)v[2 * c], (uint32_t)(v[2 * c] >> 32), (uint32_t)v[2 * c + 1], (uint32_t)(v[2 * c + 1] >> 32));
+            for (int h = 0; h < kSlots / 16; ++h) {  // 16 source slots at a time (register budget)
+                uint64_t v[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 16 * h + j < n_src ? raw[(16 * h + j) * kTileM] : 0;
+                if (h == kSlots / 16 - 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(RAW_EMPTY(rs));
+                }
+                if (has_u) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (16 * h + j < n_src) frac = __dadd_rn(frac, __dmul_rn(ntt16::u2d(v[j]), src_invd[16 * h + j]));
+                }
+                if (h == 0) mbar_wait(A_EMPTY(s), ((i >> 1) & 1) ^ 1);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    *reinterpret_cast<uint4 *>(row + (8 * h + c) * 128) =
+                        make_uint4((uint32_t)v[2 * c], (uint32_t)(v[2 * c] >> 32), (uint32_t)v[2 * c + 1],
+                                   (uint32_t)(v[2 * c + 1] >> 32));
+            }
             // the overflow count takes source slot n_src (zero so far)
-            if (has_u) *reinterpret_cast<uint64_t *>(row + (n_src >> 1) * 128 + (n_src & 1) * 8) = u;
+            if (has_u)
+                *reinterpret_cast<uint64_t *>(row + (n_src >> 1) * 128 + (n_src & 1) * 8) =
+                    (uint64_t)floor(__dadd_rn(frac, 0.5));
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A visible to the tensor core
             __syncwarp();
             if (lane == 0) mbar_arrive(A_FULL(s));
@@ -294,9 +312,9 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
                     // N is a multiple of 16: an odd target count also multiplies the next row
                     // group (the next target or the zero pad group), whose columns nobody reads
                     const uint32_t idesc = umma_idesc((nt * kRowsPerTarget + 15) & ~15);
-                    const uint32_t b0 = smem_u32(sb + t0 * kRowsPerTarget * kKBytes);
+                    const uint32_t b0 = smem_u32(sb + t0 * kRowsPerTarget * kKBytes);  // one row group per target
                     for (int k = 0; k < ksteps; ++k)
-                        mma_i8(tmem + tb * 256, umma_desc(a0 + k * 256), umma_desc(b0 + k * 256), idesc, k);
+                        mma_i8(tmem + tb * 256, umma_desc(a0 + k * 256, kSbo), umma_desc(b0 + k * 256, kSbo), idesc, k);
                     umma_commit(T_FULL(tb));
                 }
                 umma_commit(A_EMPTY(s));  // every MMA reading this A buffer has completed
@@ -348,38 +366,54 @@ __global__ void __launch_bounds__((kEpiWarp0 + kEpiWarps) * 32, 1)
 
 }  // namespace
 
-// Usable for this table and launch: prescaled sources, at most 16 source slots
-// (the overflow count of a centred conversion takes one), a built B matrix, whole
+// Usable for this table and launch: prescaled sources, at most 32 source slots (the
+// overflow count of a centred conversion takes one), a built B matrix, whole
 // 128-coefficient tiles.
 bool conv_tc_ok(const hk_ctx *c, const ConvTable &T, int n_dst, long long BN, int prescaled) {
     static const bool off = getenv("HK_CONV_TC") && atoi(getenv("HK_CONV_TC")) == 0;  // A/B knob
-    return !off && prescaled && T.d_bmat && T.n_src + (T.d_neg_m ? 1 : 0) <= 16 && n_dst <= T.n_dst &&
+    static const bool wide = !(getenv("HK_CONV_TC32") && atoi(getenv("HK_CONV_TC32")) == 0);  // A/B knob: 32-slot kernel
+    const int slots = T.n_src + (T.d_neg_m ? 1 : 0);
+    return !off && prescaled && T.d_bmat && (slots <= 16 || (wide && slots <= 32)) && n_dst <= T.n_dst &&
            BN % kTileM == 0 && c->log_n >= 7;
+}
+
+template <int kSlots>
+static int conv_tc_launch_slots(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l,
+                                long long BN, int n_dst) {
+    constexpr int kKB = kSlots * 8, kStages = kSlots == 16 ? 4 : 2;
+    const size_t fixed = (size_t)(2 + kStages) * kTileM * kKB + 64;
+    const size_t per_target = (size_t)kRowsPerTarget * kKB + sizeof(TargetC);
+    // targets per launch: the B matrix (one row group per target + one pad group) must fit
+    const int cap = (int)((227 * 1024 - fixed - (size_t)kRowsPerTarget * kKB) / per_target);
+    if (cap < 1) return hk_fail(c, HK_E_ARG, "conv_tc: no room for the B matrix");
+    const int groups = (n_dst + cap - 1) / cap, per = (n_dst + groups - 1) / groups;
+    static const int epi = getenv("HK_CONV_EPI") ? atoi(getenv("HK_CONV_EPI")) : 16;  // A/B knob: 8 / 12 / 16 warps
+    const long long tiles = BN / kTileM;
+    const unsigned grid = (unsigned)std::min<long long>(tiles, (long long)c->n_sm);  // one CTA per SM (512 TMEM columns)
+    for (int d0 = 0; d0 < n_dst; d0 += per) {
+        const int nd = std::min(per, n_dst - d0);
+        const size_t smem = fixed + (size_t)(nd + 1) * kRowsPerTarget * kKB + (size_t)nd * sizeof(TargetC);
+#define HK_CONV_TC(EW)                                                                                            \
+    {                                                                                                             \
+        static size_t attr = 0;                                                                                   \
+        if (smem > attr) {                                                                                        \
+            cudaFuncSetAttribute(k_conv_tc<EW, kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            attr = smem;                                                                                          \
+        }                                                                                                         \
+        k_conv_tc<EW, kSlots><<<grid, (kEpiWarp0 + EW) * 32, smem, c->stream>>>(                                  \
+            src, T.n_src, T.d_bmat + (size_t)d0 * kRowsPerTarget * kKB, T.d_dst_mod + d0, nd, dst, mode, l,       \
+            c->n_q, BN, c->d_fmod, T.d_src_invd, T.d_neg_m ? 1 : 0, d0);                                          \
+    }
+        if (epi == 16) HK_CONV_TC(16) else if (epi == 8) HK_CONV_TC(8) else HK_CONV_TC(12)
+#undef HK_CONV_TC
+        ++c->launches;
+        HK_LAUNCH_CHECK(c, "basis conversion (tensor cores)");
+    }
+    return HK_OK;
 }
 
 int conv_tc_launch(hk_ctx *c, const ConvTable &T, const uint64_t *src, uint64_t *dst, int mode, int l, long long BN,
                    int n_dst) {
-    const size_t smem = (size_t)(2 + kRawStages) * kTileBytes + (size_t)(n_dst + 1) * kRowsPerTarget * kKBytes +
-                        n_dst * 24 + 64;
-    if (smem > 227 * 1024) return hk_fail(c, HK_E_ARG, "conv_tc: %d targets exceed shared memory", n_dst);
-    static const int epi = getenv("HK_CONV_EPI") ? atoi(getenv("HK_CONV_EPI")) : 16;  // A/B knob: 8 / 12 / 16 warps
-    const long long tiles = BN / kTileM;
-    const unsigned grid = (unsigned)std::min<long long>(tiles, (long long)c->n_sm);  // one CTA per SM (512 TMEM columns)
-#define HK_CONV_TC(EW)                                                                                           \
-    {                                                                                                            \
-        static size_t attr = 0;                                                                                  \
-        if (smem > attr) {                                                                                       \
-            cudaFuncSetAttribute(k_conv_tc<EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-            attr = smem;                                                                                         \
-        }                                                                                                        \
-        k_conv_tc<EW><<<grid, (kEpiWarp0 + EW) * 32, smem, c->stream>>>(src, T.n_src, T.d_bmat, T.d_dst_mod,     \
-                                                                       n_dst, dst, mode, l, c->n_q, BN,         \
-                                                                       c->d_fmod, T.d_src_invd,                 \
-                                                                       T.d_neg_m ? 1 : 0);                      \
-    }
-    if (epi == 16) HK_CONV_TC(16) else if (epi == 8) HK_CONV_TC(8) else HK_CONV_TC(12)
-#undef HK_CONV_TC
-    ++c->launches;
-    HK_LAUNCH_CHECK(c, "basis conversion (tensor cores)");
-    return HK_OK;
+    if (T.n_src + (T.d_neg_m ? 1 : 0) <= 16) return conv_tc_launch_slots<16>(c, T, src, dst, mode, l, BN, n_dst);
+    return conv_tc_launch_slots<32>(c, T, src, dst, mode, l, BN, n_dst);
 }

@@ -127,16 +127,18 @@ static ConvTable make_conv(const std::vector<uint64_t> &mod, const std::vector<i
     bool below50 = true;  // 7-byte residues and constants (every generated prime is < 2^50)
     for (int m : src) below50 = below50 && mod[m] < (1ull << 50);
     for (int m : dst) below50 = below50 && mod[m] < (1ull << 50);
-    if (below50 && src.size() + (exact ? 1 : 0) <= 16) {
-        std::vector<uint8_t> b(dst.size() * 8 * 128, 0);
+    const size_t slots = src.size() + (exact ? 1 : 0);
+    if (below50 && slots <= 32) {
+        const size_t kb = slots <= 16 ? 128 : 256, sbo = 8 * kb;  // bytes per row, per 8-row group (conv_tc.cu)
+        std::vector<uint8_t> b(dst.size() * sbo, 0);
         for (size_t d = 0; d < dst.size(); ++d) {
             const uint64_t qt = mod[dst[d]];
-            for (size_t i = 0; i < src.size() + (exact ? 1 : 0); ++i) {
+            for (size_t i = 0; i < slots; ++i) {
                 uint64_t cst = i < src.size() ? hat[d * src.size() + i] : negm[d];
                 for (int a = 0; a < 8; ++a) {
                     for (int bb = 0; bb < 8; ++bb) {
                         const size_t n = d * 8 + bb, kk = i * 8 + a;
-                        b[(n / 8) * 1024 + (kk / 16) * 128 + (n % 8) * 16 + kk % 16] = (uint8_t)(cst >> (8 * bb));
+                        b[(n / 8) * sbo + (kk / 16) * 128 + (n % 8) * 16 + kk % 16] = (uint8_t)(cst >> (8 * bb));
                     }
                     cst = h_mulmod(cst, 256, qt);
                 }
