@@ -153,9 +153,11 @@ __device__ __forceinline__ void ct_f(double &x, double &y, double2 w, const FpMo
         y = f_center(y, m);
     }
 }
-// Gentleman-Sande butterfly. The sum is recentred only when `center` (small primes
-// recentre at stages 6, 4 and 2 only: |x| stays below 6q < 2^50, inside the exact
-// range of f_mulmod and f_center); the large prime recentres every stage.
+// Gentleman-Sande butterfly. The sum is recentred only when `center`: small primes
+// (q < 2^47) recentre at stages 5 and 2 of each phase only. From inputs |x| <= 1.5 q the
+// sums double per stage (3 q, 6 q, 12 q at stage 5: every difference stays below
+// 2^51 > 16 q, the exact range of f_mulmod), a recentred stage returns to q / 2 and the
+// products are below 0.75 q throughout.
 // The large prime recentres sum and product after every second stage (`cen_big`, the
 // odd stages): from |x| <= q/2 an uncentred stage leaves |x| <= q, so the next stage's
 // difference stays below 2 q < 2^51.
@@ -419,7 +421,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 128 >> sp;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m, !(sp & 1), sp & 1);
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], st[tw_idx(sp, k, v)], m, sp == 5, sp & 1);
     }
     __syncwarp();
 #pragma unroll
@@ -432,7 +434,7 @@ __device__ __forceinline__ void inv_row(const Pro &pro, int l, long long P, doub
         const int d = 8 >> sp;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m, !(sp & 1), sp & 1);
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], st[(1 << sp) + (u >> (4 - sp))], m, sp == 2, sp & 1);
     }
     // stage 0 (pairs c, c+128, twiddle Ti[1]) fused with the untwist: the table holds
     // tau^-1(r, c) for c < 128 and tau^-1(r, c) * Ti[1] for c >= 128
@@ -464,7 +466,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
         const int d = 128 >> s;
 #pragma unroll
         for (int v = 0; v < 16; ++v)
-            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, !(s & 1), s & 1);
+            if (!(v & d)) gs_f<kBig>(x[v], x[v + d], T[tw_idx(s, k, v)], m, s == 5, s & 1);
     }
 #pragma unroll
     for (int v = 0; v < 16; ++v) sm[(16 * k + v) * kTc + c] = x[v];
@@ -476,7 +478,7 @@ __device__ __forceinline__ void inv_cols(const Epi &epi, int l, long long P, con
         const int d = 8 >> s;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m, !(s & 1), s & 1);
+            if (!(u & d)) gs_f<kBig>(x[u], x[u + d], T[(1 << s) + (u >> (4 - s))], m, s == 2, s & 1);
     }
     // stage 0 (twiddle Ti[1]) fused with the N^-1 scaling: niw = N^-1 * Ti[1]
 #pragma unroll

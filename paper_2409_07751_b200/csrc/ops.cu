@@ -1270,9 +1270,9 @@ static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, K
     if (key.level < l) return hk_fail(c, HK_E_NOKEY, "key for element %u serves level %d < %d", g, key.level, l);
     const int krows = key.level + 1 + c->n_p;
     const long long BN = (long long)B * c->n;
-    // samples per thread: each key pair is read once per bb samples (bb = 1 / 2 /
-    // 4: 24.3 / 25.1 / 25.5 c1 inf/s, profiles/r2_notes.md)
-    static const int bb_max = getenv("HK_KEYIP_BB") ? atoi(getenv("HK_KEYIP_BB")) : 4;  // A/B knob
+    // samples per thread: each key pair is read (and converted) once per bb samples (bb = 1 / 2 /
+    // 4: 24.3 / 25.1 / 25.5 c1 inf/s at the start of round 2, profiles/r2_notes.md)
+    static const int bb_max = getenv("HK_KEYIP_BB") ? atoi(getenv("HK_KEYIP_BB")) : 8;  // A/B knob: 4 -> 24.87, 8 -> 24.47 ms per relinearisation
     const int bb = B % 8 == 0 && bb_max >= 8 ? 8 : B % 4 == 0 && bb_max >= 4 ? 4 : B % 2 == 0 && bb_max >= 2 ? 2 : 1;
     const int ipt = std::min(256, c->n);
     const dim3 ipg((unsigned)((c->n / ipt) * (B / bb)), (unsigned)ne);
