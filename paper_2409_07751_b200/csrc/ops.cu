@@ -1272,8 +1272,8 @@ static int ks_ip(hk_ctx *c, const uint64_t *d, int l, int B, const KsBufs &kb, K
     const long long BN = (long long)B * c->n;
     // samples per thread: each key pair is read (and converted) once per bb samples (bb = 1 / 2 /
     // 4: 24.3 / 25.1 / 25.5 c1 inf/s at the start of round 2, profiles/r2_notes.md)
-    static const int bb_max = getenv("HK_KEYIP_BB") ? atoi(getenv("HK_KEYIP_BB")) : 8;  // A/B knob: 4 -> 24.87, 8 -> 24.47 ms per relinearisation
-    const int bb = B % 8 == 0 && bb_max >= 8 ? 8 : B % 4 == 0 && bb_max >= 4 ? 4 : B % 2 == 0 && bb_max >= 2 ? 2 : 1;
+    static const int bb_max = getenv("HK_KEYIP_BB") ? atoi(getenv("HK_KEYIP_BB")) : 16;  // A/B knob: 4 / 8 / 16 -> 24.87 / 24.47 (24.80) / 24.57 ms per relinearisation
+    const int bb = B % 16 == 0 && bb_max >= 16 ? 16 : B % 8 == 0 && bb_max >= 8 ? 8 : B % 4 == 0 && bb_max >= 4 ? 4 : B % 2 == 0 && bb_max >= 2 ? 2 : 1;
     const int ipt = std::min(256, c->n);
     const dim3 ipg((unsigned)((c->n / ipt) * (B / bb)), (unsigned)ne);
 #define HK_KEY_IP(ND)                                                                                          \

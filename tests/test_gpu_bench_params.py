@@ -73,6 +73,14 @@ def test_c1_params_ops_bitexact(gpu_lib, level):
     _op_suite(g, o, level, np.random.default_rng(level))
 
 
+def test_c1_params_ops_bitexact_batch16(gpu_lib):
+    """The same chain at B = 16: the key inner product's 16-samples-per-thread
+    walk (the bench's B = 128 takes it), every product variant and rotation."""
+    p = kan_params(36)
+    g, o = _pair(p, 36)
+    _op_suite(g, o, 36, np.random.default_rng(16), batch=16)
+
+
 def test_c1_params_bsgs_grouped_mac_bitexact(gpu_lib):
     """bsgs_matvec at B = 8: device diagonals, grouped MAC (2B >= 16) with its
     fused rescale, lazy-ModDown giant steps."""
